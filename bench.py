@@ -1,0 +1,450 @@
+"""Benchmark: ternary-linear tokens/s at M=1 decode on BASELINE.json config 1.
+
+Workload (BASELINE.json configs[1]): the TL1 FFN block of a Llama-3-8B-shaped
+layer at M=1 -- gate and up (K=4096 -> N=14336) on one freshly quantised
+activation vector, down (K=14336 -> N=4096) on another, exactly the per-layer
+work of the reference bench's token pass (pkg/src/ternpack/bench.py:138-153):
+per-token absmax int8 quantisation + (implicit) TL1 LUT + exact int32 GEMV +
+rescale.  One "step" = one token through that block.
+
+  value   device-resident throughput: K steps captured in one CUDA graph,
+          inputs already in HBM, weights rotated over 6 distinct copies
+          (265 MB > 126 MB L2) so every step streams from HBM.
+  e2e     the same steps through the public Python API (quantize_activations
+          + gemv_parallel) with pinned HOST inputs and the float64 results
+          read back to the host inside the timed region.
+  roofline  the TL1 GEMV kernel timed alone (graph of back-to-back launches
+          over the rotating copies, CUDA events): algorithmic bytes per
+          launch / mean launch time vs MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline  the C port of the reference byte-table CPU kernels
+          (oracle/c/tern_oracle.c) on this host, bounded sample.
+
+``--impl reference`` times that CPU port alone on the same workload (rank 0).
+Multi-GPU (torchrun, N>1): tensor parallel -- gate/up column-parallel, down
+row-parallel with an NCCL all-reduce of the int32 partial accumulators.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, I = 4096, 14336
+NCOPY = 6
+NX = 64
+METRIC = "ternary-linear tokens/s (M=1 decode)"
+
+
+def tl1_bytes(rows, cols):
+    return rows * (-(-(-(-cols // 2) * 2 // 2) // 2))
+
+
+def algo_bytes_gemv(rows, cols, m=1):
+    # packed weights (reference TL1 size) + int8 activations + fp32 outputs
+    return tl1_bytes(rows, cols) + m * cols + 4 * m * rows
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU port of the reference (oracle/c) -- baseline and --impl reference
+# ---------------------------------------------------------------------------
+
+def cpu_token_runner(gate, up, down):
+    """Returns f(xh, xi) running one reference-style TL1 FFN token on the CPU port."""
+    from oracle import c_oracle as CO
+    g1, g2 = H // 2, I // 2
+
+    def run(xh, xi, threads):
+        qh, _ = CO.quantize(xh, 2)
+        lut_h = CO.lut_tl1(qh, g1)
+        CO.gemv_tl1(gate, lut_h, threads)
+        CO.gemv_tl1(up, lut_h, threads)
+        qi, _ = CO.quantize(xi, 2)
+        lut_i = CO.lut_tl1(qi, g2)
+        CO.gemv_tl1(down, lut_i, threads)
+
+    return run
+
+
+def cpu_baseline(gate, up, down, budget_s=12.0):
+    from oracle import c_oracle as CO
+    run = cpu_token_runner(gate, up, down)
+    rng = np.random.default_rng(7)
+    xh = rng.standard_normal(H).astype(np.float32)
+    xi = rng.standard_normal(I).astype(np.float32)
+    best = None
+    ncpu = os.cpu_count() or 1
+    for threads in sorted({1, CO.max_threads(), ncpu}):
+        run(xh, xi, threads)  # warm
+        n, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < budget_s / 2:
+            run(xh, xi, threads)
+            n += 1
+        tps = n / (time.perf_counter() - t0)
+        if best is None or tps > best[0]:
+            best = (tps, threads, n)
+    return {"value": round(best[0], 3), "unit": "tokens/s", "cores": best[1], "kind": "port",
+            "sample": f"{best[2]} TL1 FFN tokens (gate+up+down, quantise+LUT+byte-table gather) "
+                      f"on {best[1]} thread(s); best of threads in {{1, {ncpu}}}; host has {ncpu} CPUs"}
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+def make_tl1(tb, torch, rows, cols, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = torch.randn(rows, cols, generator=g, device="cuda", dtype=torch.float32) * 0.02
+    m = tb.ternarize_weights(w, rows, cols)
+    del w
+    return tb.encode_tl1(m)
+
+
+def shard_rows(p, tb, torch, r0, r1):
+    """Column-parallel shard: rows [r0, r1) of a packed TL1 matrix (byte slice)."""
+    return tb.PackedTL1(rows=r1 - r0, cols=p.cols, padded_cols=p.padded_cols,
+                        data=p.data[r0:r1].contiguous(), scale=p.scale, trusted=True)
+
+
+def shard_cols(tb, torch, m, k0, k1):
+    """Row-parallel shard: K-slice [k0, k1) (k0 even -> pairs stay whole)."""
+    sub = tb.TernaryMatrix(m.rows, k1 - k0, m.values[:, k0:k1].contiguous(), m.scale,
+                           _checked=True)
+    return tb.encode_tl1(sub)
+
+
+def run_gpu(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_16144_b200 as tb
+    from paper_2410_16144_b200.core import quantize_into
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    tp = world
+    # ---- weights: NCOPY distinct seeded copies, TP-sharded
+    plans = []
+    gate_full_bytes = 0
+    for c in range(NCOPY):
+        gen = torch.Generator(device="cuda").manual_seed(1000 + c)
+        mats = {}
+        for name, rows, cols in (("gate", I, H), ("up", I, H), ("down", H, I)):
+            w = torch.randn(rows, cols, generator=gen, device="cuda", dtype=torch.float32) * 0.02
+            m = tb.ternarize_weights(w, rows, cols)
+            del w
+            if tp == 1:
+                p = tb.encode_tl1(m)
+            elif name in ("gate", "up"):
+                per = rows // tp
+                full = tb.encode_tl1(m)
+                p = shard_rows(full, tb, torch, rank * per, (rank + 1) * per)
+            else:
+                per = cols // tp
+                p = shard_cols(tb, torch, m, rank * per, (rank + 1) * per)
+            p.tiled()
+            mats[name] = p
+        if c == 0:
+            gate_full_bytes = mats["gate"].data.numel()
+            host_copy = {k: v.data.cpu().numpy() for k, v in mats.items()} if tp == 1 else None
+        plans.append({
+            "gate": tb.GemvPlan(mats["gate"], out_dtype=torch.float32),
+            "up": tb.GemvPlan(mats["up"], out_dtype=torch.float32),
+            "down": tb.GemvPlan(mats["down"], out_dtype=(torch.float32 if tp == 1 else None),
+                                want_acc=(tp > 1)),
+            "mats": mats,
+        })
+        for p in mats.values():
+            p._cache.pop("ref_dropped", None)
+    torch.cuda.synchronize()
+
+    gen = torch.Generator(device="cuda").manual_seed(77)
+    XH = torch.randn(NX, H, generator=gen, device="cuda", dtype=torch.float32)
+    XI = torch.randn(NX, I, generator=gen, device="cuda", dtype=torch.float32)
+    qh = torch.empty((1, H), dtype=torch.int8, device=dev)
+    qi = torch.empty((1, I), dtype=torch.int8, device=dev)
+    sh = torch.empty(1, dtype=torch.float64, device=dev)
+    si = torch.empty(1, dtype=torch.float64, device=dev)
+    out_down = torch.empty((1, H), dtype=torch.float32, device=dev)
+    kloc = I // tp
+
+    def step(i):
+        pl = plans[i % NCOPY]
+        quantize_into(XH[i % NX: i % NX + 1], qh, sh)
+        pl["gate"].run(qh, sh)
+        pl["up"].run(qh, sh)
+        if tp == 1:
+            quantize_into(XI[i % NX: i % NX + 1], qi, si)
+            pl["down"].run(qi, si)
+        else:
+            # row-parallel down: every rank quantises the full vector (same
+            # per-token scale as the reference) and contracts its K-slice
+            quantize_into(XI[i % NX: i % NX + 1], qi, si)
+            pl["down"].run(qi[:, rank * kloc:(rank + 1) * kloc], si)
+            dist.all_reduce(pl["down"].acc, op=dist.ReduceOp.SUM)
+            tb.core.L.check(tb.core.L.load().tb_scale_outputs(
+                pl["down"].acc.data_ptr(), 1, H, float(pl["mats"]["down"].scale), si.data_ptr(),
+                None, out_down.data_ptr(), tb.core.L.stream_ptr()), "scale")
+
+    launches_per_step = 5 + (1 if tp > 1 else 0)
+
+    # ---- warm-up (eager, also configures kernel attributes before capture)
+    for i in range(max(args.warmup, NCOPY)):
+        step(i)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region: K steps in one CUDA graph
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            for i in range(args.steps):
+                step(i)
+    torch.cuda.synchronize()
+    graph.replay()  # untimed replay (first replay uploads the graph)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        e0.record()
+        graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+
+    # ---- roofline: the TL1 GEMV alone, back-to-back over the rotating copies
+    R = 8 * NCOPY
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g2, stream=s):
+            for i in range(R):
+                plans[i % NCOPY]["gate"].run(qh, sh)
+    g2.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    g2.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    gemv_ms = e0.elapsed_time(e1) / R
+    rows_loc = I // tp
+    gemv_bytes = algo_bytes_gemv(rows_loc, H)
+    peak, peak_kind = measured_peak()
+    achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
+
+    result = {
+        "metric": METRIC, "value": round(1000.0 / ms_per_step, 2), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "i8",
+        "data": "synthetic (seeded N(0,0.02) latent weights -> absmean ternary, N(0,1) activations)",
+        "config": {"workload": "cfg1: TL1 FFN block, gate/up 4096->14336 + down 14336->4096, M=1",
+                   "format": "TL1", "tokens_per_step": 1,
+                   "l2": f"{NCOPY} rotating weight copies ({NCOPY * 3 * gate_full_bytes / 1e6:.0f} MB "
+                         "packed per rank) > 126 MB L2",
+                   "parallelism": "tp1" if tp == 1 else f"tp{tp} (col-parallel gate/up, "
+                                  "row-parallel down + NCCL int32 all-reduce)"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": "tgemv_kernel<TL1,1> (gate, 14336x4096)",
+                     "bytes_per_launch": gemv_bytes, "launch_us": round(gemv_ms * 1e3, 3),
+                     "peak_kind": f"{peak_kind} hbm_gbs (copy)"},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+
+    # ---- e2e through the public API with host buffers
+    if rank == 0 and not args.no_e2e and tp == 1:
+        K = tb.KernelKind
+        xh_h = torch.randn(NX, H).pin_memory()
+        xi_h = torch.randn(NX, I).pin_memory()
+        n_e2e = max(10, min(args.steps, 200))
+
+        def e2e_step(i):
+            mats = plans[i % NCOPY]["mats"]
+            qa_h = tb.quantize_activations(xh_h[i % NX], pad_to=2)
+            rg = tb.gemv_parallel(K.TL1, mats["gate"], qa_h)
+            ru = tb.gemv_parallel(K.TL1, mats["up"], qa_h)
+            qa_i = tb.quantize_activations(xi_h[i % NX], pad_to=2)
+            rd = tb.gemv_parallel(K.TL1, mats["down"], qa_i)
+            return rg.output.cpu(), ru.output.cpu(), rd.output.cpu()
+
+        for i in range(3):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(n_e2e):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / n_e2e
+        result["e2e"] = {"value": round(1.0 / e2e_s, 2), "unit": "tokens/s",
+                         "h2d_bytes_per_step": (H + I) * 4,
+                         "d2h_bytes_per_step": (2 * I + H) * 8,
+                         "steps": n_e2e,
+                         "path": "tb.quantize_activations + tb.gemv_parallel(TL1) x3, pinned host "
+                                 "f32 in, float64 GemvResult.output to host"}
+
+    if rank == 0 and not args.no_cpu_baseline and tp == 1:
+        result["cpu_baseline"] = cpu_baseline(host_copy["gate"], host_copy["up"],
+                                              host_copy["down"], budget_s=args.cpu_budget)
+    return result
+
+
+def run_reference(args):
+    """--impl reference: the C port of the reference CPU kernels, all host threads."""
+    import torch  # noqa: F401  (weights are generated with the same packer)
+    from oracle import c_oracle as CO
+    from oracle import ternpack_oracle as O
+
+    rng = np.random.default_rng(1000)
+    mats = {}
+    for name, rows, cols in (("gate", I, H), ("up", I, H), ("down", H, I)):
+        v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)  # ternary draw (bench.py:102)
+        mats[name] = O.encode_tl1(v)
+    run = cpu_token_runner(mats["gate"], mats["up"], mats["down"])
+    threads = os.cpu_count() or 1
+    xs = np.random.default_rng(7)
+    XH = xs.standard_normal((NX, H)).astype(np.float32)
+    XI = xs.standard_normal((NX, I)).astype(np.float32)
+    for i in range(args.warmup):
+        run(XH[i % NX], XI[i % NX], threads)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        run(XH[i % NX], XI[i % NX], threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = round(1.0 / dt, 3)
+    return {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i8",
+        "data": "synthetic", "config": {"workload": "cfg1: TL1 FFN block, gate/up 4096->14336 + "
+                                                    "down 14336->4096, M=1", "format": "TL1"},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} timed TL1 FFN tokens, {threads} OpenMP threads, "
+                                   f"C port of the reference byte-table kernels (oracle/c); "
+                                   f"reference package itself is not shipped to the box"},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    res = run_gpu(args, rank, world)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

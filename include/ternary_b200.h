@@ -1,0 +1,166 @@
+/*
+ * ternary_b200.h -- C ABI of the B200-native ternary BitLinear hot path.
+ *
+ * Drop-in boundary for the reference package ``ternpack`` (bitnet.cpp,
+ * arXiv 2410.16144).  The reference's native boundary is its five numba
+ * kernels (pkg/src/ternpack/_fast.py:25-147) plus the NumPy arithmetic of
+ * core.py / packing.py / lut.py that surrounds them; each entry point below
+ * names the reference interface it replaces.
+ *
+ * Conventions:
+ *   - every buffer is a DEVICE pointer owned by the caller (plain pointers and
+ *     sizes; no torch types), except where a name says `host`;
+ *   - `stream` is a cudaStream_t passed as void*; nothing synchronises
+ *     implicitly; kernels are reentrant and keep no global mutable state;
+ *   - every function returns a tb_status (0 = OK); tb_strerror() maps it to
+ *     text; data-dependent errors (invalid codes, non-finite input) are
+ *     reported through caller-provided device int32 flags so the call stays
+ *     asynchronous -- the Python mirror turns them into the reference's
+ *     ValueError messages.
+ *
+ * Packed-weight layouts:
+ *   reference layout   -- byte-identical to ternpack's PackedI2S.data,
+ *                         PackedTL1.data, PackedTL2.index_data/sign_data
+ *                         (packing.py:77-197): row-major, rows byte aligned;
+ *   tiled layout       -- the GEMV layout: 32-row tiles, each row split into
+ *                         16-byte chunks, stored [tile][chunk][row][16 B]
+ *                         (TL2 sign bits alongside as [tile][chunk][row][4 B]);
+ *                         it is a pure permutation of 16-byte granules of the
+ *                         reference layout plus zero-weight padding.
+ */
+#ifndef TERNARY_B200_H
+#define TERNARY_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum tb_status {
+  TB_OK = 0,
+  TB_ERR_ARGUMENT = 1,     /* bad size / null pointer / unsupported format    */
+  TB_ERR_CUDA = 2,         /* a CUDA runtime call failed                      */
+  TB_ERR_UNSUPPORTED = 3,  /* shape outside what this build handles           */
+} tb_status;
+
+typedef enum tb_format { TB_I2S = 1, TB_TL1 = 2, TB_TL2 = 3 } tb_format;
+
+const char *tb_strerror(int status);
+int tb_abi_version(void);            /* bumps on any signature change          */
+int tb_device_sm_count(int device);  /* cached multiProcessorCount             */
+
+/* ---------------------------------------------------------------- core.py */
+
+/* quantize_activations (core.py:116-134), M tokens at once: x[M][ldx] (K valid
+ * entries per row), q[M][ldq] int8 with zero padding up to ldq, scale[M] f64.
+ * Bit-exact with the reference: float64 absmax, scale = amax/127 (1 when 0),
+ * q = clip(trunc(x/scale + copysign(.5, x/scale)), -127, 127).
+ * nonfinite_flag (device int32, may be NULL) is set to 1 on NaN/Inf input.   */
+int tb_quantize_f32(const float *x, int64_t M, int64_t K, int64_t ldx,
+                    int8_t *q, int64_t ldq, double *scale,
+                    int32_t *nonfinite_flag, void *stream);
+int tb_quantize_f64(const double *x, int64_t M, int64_t K, int64_t ldx,
+                    int8_t *q, int64_t ldq, double *scale,
+                    int32_t *nonfinite_flag, void *stream);
+
+/* ternarize_weights (core.py:104-113), split in two so the scale is bit-exact
+ * with NumPy's pairwise np.mean: the host enumerates the pairwise tree down to
+ * `nsub` subtrees (offsets/lengths in device int64 arrays), the device sums
+ * |w| over each subtree in NumPy's exact order, the host combines the partial
+ * sums up the tree and divides by n; then tb_ternarize_apply writes
+ * q = clip(rha(w / scale), -1, 1).                                          */
+int tb_abs_pairwise_sums_f32(const float *w, const int64_t *sub_off,
+                             const int64_t *sub_len, int64_t nsub,
+                             double *sums, int32_t *nonfinite_flag, void *stream);
+int tb_abs_pairwise_sums_f64(const double *w, const int64_t *sub_off,
+                             const int64_t *sub_len, int64_t nsub,
+                             double *sums, int32_t *nonfinite_flag, void *stream);
+int tb_ternarize_apply_f32(const float *w, int64_t n, double scale, int8_t *q,
+                           void *stream);
+int tb_ternarize_apply_f64(const double *w, int64_t n, double scale, int8_t *q,
+                           void *stream);
+
+/* output = float64(acc) * w_scale * a_scale[m]  (core.py:99-101); either
+ * output may be NULL.                                                      */
+int tb_scale_outputs(const int32_t *acc, int64_t M, int64_t N, double w_scale,
+                     const double *a_scale, double *out64, float *out32,
+                     void *stream);
+
+/* ------------------------------------------------------------ packing.py */
+
+/* Reference-layout sizes (packing.py:42-53). */
+int64_t tb_ref_row_bytes(int fmt, int64_t cols);       /* I2S/TL1/TL2 index */
+int64_t tb_ref_sign_row_bytes(int64_t cols);           /* TL2 sign plane    */
+
+/* encode_i2s / encode_tl1 / encode_tl2 (packing.py:200-262): int8 ternary
+ * values [rows][cols] -> reference-layout bytes.  `sign` only for TL2.     */
+int tb_encode(int fmt, const int8_t *values, int64_t rows, int64_t cols,
+              uint8_t *out, uint8_t *sign, void *stream);
+/* decode_* (packing.py:209-277).  bad_flag (device int32) is set to 1 on an
+ * invalid code (I2S 0b11 / TL1 nibble > 8 / TL2 index > 13), 2 on a TL2
+ * non-canonical zero.                                                       */
+int tb_decode(int fmt, const uint8_t *data, const uint8_t *sign, int64_t rows,
+              int64_t cols, int8_t *values, int32_t *bad_flag, void *stream);
+/* validate() (packing.py:98-107, 135-141, 176-186): first_bad[0] = first row
+ * with an invalid code, first_bad[1] = first row with a TL2 non-canonical
+ * zero; both must be initialised to INT32_MAX by the caller.               */
+int tb_validate(int fmt, const uint8_t *data, const uint8_t *sign, int64_t rows,
+                int64_t cols, int32_t *first_bad, void *stream);
+
+/* Tiled GEMV layout: sizes, repack from the reference layout, and inverse. */
+int64_t tb_tiled_chunks(int fmt, int64_t cols);          /* 16-B chunks/row */
+int64_t tb_tiled_bytes(int fmt, int64_t rows, int64_t cols);
+int64_t tb_tiled_sign_bytes(int fmt, int64_t rows, int64_t cols);
+int tb_repack(int fmt, const uint8_t *ref, const uint8_t *ref_sign, int64_t rows,
+              int64_t cols, uint8_t *tiled, uint8_t *tiled_sign, void *stream);
+int tb_unrepack(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
+                int64_t rows, int64_t cols, uint8_t *ref, uint8_t *ref_sign,
+                void *stream);
+
+/* ---------------------------------------------------------------- lut.py */
+
+/* build_lut_tl1 / build_lut_tl2 (lut.py:72-84): act int8[len] zero-extended
+ * to groups*2 (groups*3); entries int16 [groups][9] ([groups][14]).         */
+int tb_build_lut(int fmt, const int8_t *act, int64_t len, int64_t groups,
+                 int16_t *entries, void *stream);
+
+/* ------------------------------------------------------------ kernels.py */
+
+/* Decode GEMV / small-M GEMM on the tiled layout: replaces gemv_i2s /
+ * gemv_tl1 / gemv_tl2 / gemv_parallel (kernels.py:86-157, 189-268) and the
+ * numba byte-table gathers (_fast.py:25-95).  act int8 [M][ld_act] with
+ * `act_len` valid entries per token (zero beyond), M <= 16.  Results are the
+ * exact int32 dot products for every M; outputs (each may be NULL):
+ *   acc_out[M][N] int32, out64[M][N] = f64(acc)*w_scale*a_scale[m],
+ *   out32[M][N] = (float)out64.
+ * The workspace (tb_gemv_workspace_bytes) must be zeroed once before first
+ * use; every call leaves it zeroed again (self-cleaning), so one workspace
+ * serves any number of back-to-back calls on ONE stream.                    */
+int64_t tb_gemv_workspace_bytes(int fmt, int64_t rows, int64_t cols);
+int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
+            int64_t rows, int64_t cols, const int8_t *act, int64_t M,
+            int64_t ld_act, int64_t act_len, const double *a_scale,
+            double w_scale, void *workspace, int32_t *acc_out, double *out64,
+            float *out32, void *stream);
+
+/* LUT-driven TL1/TL2 GEMV for a caller-supplied LUT (gemv_tl1/gemv_tl2 with
+ * an explicit LutTL1/LutTL2, kernels.py:109-157): lut int16 [groups][9|14];
+ * every lookup reads the given entries, so corrupted tables behave exactly
+ * as in the reference (runtime.py:191-196 fault injection).  acc_out must be
+ * zero-initialised; a_scale is a single host scalar here.                 */
+int tb_gemv_lut(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
+                int64_t rows, int64_t cols, const int16_t *lut, int64_t groups,
+                int32_t *acc_out, void *stream);
+
+/* gemv_ref_int32 (kernels.py:59-63) on unpacked int8 values [rows][cols];
+ * gemv_f32_ref (kernels.py:66-72) on the dequantised fp32 matrix.          */
+int tb_gemv_ref_int32(const int8_t *values, int64_t rows, int64_t cols,
+                      const int8_t *act, int32_t *acc_out, void *stream);
+int tb_gemv_f32_ref(const int8_t *values, int64_t rows, int64_t cols,
+                    float w_scale, const float *x, float *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TERNARY_B200_H */

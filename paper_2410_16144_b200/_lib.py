@@ -1,0 +1,103 @@
+"""ctypes binding of libternary_b200.so (the C ABI in include/ternary_b200.h).
+
+The product path has no fallback: if the library is missing or no CUDA
+device is present, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libternary_b200.so"
+
+I2S, TL1, TL2 = 1, 2, 3
+
+_p = C.c_void_p
+_i64 = C.c_int64
+_i32 = C.c_int
+_f64 = C.c_double
+_f32 = C.c_float
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "tb_strerror": (C.c_char_p, [_i32]),
+    "tb_abi_version": (_i32, []),
+    "tb_device_sm_count": (_i32, [_i32]),
+    "tb_quantize_f32": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _p]),
+    "tb_quantize_f64": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _p]),
+    "tb_abs_pairwise_sums_f32": (_i32, [_p, _p, _p, _i64, _p, _p, _p]),
+    "tb_abs_pairwise_sums_f64": (_i32, [_p, _p, _p, _i64, _p, _p, _p]),
+    "tb_ternarize_apply_f32": (_i32, [_p, _i64, _f64, _p, _p]),
+    "tb_ternarize_apply_f64": (_i32, [_p, _i64, _f64, _p, _p]),
+    "tb_scale_outputs": (_i32, [_p, _i64, _i64, _f64, _p, _p, _p, _p]),
+    "tb_ref_row_bytes": (_i64, [_i32, _i64]),
+    "tb_ref_sign_row_bytes": (_i64, [_i64]),
+    "tb_encode": (_i32, [_i32, _p, _i64, _i64, _p, _p, _p]),
+    "tb_decode": (_i32, [_i32, _p, _p, _i64, _i64, _p, _p, _p]),
+    "tb_validate": (_i32, [_i32, _p, _p, _i64, _i64, _p, _p]),
+    "tb_tiled_chunks": (_i64, [_i32, _i64]),
+    "tb_tiled_bytes": (_i64, [_i32, _i64, _i64]),
+    "tb_tiled_sign_bytes": (_i64, [_i32, _i64, _i64]),
+    "tb_repack": (_i32, [_i32, _p, _p, _i64, _i64, _p, _p, _p]),
+    "tb_unrepack": (_i32, [_i32, _p, _p, _i64, _i64, _p, _p, _p]),
+    "tb_build_lut": (_i32, [_i32, _p, _i64, _i64, _p, _p]),
+    "tb_gemv_workspace_bytes": (_i64, [_i32, _i64, _i64]),
+    "tb_gemv": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _i64, _i64, _p, _f64, _p, _p, _p,
+                       _p, _p]),
+    "tb_gemv_lut": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _p, _p]),
+    "tb_gemv_ref_int32": (_i32, [_p, _i64, _i64, _p, _p, _p]),
+    "tb_gemv_f32_ref": (_i32, [_p, _i64, _i64, _f32, _p, _p, _p]),
+    "tb_gemm_i8": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _i64, _p, _f64, _p, _p, _p,
+                          _p, _p]),
+    "tb_gemm_workspace_bytes": (_i64, [_i32, _i64, _i64, _i64]),
+}
+
+_lib = None
+
+
+class ExtensionMissing(RuntimeError):
+    pass
+
+
+def load(path: os.PathLike | None = None):
+    """Load (once) and return the CDLL with typed entry points."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise ExtensionMissing(
+            f"{p} not found: build the CUDA extension first "
+            "(python -m paper_2410_16144_b200.build or __graft_entry__.build())")
+    lib = C.CDLL(str(p))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name, None)
+        if fn is None:
+            continue
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def declared_symbols():
+    return list(_SIGS)
+
+
+def check(status: int, what: str = "") -> None:
+    if status != 0:
+        msg = load().tb_strerror(status).decode()
+        raise RuntimeError(f"ternary_b200 {what} failed: {msg} (status {status})")
+
+
+def ptr(t) -> int | None:
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

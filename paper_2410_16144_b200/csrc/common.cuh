@@ -1,0 +1,127 @@
+// Shared device helpers for the sm_100a ternary kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ternary_b200.h"
+
+#define TB_CHECK_LAUNCH()                                   \
+  do {                                                      \
+    cudaError_t _e = cudaGetLastError();                    \
+    if (_e != cudaSuccess) return TB_ERR_CUDA;              \
+  } while (0)
+
+namespace tb {
+
+constexpr int kRowTile = 32;     // rows per tile == lanes per warp
+constexpr int kChunkBytes = 16;  // bytes of one row's stream per chunk
+constexpr int kTileChunkBytes = kRowTile * kChunkBytes;  // 512 B
+constexpr int kTileSignBytes = kRowTile * 4;             // 128 B (TL2)
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t pad_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+__host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// reference row bytes (packing.py:42-53)
+__host__ __device__ inline int64_t ref_row_bytes(int fmt, int64_t cols) {
+  if (fmt == TB_I2S) return pad_up(cols, 4) / 4;
+  if (fmt == TB_TL1) return ceil_div(pad_up(cols, 2) / 2, 2);
+  return pad_up(cols, 6) / 6;  // TL2 index plane
+}
+__host__ __device__ inline int64_t ref_sign_row_bytes(int64_t cols) {
+  return ceil_div(pad_up(cols, 6) / 3, 8);
+}
+// weights covered by one 16-byte chunk
+__host__ __device__ inline int chunk_weights(int fmt) { return fmt == TB_TL2 ? 96 : 64; }
+// byte used to pad a row's stream (a run of zero weights)
+__host__ __device__ inline uint8_t zero_byte(int fmt) {
+  return fmt == TB_I2S ? 0x55 : (fmt == TB_TL1 ? 0x44 : 0x00);
+}
+
+// ---------------------------------------------------------------- PTX bits
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 1-D bulk async copy global -> shared, completion via mbarrier tx count.
+// (cp.async.bulk: SASS UBLKCP; src/dst 16-B aligned, size multiple of 16.)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ void red_add_s32(int32_t *p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// dot of 4 unsigned bytes (codes) with 4 signed bytes (activations)
+__device__ __forceinline__ int dp4a_us(uint32_t codes, uint32_t act, int acc) {
+  int r;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(codes), "r"(act), "r"(acc));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t lop3_sel(uint32_t p, uint32_t q, uint32_t m) {
+  // (p & ~m) | (q & m)
+  return (p & ~m) | (q & m);
+}
+
+// Round half away from zero in float64 exactly as core.py:24-27.
+__device__ __forceinline__ double rha(double v) { return trunc(v + copysign(0.5, v)); }
+
+int sm_count_cached();
+
+}  // namespace tb

@@ -1,0 +1,232 @@
+"""GEMV entry points (mirrors ternpack.kernels, pkg/src/ternpack/kernels.py).
+
+Every integer kind returns the exact int32 accumulators, bit-identical to
+the reference oracle, plus float64 outputs acc * w_scale * a_scale.
+
+  gemv_ref_int32  kernels.py:59-63   -> tb_gemv_ref_int32 (unpacked int8)
+  gemv_f32_ref    kernels.py:66-72   -> tb_gemv_f32_ref (dequantised fp32)
+  gemv_i2s        kernels.py:86-94   -> tb_gemv on the tiled I2_S layout
+  gemv_tl1        kernels.py:109-126 -> tb_gemv_lut with the caller's LUT
+  gemv_tl2        kernels.py:140-157 -> tb_gemv_lut with the caller's LUT
+  gemv_parallel   kernels.py:189-268 -> tb_gemv (LUT implicit) or tb_gemv_lut
+                                        when the caller passes a LUT
+
+``thread_count`` keeps the reference's validation and meaning of "results
+are identical for every value"; on the GPU the row partition is the CTA
+grid, so it does not change the launch.  Activations may be a batch
+(QuantizedActivations with data [M, K], M <= 16) -- each token is an
+independent reference GEMV; outputs are then [M, rows].
+"""
+
+from __future__ import annotations
+
+import enum
+
+import torch
+
+from . import _lib as L
+from .core import GemvResult, QuantizedActivations, TernaryMatrix, make_result, to_device
+from .lut import LutTL1, LutTL2, build_lut_tl1, build_lut_tl2  # noqa: F401
+from .packing import PackedI2S, PackedTL1, PackedTL2
+
+__all__ = ["KernelKind", "WIDEN_GROUPS", "gemv_ref_int32", "gemv_f32_ref", "gemv_i2s",
+           "gemv_tl1", "gemv_tl2", "gemv_parallel", "GemvPlan", "KERNEL_PAD"]
+
+WIDEN_GROUPS = 64  # kernels.py:34
+MAX_DECODE_TOKENS = 16
+
+
+class KernelKind(enum.Enum):
+    REF_INT32 = "ref_int32"
+    REF_F32 = "ref_f32"
+    I2_S = "i2s"
+    TL1 = "tl1"
+    TL2 = "tl2"
+
+
+KERNEL_PAD = {KernelKind.REF_INT32: 1, KernelKind.I2_S: 4, KernelKind.TL1: 2,
+              KernelKind.TL2: 3}  # runtime.py:32-37
+
+
+def _check_activation_cover(a: QuantizedActivations, cols: int) -> None:
+    """kernels.py:45-49."""
+    if len(a) < cols:
+        raise ValueError("dimension mismatch: activations shorter than matrix cols")
+    if len(a) == cols or (a._trusted and a.original_len <= cols):
+        return  # our quantiser zero-pads by construction: no device read needed
+    if bool((a.data[..., cols:] != 0).any()):
+        raise ValueError("dimension mismatch: nonzero activations beyond matrix cols")
+
+
+def _out_shape(a: QuantizedActivations, rows: int):
+    return (rows,) if a.data.dim() == 1 else (a.tokens, rows)
+
+
+def gemv_ref_int32(m: TernaryMatrix, a: QuantizedActivations) -> GemvResult:
+    _check_activation_cover(a, m.cols)
+    lib = L.load()
+    acts = a.data.reshape(a.tokens, -1)
+    acc = torch.empty((a.tokens, m.rows), dtype=torch.int32, device=m.values.device)
+    for t in range(a.tokens):
+        L.check(lib.tb_gemv_ref_int32(L.ptr(m.values), m.rows, m.cols, L.ptr(acts[t]),
+                                      L.ptr(acc[t]), L.stream_ptr()), "gemv_ref_int32")
+    acc = acc.reshape(_out_shape(a, m.rows))
+    return make_result(acc, m.scale, a.scales)
+
+
+def gemv_f32_ref(m: TernaryMatrix, x) -> GemvResult:
+    xd = to_device(x, torch.float32).reshape(-1).contiguous()
+    if xd.numel() != m.cols:
+        raise ValueError("dimension mismatch")
+    out = torch.empty(m.rows, dtype=torch.float32, device=xd.device)
+    L.check(L.load().tb_gemv_f32_ref(L.ptr(m.values), m.rows, m.cols, float(m.scale),
+                                     L.ptr(xd), L.ptr(out), L.stream_ptr()), "gemv_f32_ref")
+    return GemvResult(accumulators=None, output=out.to(torch.float64))
+
+
+def _tiled_gemv(p, a: QuantizedActivations, want_out64: bool = True) -> GemvResult:
+    """Decode GEMV through the C ABI (LUT implicit; M <= 16 tokens per launch)."""
+    lib = L.load()
+    main, sign = p.tiled()
+    acts = a.data.reshape(a.tokens, -1)
+    M, K = acts.shape
+    dev = main.device
+    acc = torch.empty((M, p.rows), dtype=torch.int32, device=dev)
+    out = torch.empty((M, p.rows), dtype=torch.float64, device=dev) if want_out64 else None
+    ws = p.workspace()
+    s = L.stream_ptr()
+    for t0 in range(0, M, MAX_DECODE_TOKENS):
+        t1 = min(M, t0 + MAX_DECODE_TOKENS)
+        L.check(lib.tb_gemv(p.FMT, L.ptr(main), L.ptr(sign), p.rows, p.cols, L.ptr(acts[t0]),
+                            t1 - t0, acts.stride(0), K, L.ptr(a.scales[t0:t1]), float(p.scale),
+                            L.ptr(ws), L.ptr(acc[t0]), L.ptr(out[t0] if out is not None else None),
+                            None, s), "gemv")
+    shape = _out_shape(a, p.rows)
+    return GemvResult(accumulators=acc.reshape(shape),
+                      output=out.reshape(shape) if out is not None else None)
+
+
+def _lut_gemv(p, lut, a_scale) -> GemvResult:
+    lib = L.load()
+    main, sign = p.tiled()
+    acc = torch.zeros(p.rows, dtype=torch.int32, device=main.device)
+    L.check(lib.tb_gemv_lut(p.FMT, L.ptr(main), L.ptr(sign), p.rows, p.cols, L.ptr(lut.entries),
+                            lut.groups, L.ptr(acc), L.stream_ptr()), "gemv_lut")
+    return make_result(acc, p.scale, a_scale)
+
+
+def _widened_sum(vals: torch.Tensor) -> torch.Tensor:
+    """int16 partials folded every 64 groups, asserting |partial| <= 32767
+    (kernels.py:160-173); evaluated on the device."""
+    rows, groups = vals.shape
+    blocks = -(-groups // WIDEN_GROUPS)
+    padded = torch.zeros((rows, blocks * WIDEN_GROUPS), dtype=torch.int32, device=vals.device)
+    padded[:, :groups] = vals.to(torch.int32)
+    running = torch.cumsum(padded.reshape(rows, blocks, WIDEN_GROUPS), dim=2, dtype=torch.int32)
+    peak = int(running.abs().max()) if running.numel() else 0
+    assert peak <= 32767, f"16-bit partial sum overflow: |{peak}| > 32767"
+    return running[:, :, -1].sum(dim=1, dtype=torch.int32)
+
+
+def gemv_i2s(p: PackedI2S, a: QuantizedActivations) -> GemvResult:
+    """2-bit kernel: weights decoded on the fly, never materialised."""
+    if not p.trusted:
+        p.validate()
+    _check_activation_cover(a, p.cols)
+    return _tiled_gemv(p, a)
+
+
+def gemv_tl1(p: PackedTL1, lut: LutTL1, a_scale: float, *, checked: bool = False) -> GemvResult:
+    """Pair-index kernel: one 9-entry table lookup per weight pair."""
+    if not p.trusted:
+        p.validate()
+    if lut.groups != p.groups:
+        raise ValueError("group-count mismatch")
+    if checked:
+        nib = torch.empty((p.rows, 2 * p.bytes_per_row), dtype=torch.int64, device=p.data.device)
+        nib[:, 0::2] = (p.data & 15).to(torch.int64)
+        nib[:, 1::2] = (p.data >> 4).to(torch.int64)
+        g = torch.arange(p.groups, device=nib.device)
+        vals = lut.entries[g.unsqueeze(0), nib[:, : p.groups]]
+        return make_result(_widened_sum(vals), p.scale, a_scale)
+    return _lut_gemv(p, lut, a_scale)
+
+
+def gemv_tl2(p: PackedTL2, lut: LutTL2, a_scale: float, *, checked: bool = False) -> GemvResult:
+    """Sign + index kernel: 14-entry canonical table, sign applied on lookup."""
+    if not p.trusted:
+        p.validate()
+    if lut.groups != p.groups:
+        raise ValueError("group-count mismatch")
+    if checked:
+        idx = p.data_nibbles().to(torch.int64)
+        sg = p.data_signs().bool()
+        g = torch.arange(p.groups, device=idx.device)
+        vals = lut.entries[g.unsqueeze(0), idx]
+        vals = torch.where(sg, -vals, vals)
+        return make_result(_widened_sum(vals), p.scale, a_scale)
+    return _lut_gemv(p, lut, a_scale)
+
+
+def gemv_parallel(kernel: KernelKind, weights, a, thread_count: int = 1,
+                  lut=None) -> GemvResult:
+    """kernels.py:189-268 with the GPU grid as the row partition."""
+    if thread_count < 1:
+        raise ValueError("thread_count must be >= 1")
+    if kernel is KernelKind.REF_F32:
+        return gemv_f32_ref(weights, a)
+    if kernel is KernelKind.REF_INT32:
+        return gemv_ref_int32(weights, a)
+    if not weights.trusted:
+        weights.validate()
+    _check_activation_cover(a, weights.cols)
+    if kernel is KernelKind.I2_S:
+        return _tiled_gemv(weights, a)
+    if kernel in (KernelKind.TL1, KernelKind.TL2):
+        if lut is None:
+            return _tiled_gemv(weights, a)  # LUT implicit (exact identity, lut.py docstring)
+        if lut.groups != weights.groups:
+            raise ValueError("group-count mismatch")
+        return _lut_gemv(weights, lut, a.scales[:1])
+    raise ValueError(f"unsupported kernel kind: {kernel}")
+
+
+class GemvPlan:
+    """Pre-allocated, capture-safe decode GEMV for one packed matrix.
+
+    Holds the tiled weights, a self-cleaning workspace and output buffers so
+    that ``run`` is a single C-ABI launch with no allocation or host sync --
+    the form the stack runner and bench capture into CUDA graphs.
+    """
+
+    def __init__(self, packed, max_tokens: int = 1, out_dtype=torch.float32,
+                 want_acc: bool = False, stream=None):
+        if not 1 <= max_tokens <= MAX_DECODE_TOKENS:
+            raise ValueError(f"max_tokens must be in [1, {MAX_DECODE_TOKENS}]")
+        self.p = packed
+        self.main, self.sign = packed.tiled()
+        dev = self.main.device
+        self.ws = torch.zeros(
+            L.load().tb_gemv_workspace_bytes(packed.FMT, packed.rows, packed.cols) // 4,
+            dtype=torch.int32, device=dev)
+        self.out32 = self.out64 = None
+        if out_dtype == torch.float32:
+            self.out32 = torch.empty((max_tokens, packed.rows), dtype=torch.float32, device=dev)
+        elif out_dtype == torch.float64:
+            self.out64 = torch.empty((max_tokens, packed.rows), dtype=torch.float64, device=dev)
+        self.acc = (torch.empty((max_tokens, packed.rows), dtype=torch.int32, device=dev)
+                    if want_acc else None)
+        self.max_tokens = max_tokens
+        self._lib = L.load()
+
+    def run(self, act: torch.Tensor, scales: torch.Tensor, stream_ptr: int | None = None):
+        M, K = act.shape
+        st = self._lib.tb_gemv(self.p.FMT, self.main.data_ptr(),
+                               self.sign.data_ptr() if self.sign is not None else None,
+                               self.p.rows, self.p.cols, act.data_ptr(), M, act.stride(0), K,
+                               scales.data_ptr(), float(self.p.scale), self.ws.data_ptr(),
+                               L.ptr(self.acc), L.ptr(self.out64), L.ptr(self.out32),
+                               stream_ptr if stream_ptr is not None else L.stream_ptr())
+        if st:
+            L.check(st, "gemv")
+        return self.out32 if self.out32 is not None else self.out64

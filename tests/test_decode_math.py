@@ -1,0 +1,95 @@
+"""CPU emulation of the GEMV kernel's SIMD-within-a-register decode.
+
+gemv.cu decodes packed bytes with 32-bit word arithmetic (no per-byte
+branches).  These tests replay exactly that arithmetic in NumPy uint32 over
+every possible input byte/nibble/sign combination and compare the recovered
+weights with the oracle's decoders, so a wrong constant is caught before any
+GPU time is spent.
+"""
+
+import itertools
+
+import numpy as np
+
+from oracle import ternpack_oracle as O
+
+U = np.uint32
+
+
+def prmt_sign_replicate(x):
+    """prmt(x, 0, 0xBA98): byte b = 0xFF if bit 7 of byte b of x else 0x00."""
+    out = U(0)
+    for b in range(4):
+        if (int(x) >> (8 * b + 7)) & 1:
+            out |= U(0xFF << (8 * b))
+    return out
+
+
+def bytes_of(w):
+    return [(int(w) >> (8 * b)) & 0xFF for b in range(4)]
+
+
+def test_i2s_slot_masks():
+    # byte b of (W & (3 << 2s)) / 4^s = code of weight 4b+s of this word
+    for byte in range(256):
+        W = U(byte * 0x01010101)
+        for s in range(4):
+            x = int(W & U(0x03030303 << (2 * s)))
+            for b in range(4):
+                assert ((x >> (8 * b)) & 0xFF) >> (2 * s) == (byte >> (2 * s)) & 3
+
+
+def test_tl1_word_decode_all_nibble_pairs():
+    for n0, n1, n2, n3 in itertools.product(range(9), repeat=4):
+        # four bytes, each with a low nibble (pair 2b) and a high nibble (pair 2b+1)
+        lo_n = [n0, n1, n2, n3]
+        hi_n = [n3, n2, n1, n0]
+        W = U(sum((lo_n[b] | (hi_n[b] << 4)) << (8 * b) for b in range(4)))
+        lo = W & U(0x0F0F0F0F)
+        hi = (W >> U(4)) & U(0x0F0F0F0F)
+        for x, nib in ((lo, lo_n), (hi, hi_n)):
+            q = ((x * U(11)) >> U(5)) & U(0x03030303)
+            r = x - U(3) * q
+            for b in range(4):
+                assert bytes_of(q)[b] == nib[b] // 3
+                assert bytes_of(r)[b] == nib[b] % 3
+
+
+def test_tl2_sign_masks_all_bytes():
+    for S in range(256):
+        mlo = prmt_sign_replicate(U((S & 0x55) * 0x02082080 & 0xFFFFFFFF))
+        mhi = prmt_sign_replicate(U((S & 0xAA) * 0x01041040 & 0xFFFFFFFF))
+        for b in range(4):
+            assert bytes_of(mlo)[b] == (0xFF if (S >> (2 * b)) & 1 else 0)
+            assert bytes_of(mhi)[b] == (0xFF if (S >> (2 * b + 1)) & 1 else 0)
+
+
+def test_tl2_triple_decode_all_codes():
+    # every (sign, index) incl. the canonical codes; 4 triples per word lane
+    codes = [(0, 0)] + [(s, i) for s in (0, 1) for i in range(1, 14)]
+    for quad in itertools.product(codes, repeat=2):
+        lanes = [quad[0], quad[1], quad[1], quad[0]]
+        x = U(sum(idx << (8 * b) for b, (_, idx) in enumerate(lanes)))
+        msk = U(sum((0xFF if s else 0) << (8 * b) for b, (s, _) in enumerate(lanes)))
+        P = (x + U(0x0D0D0D0D)) & U(0xFFFFFFFF)
+        Q = (U(0x0D0D0D0D) - x) & U(0xFFFFFFFF)
+        d = (P & ~msk) | (Q & msk)
+        c0 = (((d * U(7) + U(0x07070707)) & U(0xFFFFFFFF)) >> U(6)) & U(0x03030303)
+        r = (d - U(9) * c0) & U(0xFFFFFFFF)
+        c1 = (((r * U(11)) & U(0xFFFFFFFF)) >> U(5)) & U(0x03030303)
+        c2 = (r - U(3) * c1) & U(0xFFFFFFFF)
+        for b, (s, idx) in enumerate(lanes):
+            ip = np.array([[idx]], np.uint8)
+            sp = np.array([[s]], np.uint8)
+            want = O.decode_tl2(ip, sp, 3)[0] if not (s and idx == 0) else None
+            if want is None:
+                continue
+            got = [bytes_of(c0)[b] - 1, bytes_of(c1)[b] - 1, bytes_of(c2)[b] - 1]
+            assert got == want.tolist(), (s, idx)
+
+
+def test_activation_permutation_covers_chunk():
+    # word 4i+s holds a[16i+4j+s] (I2_S/TL1); word 6i+s holds a[24i+6j+s] (TL2)
+    for width, G in ((64, 4), (96, 6)):
+        seen = sorted(i * 4 * G + s + G * j for i in range(4) for s in range(G) for j in range(4))
+        assert seen == list(range(width))

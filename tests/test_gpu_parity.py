@@ -1,0 +1,368 @@
+"""GPU parity: the CUDA path against the reference's golden fixtures and the oracle.
+
+Bit-exact for int8 activations, float64 scales, packed bytes, int32
+accumulators and float64 outputs; the fp32 output of the fused path is
+checked against the float64 reference with rel. tolerance 1e-5 (north star).
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import ternpack_oracle as O  # noqa: E402
+from workloads import LARGE_CASES, activations, latent_weights, sha  # noqa: E402
+
+GOLD = Path(__file__).parent / "golden"
+SMALL = np.load(GOLD / "small.npz")
+LARGE = json.loads((GOLD / "large.json").read_text())
+
+
+@pytest.fixture(scope="module")
+def tb():
+    import paper_2410_16144_b200 as tb
+    return tb
+
+
+def split(flat, offs):
+    return [flat[offs[i]:offs[i + 1]] for i in range(len(offs) - 1)]
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+# ----------------------------------------------------------------- core
+
+def test_quantize_golden(tb):
+    xs = split(SMALL["q_x"], SMALL["q_xoff"])
+    for pad in (1, 2, 3, 4):
+        want = split(SMALL[f"q_data_p{pad}"], SMALL[f"q_doff_p{pad}"])
+        for x, d, s in zip(xs, want, SMALL[f"q_scale_p{pad}"]):
+            qa = tb.quantize_activations(x, pad_to=pad)
+            assert np.array_equal(host(qa.data), d)
+            assert qa.scale == s
+            assert len(qa) == d.size and qa.original_len == x.size
+
+
+def test_quantize_batch_and_errors(tb):
+    x = np.random.default_rng(5).standard_normal((7, 333)).astype(np.float32)
+    qa = tb.quantize_activations(x, pad_to=3)
+    for i in range(7):
+        d, s, _ = O.quantize(x[i], 3)
+        assert np.array_equal(host(qa.data[i]), d) and host(qa.scales)[i] == s
+    with pytest.raises(ValueError, match=r"pad_to must be in \{1, 2, 3, 4\}"):
+        tb.quantize_activations([1.0], pad_to=5)
+    with pytest.raises(ValueError, match="activations must be finite"):
+        tb.quantize_activations([1.0, np.nan])
+    with pytest.raises(ValueError, match="empty activation vector"):
+        tb.quantize_activations(np.zeros(0))
+
+
+def test_ternarize_golden(tb):
+    offs = np.cumsum([0] + [r * c for r, c in SMALL["t_shape"]])
+    ws, qs = split(SMALL["t_w"], offs), split(SMALL["t_q"], offs)
+    for w, q, (r, c), s in zip(ws, qs, SMALL["t_shape"], SMALL["t_scale"]):
+        m = tb.ternarize_weights(w, int(r), int(c))
+        assert m.scale == s and np.array_equal(host(m.values).ravel(), q)
+    with pytest.raises(ValueError, match="degenerate weight matrix"):
+        tb.ternarize_weights([0.0] * 4, 2, 2)
+    with pytest.raises(ValueError, match="weights must be finite"):
+        tb.ternarize_weights([1.0, np.inf], 1, 2)
+
+
+def test_round_half_away(tb):
+    got = host(tb.round_half_away(np.array([0.5, -0.5, 1.5, -1.5, 0.49, 2.5, -2.5])))
+    assert got.tolist() == [1, -1, 2, -2, 0, 3, -3]
+
+
+# -------------------------------------------------------------- packing
+
+def _packing_cases():
+    shapes = SMALL["p_shape"]
+    vals = split(SMALL["p_vals"], np.cumsum([0] + [r * c for r, c in shapes]))
+    return (shapes, vals, split(SMALL["p_i2s"], SMALL["p_i2s_off"]),
+            split(SMALL["p_tl1"], SMALL["p_tl1_off"]), split(SMALL["p_tl2i"], SMALL["p_tl2i_off"]),
+            split(SMALL["p_tl2s"], SMALL["p_tl2s_off"]))
+
+
+def test_encode_decode_golden(tb):
+    shapes, vals, i2s, tl1, tl2i, tl2s = _packing_cases()
+    for k, (r, c) in enumerate(shapes):
+        v = vals[k].reshape(r, c)
+        m = tb.TernaryMatrix(int(r), int(c), v, 1.0)
+        pi, p1, p2 = tb.encode_i2s(m), tb.encode_tl1(m), tb.encode_tl2(m)
+        assert np.array_equal(host(pi.data).ravel(), i2s[k])
+        assert np.array_equal(host(p1.data).ravel(), tl1[k])
+        assert np.array_equal(host(p2.index_data).ravel(), tl2i[k])
+        assert np.array_equal(host(p2.sign_data).ravel(), tl2s[k])
+        for dec, p in ((tb.decode_i2s, pi), (tb.decode_tl1, p1), (tb.decode_tl2, p2)):
+            assert np.array_equal(host(dec(p).values), v)
+
+
+def test_tiled_repack_roundtrip(tb):
+    from paper_2410_16144_b200 import _lib as L
+    lib = L.load()
+    shapes, vals, *_ = _packing_cases()
+    for k, (r, c) in enumerate(shapes):
+        m = tb.TernaryMatrix(int(r), int(c), vals[k].reshape(r, c), 1.0)
+        for p in (tb.encode_i2s(m), tb.encode_tl1(m), tb.encode_tl2(m)):
+            main, sign = p.tiled()
+            ref = p._main_ref()
+            back = torch.empty_like(ref)
+            sref = p._sign_ref()
+            sback = torch.empty_like(sref) if sref is not None else None
+            L.check(lib.tb_unrepack(p.FMT, L.ptr(main), L.ptr(sign), p.rows, p.cols,
+                                    L.ptr(back), L.ptr(sback), L.stream_ptr()))
+            assert torch.equal(back, ref)
+            if sref is not None:
+                assert torch.equal(sback, sref)
+
+
+def test_invalid_codes(tb):
+    bad = tb.PackedI2S(rows=1, cols=4, padded_cols=4, data=np.array([[0xFF]], np.uint8), scale=1.0)
+    with pytest.raises(ValueError, match="invalid I2_S code"):
+        tb.decode_i2s(bad)
+    with pytest.raises(ValueError, match="invalid I2_S code at row 0"):
+        bad.validate()
+    data = np.full((3, 1), 0x55, np.uint8)
+    data[2, 0] = 0xC5
+    with pytest.raises(ValueError, match="invalid I2_S code at row 2"):
+        tb.PackedI2S(rows=3, cols=4, padded_cols=4, data=data, scale=1.0).validate()
+    bad1 = tb.PackedTL1(rows=1, cols=4, padded_cols=4, data=np.array([[0xF5]], np.uint8), scale=1.0)
+    with pytest.raises(ValueError, match="invalid TL1 index"):
+        tb.decode_tl1(bad1)
+    good2 = tb.encode_tl2(tb.TernaryMatrix(1, 6, np.array([[1, 1, 1, -1, -1, 0]]), 1.0))
+    bad2 = tb.PackedTL2(rows=1, cols=6, padded_cols=6, index_data=np.array([[0xED]], np.uint8),
+                        sign_data=host(good2.sign_data), scale=1.0)
+    with pytest.raises(ValueError, match="invalid TL2 index"):
+        tb.decode_tl2(bad2)
+    nc = tb.PackedTL2(rows=1, cols=6, padded_cols=6, index_data=np.array([[0x00]], np.uint8),
+                      sign_data=np.array([[0b01]], np.uint8), scale=1.0)
+    with pytest.raises(ValueError, match="non-canonical zero"):
+        tb.decode_tl2(nc)
+    with pytest.raises(ValueError, match="non-canonical zero at row 0"):
+        nc.validate()
+    # untrusted containers are validated by the kernels (test_kernels.py:146-161)
+    qa = tb.QuantizedActivations(data=np.array([1, 2, 3, 4], np.int8), scale=1.0, original_len=4)
+    lut = tb.build_lut_tl1(qa)
+    badk = tb.PackedTL1(rows=1, cols=4, padded_cols=4, data=np.array([[0xF0]], np.uint8), scale=1.0)
+    with pytest.raises(ValueError, match="invalid TL1 index"):
+        tb.gemv_tl1(badk, lut, qa.scale)
+    with pytest.raises(ValueError, match="group-count mismatch"):
+        p = tb.encode_tl1(tb.TernaryMatrix(1, 4, np.array([[1, -1, 0, 0]]), 1.0))
+        qa2 = tb.QuantizedActivations(data=np.array([1, 2], np.int8), scale=1.0, original_len=2)
+        tb.gemv_tl1(p, tb.build_lut_tl1(qa2), 1.0)
+
+
+# ------------------------------------------------------------------ lut
+
+def test_lut_golden(tb):
+    xs = split(SMALL["l_x"], SMALL["l_xoff"])
+    for x, extra, e1, e2 in zip(xs, SMALL["l_extra"], split(SMALL["l_tl1"], SMALL["l_tl1_off"]),
+                                split(SMALL["l_tl2"], SMALL["l_tl2_off"])):
+        q2 = tb_q(x, 2)
+        q3 = tb_q(x, 3)
+        l1 = TB.build_lut_tl1(q2, groups=len(q2) // 2 + int(extra))
+        l2 = TB.build_lut_tl2(q3, groups=len(q3) // 3 + int(extra))
+        assert np.array_equal(host(l1.entries).ravel(), e1)
+        assert np.array_equal(host(l2.entries).ravel(), e2)
+
+
+import paper_2410_16144_b200 as TB  # noqa: E402
+
+
+def tb_q(x, pad):
+    return TB.quantize_activations(x, pad_to=pad)
+
+
+# -------------------------------------------------------------- kernels
+
+def _cross_instances(n):
+    shapes = SMALL["g_shape"]
+    vals = split(SMALL["g_vals"], np.cumsum([0] + [r * c for r, c in shapes]))
+    xs = split(SMALL["g_x"], SMALL["g_xoff"])
+    accs = split(SMALL["g_acc"], SMALL["g_accoff"])
+    outs = split(SMALL["g_out"], SMALL["g_accoff"])
+    for k in range(n):
+        r, c = shapes[k]
+        yield (vals[k].reshape(r, c), float(SMALL["g_wscale"][k]), xs[k], accs[k], outs[k])
+
+
+@pytest.mark.parametrize("lo,hi", [(0, 500), (500, 1000), (1000, 2000)])
+def test_cross_kernel_golden(tb, lo, hi):
+    K = tb.KernelKind
+    for k, (v, ws, x, acc, out) in enumerate(_cross_instances(hi)):
+        if k < lo:
+            continue
+        m = tb.TernaryMatrix(v.shape[0], v.shape[1], v, ws)
+        packs = {K.I2_S: tb.encode_i2s(m), K.TL1: tb.encode_tl1(m), K.TL2: tb.encode_tl2(m)}
+        for kind, p in packs.items():
+            qa = tb.quantize_activations(x, pad_to=tb.KERNEL_PAD[kind])
+            r = tb.gemv_parallel(kind, p, qa)
+            assert np.array_equal(host(r.accumulators), acc), (k, kind)
+            assert np.array_equal(host(r.output), out), (k, kind)
+        r = tb.gemv_ref_int32(m, tb.quantize_activations(x, pad_to=1))
+        assert np.array_equal(host(r.accumulators), acc)
+        if k % 4 == 0:  # explicit-LUT kernels (verify.py:17-33 path)
+            q2, q3 = tb.quantize_activations(x, pad_to=2), tb.quantize_activations(x, pad_to=3)
+            r1 = tb.gemv_tl1(packs[K.TL1], tb.build_lut_tl1(q2, groups=packs[K.TL1].groups), q2.scale)
+            r2 = tb.gemv_tl2(packs[K.TL2], tb.build_lut_tl2(q3, groups=packs[K.TL2].groups), q3.scale)
+            assert np.array_equal(host(r1.accumulators), acc)
+            assert np.array_equal(host(r2.accumulators), acc)
+            assert np.array_equal(host(r1.output), out)
+
+
+def test_kernel_kats(tb):
+    K = tb.KernelKind
+    m = tb.TernaryMatrix(1, 4, np.array([[1, -1, 0, 1]]), 1.0)
+    qa = tb.QuantizedActivations(data=np.array([2, 3, -1, 4], np.int8), scale=1.0, original_len=4)
+    assert host(tb.gemv_ref_int32(m, qa).accumulators).tolist() == [3]
+    assert host(tb.gemv_parallel(K.I2_S, tb.encode_i2s(m), qa, thread_count=8).accumulators).tolist() == [3]
+    with pytest.raises(ValueError, match="thread_count must be >= 1"):
+        tb.gemv_parallel(K.I2_S, tb.encode_i2s(m), qa, thread_count=0)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        tb.gemv_ref_int32(tb.TernaryMatrix(1, 3, np.array([[1, -1, 0]]), 1.0),
+                          tb.QuantizedActivations(data=np.array([1, 2], np.int8), scale=1.0,
+                                                  original_len=2))
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        tb.gemv_ref_int32(tb.TernaryMatrix(1, 1, np.array([[1]]), 1.0),
+                          tb.QuantizedActivations(data=np.array([1, 2], np.int8), scale=1.0,
+                                                  original_len=2))
+    r = tb.gemv_ref_int32(tb.TernaryMatrix(1, 2, np.array([[1, 1]]), 0.5),
+                          tb.QuantizedActivations(data=np.array([10, 20], np.int8), scale=0.25,
+                                                  original_len=2))
+    assert host(r.output)[0] == 30 * 0.5 * 0.25
+    p = tb.encode_tl2(tb.TernaryMatrix(1, 3, np.array([[-1, -1, -1]]), 1.0))
+    qa3 = tb.QuantizedActivations(data=np.array([1, 2, 3], np.int8), scale=1.0, original_len=3)
+    assert host(tb.gemv_tl2(p, tb.build_lut_tl2(qa3, groups=p.groups), 1.0).accumulators).tolist() == [-6]
+    out = host(tb.gemv_f32_ref(tb.TernaryMatrix(1, 3, np.array([[1, 0, -1]]), 1.0),
+                               [0.5, 9.9, 0.25]).output)
+    assert out[0] == pytest.approx(0.25)
+
+
+def test_checked_paths_and_overflow(tb):
+    for cols in (4092, 16384):
+        v, a, acc = SMALL[f"ov_v{cols}"], SMALL[f"ov_a{cols}"], SMALL[f"ov_acc{cols}"]
+        m = tb.TernaryMatrix(6, cols, v, 1.0)
+        qa = tb.QuantizedActivations(data=a, scale=1.0, original_len=cols)
+        assert np.array_equal(host(tb.gemv_i2s(tb.encode_i2s(m), qa).accumulators), acc)
+        p1, p2 = tb.encode_tl1(m), tb.encode_tl2(m)
+        l1 = tb.build_lut_tl1(qa, groups=p1.groups)
+        l2 = tb.build_lut_tl2(qa, groups=p2.groups)
+        for chk in (False, True):
+            assert np.array_equal(host(tb.gemv_tl1(p1, l1, 1.0, checked=chk).accumulators), acc)
+            assert np.array_equal(host(tb.gemv_tl2(p2, l2, 1.0, checked=chk).accumulators), acc)
+        for kind, p in ((tb.KernelKind.TL1, p1), (tb.KernelKind.TL2, p2)):
+            assert np.array_equal(host(tb.gemv_parallel(kind, p, qa).accumulators), acc)
+
+
+def test_batched_tokens_match_single(tb):
+    rng = np.random.default_rng(3)
+    for rows, cols in ((70, 1000), (33, 4096), (5, 97)):
+        v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+        m = tb.TernaryMatrix(rows, cols, v, 0.7)
+        x = rng.standard_normal((13, cols)).astype(np.float32)
+        for kind, enc in ((tb.KernelKind.I2_S, tb.encode_i2s), (tb.KernelKind.TL1, tb.encode_tl1),
+                          (tb.KernelKind.TL2, tb.encode_tl2)):
+            p = enc(m)
+            for M in (1, 2, 3, 5, 8, 13):
+                qa = tb.quantize_activations(x[:M], pad_to=tb.KERNEL_PAD[kind])
+                r = tb.gemv_parallel(kind, p, qa)
+                want = np.stack([O.gemv_ref_int32(v, O.quantize(x[i], 1)[0]) for i in range(M)])
+                assert np.array_equal(host(r.accumulators), want), (kind, M)
+
+
+def test_workspace_self_cleans(tb):
+    rng = np.random.default_rng(4)
+    v = rng.integers(-1, 2, size=(300, 2000), dtype=np.int8)
+    p = tb.encode_tl2(tb.TernaryMatrix(300, 2000, v, 1.0))
+    qa = tb.quantize_activations(rng.standard_normal(2000), pad_to=3)
+    a1 = host(tb.gemv_parallel(tb.KernelKind.TL2, p, qa).accumulators)
+    a2 = host(tb.gemv_parallel(tb.KernelKind.TL2, p, qa).accumulators)
+    assert np.array_equal(a1, a2)
+    assert int(p.workspace().abs().sum()) == 0
+
+
+def test_gemv_plan_fp32_output(tb):
+    rng = np.random.default_rng(8)
+    v = rng.integers(-1, 2, size=(1000, 4096), dtype=np.int8)
+    m = tb.TernaryMatrix(1000, 4096, v, 0.0123)
+    x = rng.standard_normal((4, 4096)).astype(np.float32)
+    for enc, pad in ((tb.encode_i2s, 4), (tb.encode_tl1, 2), (tb.encode_tl2, 3)):
+        plan = tb.GemvPlan(enc(m), max_tokens=4, out_dtype=torch.float32, want_acc=True)
+        qa = tb.quantize_activations(x, pad_to=pad)
+        out = host(plan.run(qa.data, qa.scales)).astype(np.float64)
+        for i in range(4):
+            d, s, _ = O.quantize(x[i], 1)
+            ref = O.make_output(O.gemv_ref_int32(v, d), 0.0123, s)
+            np.testing.assert_allclose(out[i], ref, rtol=1e-5, atol=0)
+
+
+# ------------------------------------------------------- config-sized pins
+
+def _run_large(tb, cname, formats=("i2s", "tl1", "tl2")):
+    case, gold = LARGE_CASES[cname], LARGE[cname]
+    K = tb.KernelKind
+    kinds = {"i2s": (K.I2_S, tb.encode_i2s, 4), "tl1": (K.TL1, tb.encode_tl1, 2),
+             "tl2": (K.TL2, tb.encode_tl2, 3)}
+    mats = {}
+    for name, n, k, seed in case["matrices"]:
+        m = tb.ternarize_weights(torch.from_numpy(latent_weights(seed, n, k)), n, k)
+        g = gold["matrices"][name]
+        assert m.scale.hex() == g["scale"], (cname, name)
+        packs = {}
+        for f in formats:
+            kind, enc, _ = kinds[f]
+            p = enc(m)
+            if f == "tl2":
+                assert sha(host(p.index_data)) == g["tl2_index"]
+                assert sha(host(p.sign_data)) == g["tl2_sign"]
+            else:
+                assert sha(host(p.data)) == g[f], (cname, name, f)
+            packs[f] = p
+        mats[name] = (m, packs)
+    for name, mm, k, seed in case["acts"]:
+        x = torch.from_numpy(activations(seed, mm, k))
+        for pad in (1, 2, 3, 4):
+            qa = tb.quantize_activations(x, pad_to=pad)
+            assert sha(host(qa.data)) == gold["acts"][name][f"data_p{pad}"]
+            assert [float(s).hex() for s in host(qa.scales)] == gold["acts"][name]["scales"]
+    for wname, aname in case["gemv"]:
+        m, packs = mats[wname]
+        mm, k, seed = [(a[1], a[2], a[3]) for a in case["acts"] if a[0] == aname][0]
+        x = torch.from_numpy(activations(seed, mm, k))
+        g = gold["gemv"][f"{wname}:{aname}"]
+        for f, p in packs.items():
+            kind, _, pad = kinds[f]
+            qa = tb.quantize_activations(x, pad_to=pad)
+            r = tb.gemv_parallel(kind, p, qa)
+            acc = host(r.accumulators).reshape(mm, -1)
+            out = host(r.output).reshape(mm, -1)
+            assert sha(acc) == g["acc"], (cname, wname, f)
+            assert sha(out) == g["out"], (cname, wname, f)
+
+
+def test_large_cfg0(tb):
+    _run_large(tb, "cfg0")
+
+
+def test_large_cfg1(tb):
+    _run_large(tb, "cfg1")
+
+
+def test_large_cfg2(tb):
+    _run_large(tb, "cfg2", formats=("i2s", "tl2"))
+
+
+def test_large_cfg3(tb):
+    _run_large(tb, "cfg3", formats=("i2s",))
+
+
+def test_large_cfg4(tb):
+    _run_large(tb, "cfg4", formats=("i2s",))
