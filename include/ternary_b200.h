@@ -138,6 +138,53 @@ int tb_build_lut(int fmt, const int8_t *act, int64_t len, int64_t groups,
  * use; every call leaves it zeroed again (self-cleaning), so one workspace
  * serves any number of back-to-back calls on ONE stream.                    */
 int64_t tb_gemv_workspace_bytes(int fmt, int64_t rows, int64_t cols);
+
+/* Activation "records": the decode GEMV's input form of M int8 activation
+ * vectors -- per 16-byte weight chunk, the chunk's activations byte-
+ * transposed to match the decoded code words plus their sum (80 B per chunk
+ * for I2S/TL1, 112 B for TL2).  GEMVs that share an input (q/k/v, gate/up)
+ * share one record buffer.  `rec` must be 16-byte aligned.                  */
+int64_t tb_act_records_bytes(int fmt, int64_t M, int64_t cols);
+int tb_prep_activations(int fmt, const int8_t *act, int64_t M, int64_t ld_act,
+                        int64_t act_len, int64_t cols, uint8_t *rec, void *stream);
+/* quantize_activations fused with record construction (core.py:116-134):
+ * x[M][ldx] (K = cols valid) -> scale[M], records, and optionally the natural
+ * int8 q[M][ldq] (bit-exact reference data; NULL to skip).                 */
+int tb_quantize_records_f32(int fmt, const float *x, int64_t M, int64_t K,
+                            int64_t ldx, int8_t *q, int64_t ldq, double *scale,
+                            uint8_t *rec, int32_t *nonfinite_flag, void *stream);
+int tb_quantize_records_f64(int fmt, const double *x, int64_t M, int64_t K,
+                            int64_t ldx, int8_t *q, int64_t ldq, double *scale,
+                            uint8_t *rec, int32_t *nonfinite_flag, void *stream);
+/* The decode GEMV proper, on prepared records (one launch).                */
+int tb_gemv_records(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
+                    int64_t rows, int64_t cols, const uint8_t *rec, int64_t M,
+                    const double *a_scale, double w_scale, void *workspace,
+                    int32_t *acc_out, double *out64, float *out32, void *stream);
+/* Grouped decode GEMV: several independent GEMVs of one format in ONE launch
+ * (the weight stream never stops at a matrix boundary).  prepare() fills a
+ * caller-provided host buffer of njobs * tb_gemv_job_bytes() bytes; copy it
+ * to device memory once, then launch() as often as needed (capturable: no
+ * host sync, no allocation).                                                */
+typedef struct tb_gemv_desc {
+  const uint8_t *tiled;
+  const uint8_t *tiled_sign;
+  int64_t rows, cols;
+  const uint8_t *rec; /* records of this GEMV's input (shared is fine)     */
+  int64_t M;
+  const double *a_scale;
+  double w_scale;
+  void *workspace; /* per GEMV, tb_gemv_workspace_bytes, zeroed once        */
+  int32_t *acc_out;
+  double *out64;
+  float *out32;
+} tb_gemv_desc;
+int64_t tb_gemv_job_bytes(void);
+int tb_gemv_batch_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
+                          void *table_host, int64_t *total_chunks, int32_t *max_m);
+int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t njobs,
+                         int64_t total_chunks, int32_t max_m, void *stream);
+/* Convenience: tb_prep_activations into the workspace + tb_gemv_records.   */
 int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
             int64_t rows, int64_t cols, const int8_t *act, int64_t M,
             int64_t ld_act, int64_t act_len, const double *a_scale,

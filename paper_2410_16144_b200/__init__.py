@@ -20,6 +20,8 @@ from .core import (
 )
 from .kernels import (
     KERNEL_PAD,
+    ActRecords,
+    GemvBatch,
     GemvPlan,
     KernelKind,
     gemv_f32_ref,

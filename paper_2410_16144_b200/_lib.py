@@ -46,6 +46,15 @@ _SIGS = {
     "tb_gemv_workspace_bytes": (_i64, [_i32, _i64, _i64]),
     "tb_gemv": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _i64, _i64, _p, _f64, _p, _p, _p,
                        _p, _p]),
+    "tb_act_records_bytes": (_i64, [_i32, _i64, _i64]),
+    "tb_prep_activations": (_i32, [_i32, _p, _i64, _i64, _i64, _i64, _p, _p]),
+    "tb_quantize_records_f32": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _p]),
+    "tb_quantize_records_f64": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _p]),
+    "tb_gemv_records": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _p, _f64, _p, _p, _p, _p,
+                               _p]),
+    "tb_gemv_job_bytes": (_i64, []),
+    "tb_gemv_batch_prepare": (_i32, [_i32, _i64, _p, _p, _p, _p]),
+    "tb_gemv_batch_launch": (_i32, [_i32, _p, _i64, _i64, _i32, _p]),
     "tb_gemv_lut": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _p, _p]),
     "tb_gemv_ref_int32": (_i32, [_p, _i64, _i64, _p, _p, _p]),
     "tb_gemv_f32_ref": (_i32, [_p, _i64, _i64, _f32, _p, _p, _p]),
@@ -53,6 +62,14 @@ _SIGS = {
                           _p, _p]),
     "tb_gemm_workspace_bytes": (_i64, [_i32, _i64, _i64, _i64]),
 }
+
+class GemvDesc(C.Structure):
+    """Mirror of tb_gemv_desc (include/ternary_b200.h)."""
+
+    _fields_ = [("tiled", _p), ("tiled_sign", _p), ("rows", _i64), ("cols", _i64),
+                ("rec", _p), ("M", _i64), ("a_scale", _p), ("w_scale", _f64),
+                ("workspace", _p), ("acc_out", _p), ("out64", _p), ("out32", _p)]
+
 
 _lib = None
 

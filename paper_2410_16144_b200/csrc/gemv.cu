@@ -1,41 +1,79 @@
-// Decode GEMV (M <= 16) on the tiled I2_S / TL1 / TL2 layouts.
+// Decode GEMV (M <= 16) on the tiled I2_S / TL1 / TL2 layouts -- grouped.
 //
 // Replaces kernels.gemv_i2s / gemv_tl1 / gemv_tl2 / gemv_parallel
 // (pkg/src/ternpack/kernels.py:86-157, 189-268) and the numba byte-table
 // gathers (_fast.py:25-95).  The reference gathers one int32 table entry per
 // packed byte; here the packed bytes are decoded in registers to 2-bit codes
 // c = w + 1 in {0,1,2} (four per 32-bit word, one per byte lane) and
-// contracted with dp4a against a byte-transposed copy of the int8 activations
-// held in shared memory.  sum_k w_k a_k = sum_k c_k a_k - sum_k a_k, so the
-// per-chunk activation sums are subtracted once per chunk.  Integer results
+// contracted with dp4a against byte-transposed int8 activations (the
+// "records" of gemv_records.cuh).  sum_k w_k a_k = sum_k c_k a_k - sum_k a_k,
+// so per-chunk activation sums are subtracted once per chunk.  Integer results
 // are exact, hence bit-identical to the reference's LUT/byte-table kernels.
 //
-// Data movement: a persistent grid (one CTA per SM); each CTA owns a
-// contiguous range of (row tile, chunk) units -- a contiguous byte range of
-// the tiled layout -- and one producer thread streams it HBM -> SMEM with
-// cp.async.bulk into a 6-stage mbarrier ring.  Eight consumer warps decode:
+// One launch serves a *group* of independent GEMVs ("jobs": e.g. the gate, up
+// and down projections of a token, or every projection of a layer) so the
+// weight stream never stops at a matrix boundary and the kernel's fixed
+// costs (launch, first-byte latency, completion) are paid once per group.
+//
+// Data movement: persistent grid, one CTA per SM, every warp autonomous.  The
+// jobs' (row tile, chunk) spaces are concatenated into one flat range -- each
+// job's part a contiguous byte range of its tiled layout -- split evenly over
+// all warps of the grid; each warp streams its range (weights, TL2 signs and
+// the matching activation records) HBM/L2 -> SMEM through its own ring of
+// cp.async.bulk stages, one mbarrier per stage: no CTA-wide synchronisation.
 // lane = row of the 32-row tile, so activation reads are warp broadcasts and
-// weight reads are conflict-free 16-byte LDS.  Partial sums of a row tile are
-// combined with red.global.add in a self-cleaning int32 workspace; the warp
-// that retires the tile's last chunk applies the scales (core.py:99-101).
+// weight reads conflict-free 16-byte LDS.  A warp's partial sums for a row
+// tile go to the job's self-cleaning int32 workspace with red.global.add; the
+// warp that retires the tile's last chunk (acq_rel counter) applies the
+// scales (core.py:99-101), writes the outputs and resets the workspace.
 #include <algorithm>
 
-#include "common.cuh"
+#include "gemv_records.cuh"
 
 namespace tb {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = 32 * (1 + kConsumerWarps);
-constexpr int kStageChunks = 16;
-constexpr int kStages = 6;
-constexpr int64_t kActSmemBudget = 120 * 1024;
+constexpr int kMaxInlineJobs = 8;
 
-struct GemvParams {
+// Optional per-warp timeline (debug builds with -DTB_TIMELINE only).
+#ifdef TB_TIMELINE
+constexpr int kTimelineWarps = 148 * 32;
+__device__ unsigned long long g_timeline[kTimelineWarps][5];
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_MARK(i)                                                    \
+  do {                                                                \
+    if (lane == 0 && gw < kTimelineWarps) g_timeline[gw][i] = globaltimer_ns(); \
+  } while (0)
+#else
+#define TL_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
+template <int FMT, int MT>
+struct Cfg {
+#ifndef TB_MT1_WARPS
+#define TB_MT1_WARPS 16
+#endif
+  static constexpr int kWarps = MT == 1 ? TB_MT1_WARPS : (MT <= 4 ? 16 : 8);
+#ifndef TB_MT1_RING
+#define TB_MT1_RING (TB_MT1_WARPS > 16 ? 3 : 4)
+#endif
+  static constexpr int kRing = MT == 1 ? TB_MT1_RING : (MT == 2 ? 3 : 2);
+  static constexpr int kThreads = 32 * kWarps;
+  static constexpr int kStageBytes =
+      kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + MT * Fmt<FMT>::kRecBytes);
+  static constexpr int kSmem = kWarps * kRing * kStageBytes;
+  static_assert(kSmem <= 227 * 1024, "ring does not fit in shared memory");
+};
+
+struct GemvJob {
   const uint8_t *wmain;
   const uint8_t *wsign;
-  const int8_t *act;
-  int64_t ld_act;
-  int64_t act_len;
+  const uint8_t *rec;  // [M][C][kRecBytes]
   const double *a_scale;
   double w_scale;
   int32_t *ws_acc;  // [16][Npad]
@@ -43,400 +81,606 @@ struct GemvParams {
   int32_t *acc_out;
   double *out64;
   float *out32;
-  int64_t total;  // T * Cs units in this pass
-  int N, Npad, T, C, c0, Cs, M;
+  int N, Npad, C, M;
+  int start;  // first flat chunk of this job
+  int end;    // one past its last flat chunk (start + T * C)
 };
 
-template <int FMT>
-struct Fmt {
-  static constexpr int kActWords = FMT == TB_TL2 ? 24 : 16;  // permuted act words / chunk
-  static constexpr int kSignBytes = FMT == TB_TL2 ? kTileSignBytes : 0;
-  static constexpr int kStageBytes = kStageChunks * (kTileChunkBytes + kSignBytes);
+struct GemvBatch {
+  GemvJob jobs[kMaxInlineJobs];
+  const GemvJob *table;  // device copy, used when njobs > kMaxInlineJobs
+  int njobs;
+  int total;  // flat chunks over all jobs
+  int base, rem;  // warp w gets base + (w < rem) chunks
 };
 
-template <int FMT>
-static size_t gemv_smem_bytes(int M, int Cs) {
-  size_t stages = (size_t)kStages * Fmt<FMT>::kStageBytes;
-  size_t bars = 2 * kStages * sizeof(uint64_t);
-  size_t acts = (size_t)M * Cs * (Fmt<FMT>::kActWords * 4 + 4);
-  return stages + bars + acts;
+// Job descriptor by value: inline jobs come from the (grid-constant) kernel
+// parameters via indexed constant loads, larger groups from a global table.
+__device__ __forceinline__ GemvJob job_at(const GemvBatch &b, int j) {
+  if (b.table) return b.table[j];
+  return b.jobs[j];
 }
 
-__device__ __forceinline__ uint32_t byte_of(const uint8_t *buf, int i) { return buf[i]; }
-
-// Build the byte-transposed activation words of one chunk.
-//   I2_S / TL1 (64 acts): word 4i+s = (a[16i+s], a[16i+4+s], a[16i+8+s], a[16i+12+s])
-//   TL2        (96 acts): word 6i+s = (a[24i+s], a[24i+6+s], a[24i+12+s], a[24i+18+s])
-template <int FMT>
-__device__ void stage_activation_chunk(const int8_t *arow, int64_t act_len, int64_t k0,
-                                       uint32_t *dst, int32_t *sum_out) {
-  constexpr int W = FMT == TB_TL2 ? 96 : 64;
-  constexpr int G = FMT == TB_TL2 ? 6 : 4;  // stride between bytes of one word
-  alignas(16) uint8_t buf[W];
-  if (k0 + W <= act_len && (reinterpret_cast<uintptr_t>(arow + k0) & 15) == 0) {
-#pragma unroll
-    for (int v = 0; v < W / 16; ++v)
-      reinterpret_cast<uint4 *>(buf)[v] = __ldg(reinterpret_cast<const uint4 *>(arow + k0) + v);
-  } else {
-    for (int b = 0; b < W; ++b) buf[b] = (k0 + b < act_len) ? (uint8_t)arow[k0 + b] : 0;
-  }
-  int32_t sum = 0;
-#pragma unroll
-  for (int b = 0; b < W; ++b) sum += (int8_t)buf[b];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-#pragma unroll
-    for (int s = 0; s < G; ++s) {
-      const int base = i * 4 * G + s;
-      dst[i * G + s] = byte_of(buf, base) | (byte_of(buf, base + G) << 8) |
-                       (byte_of(buf, base + 2 * G) << 16) | (byte_of(buf, base + 3 * G) << 24);
-    }
-  }
-  *sum_out = sum;
+__device__ __forceinline__ int atom_add_acq_rel(int *ptr, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(ptr), "r"(v)
+               : "memory");
+  return old;
 }
 
-template <int FMT, int MT>
-struct Acc {
-  // I2_S keeps one accumulator per 2-bit slot (scaled by 4^s, see decode);
-  // TL1 / TL2 decode straight to unscaled codes.
-  static constexpr int kSlots = FMT == TB_I2S ? 4 : 1;
-  int32_t v[MT][kSlots];
-  int32_t csum[MT];
-  __device__ __forceinline__ void zero() {
-#pragma unroll
-    for (int m = 0; m < MT; ++m) {
-#pragma unroll
-      for (int s = 0; s < kSlots; ++s) v[m][s] = 0;
-      csum[m] = 0;
-    }
-  }
-  __device__ __forceinline__ int32_t total(int m) const {
-    if (FMT == TB_I2S)
-      return v[m][0] + (v[m][1] >> 2) + (v[m][2] >> 4) + (v[m][3] >> 6) - csum[m];
-    return v[m][0] - csum[m];
-  }
-};
-
-// One 16-byte chunk of one row (this lane's row) against MT activation rows.
-template <int FMT, int MT>
-__device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn,
-                                              const uint32_t *__restrict__ a_chunk,
-                                              int64_t act_tok_stride, int M, Acc<FMT, MT> &acc) {
-  const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t W = w[i];
-    if constexpr (FMT == TB_I2S) {
-      // byte b of (W & (3 << 2s)) = code of weight 16i + 4b + s, times 4^s
-      const uint32_t x0 = W & 0x03030303u, x1 = W & 0x0C0C0C0Cu;
-      const uint32_t x2 = W & 0x30303030u, x3 = W & 0xC0C0C0C0u;
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        if (m < M) {
-          const uint4 A = *reinterpret_cast<const uint4 *>(a_chunk + m * act_tok_stride + 4 * i);
-          acc.v[m][0] = dp4a_us(x0, A.x, acc.v[m][0]);
-          acc.v[m][1] = dp4a_us(x1, A.y, acc.v[m][1]);
-          acc.v[m][2] = dp4a_us(x2, A.z, acc.v[m][2]);
-          acc.v[m][3] = dp4a_us(x3, A.w, acc.v[m][3]);
-        }
-      }
-    } else if constexpr (FMT == TB_TL1) {
-      // nibble n = 3*c0 + c1 (packing.py:56-60): c0 = n/3 = (11n)>>5 for n <= 8
-      const uint32_t lo = W & 0x0F0F0F0Fu, hi = (W >> 4) & 0x0F0F0F0Fu;
-      const uint32_t qlo = ((lo * 11u) >> 5) & 0x03030303u, rlo = lo - 3u * qlo;
-      const uint32_t qhi = ((hi * 11u) >> 5) & 0x03030303u, rhi = hi - 3u * qhi;
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        if (m < M) {
-          const uint4 A = *reinterpret_cast<const uint4 *>(a_chunk + m * act_tok_stride + 4 * i);
-          int32_t t = acc.v[m][0];
-          t = dp4a_us(qlo, A.x, t);
-          t = dp4a_us(rlo, A.y, t);
-          t = dp4a_us(qhi, A.z, t);
-          t = dp4a_us(rhi, A.w, t);
-          acc.v[m][0] = t;
-        }
-      }
-    } else {
-      // TL2 (packing.py:63-74): d = 13 + idx (sign 0) or 13 - idx (sign 1) is
-      // the base-3 number of the triple's codes (c0 c1 c2).
-      const uint32_t S = (sgn >> (8 * i)) & 0xFFu;
-      const uint32_t lo = W & 0x0F0F0F0Fu, hi = (W >> 4) & 0x0F0F0F0Fu;
-      // byte-wide sign masks: even sign bits -> low-nibble triples, odd -> high
-      const uint32_t mlo = prmt((S & 0x55u) * 0x02082080u, 0u, 0xBA98u);
-      const uint32_t mhi = prmt((S & 0xAAu) * 0x01041040u, 0u, 0xBA98u);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t x = h ? hi : lo;
-        const uint32_t msk = h ? mhi : mlo;
-        const uint32_t d = lop3_sel(x + 0x0D0D0D0Du, 0x0D0D0D0Du - x, msk);
-        const uint32_t c0 = ((d * 7u + 0x07070707u) >> 6) & 0x03030303u;  // d / 9
-        const uint32_t r = d - 9u * c0;                                      // d % 9
-        const uint32_t c1 = ((r * 11u) >> 5) & 0x03030303u;                  // r / 3
-        const uint32_t c2 = r - 3u * c1;                                     // r % 3
-#pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          if (m < M) {
-            const uint32_t *A = a_chunk + m * act_tok_stride + 6 * i + 3 * h;
-            int32_t t = acc.v[m][0];
-            t = dp4a_us(c0, A[0], t);
-            t = dp4a_us(c1, A[1], t);
-            t = dp4a_us(c2, A[2], t);
-            acc.v[m][0] = t;
-          }
-        }
-      }
-    }
-  }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Publish a warp's partial sums of one row tile: fire-and-forget REDs into
+// the job's int32 workspace (no fence, no completion counter -- measured at
+// ~4.6 us per launch on B200 for a 43 MB group).  The grid boundary orders
+// them before gemv_finalize_kernel, which applies the scales.
 template <int FMT, int MT>
-__device__ __forceinline__ void flush_tile(const GemvParams &p, int t, int nch,
-                                           const Acc<FMT, MT> &acc, int lane) {
+__device__ __forceinline__ void flush_tile(const GemvBatch &b, int j, int t,
+                                           const Acc<FMT, MT> &acc, int M, int lane) {
+#ifdef TB_NO_FLUSH  // profiling variant: drop the partial sums
+  return;
+#endif
+  const GemvJob J = job_at(b, j);
   const int row = t * kRowTile + lane;
 #pragma unroll
   for (int m = 0; m < MT; ++m)
-    if (m < p.M) red_add_s32(p.ws_acc + (int64_t)m * p.Npad + row, acc.total(m));
-  __threadfence();
-  __syncwarp();
-  int last = 0;
-  if (lane == 0) {
-    int old = atomicAdd(p.ws_cnt + t, nch);
-    last = (old + nch == p.C);
-  }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  __threadfence();
-#pragma unroll
-  for (int m = 0; m < MT; ++m) {
-    if (m < p.M) {
-      const int32_t v = atomicExch(p.ws_acc + (int64_t)m * p.Npad + row, 0);
-      if (row < p.N) {
-        const int64_t o = (int64_t)m * p.N + row;
-        if (p.acc_out) p.acc_out[o] = v;
-        if (p.out64 || p.out32) {
-          const double y = static_cast<double>(v) * p.w_scale * p.a_scale[m];
-          if (p.out64) p.out64[o] = y;
-          if (p.out32) p.out32[o] = static_cast<float>(y);
+    if (m < M) red_add_s32(J.ws_acc + (int64_t)m * J.Npad + row, acc.total(m));
+}
+
+// After the GEMV grid: output = f64(acc) * w_scale * a_scale[m] (core.py:
+// 99-101), optional int32 / f32 copies, and the workspace is zeroed again.
+// Launched with programmatic dependent launch: griddepcontrol.wait blocks
+// until the GEMV grid has completed and its memory operations are visible.
+__global__ void gemv_finalize_kernel(const __grid_constant__ GemvBatch b) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int j = 0; j < b.njobs; ++j) {
+    const GemvJob J = job_at(b, j);
+    const int64_t total = (int64_t)J.M * J.Npad;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int m = (int)(i / J.Npad), row = (int)(i - (int64_t)m * J.Npad);
+      const int32_t v = J.ws_acc[i];
+      J.ws_acc[i] = 0;
+      if (row < J.N) {
+        const int64_t o = (int64_t)m * J.N + row;
+        if (J.acc_out) J.acc_out[o] = v;
+        if (J.out64 || J.out32) {
+          const double y = static_cast<double>(v) * J.w_scale * J.a_scale[m];
+          if (J.out64) J.out64[o] = y;
+          if (J.out32) J.out32[o] = static_cast<float>(y);
         }
       }
     }
   }
-  if (lane == 0) p.ws_cnt[t] = 0;
 }
+
+// Position of the warp's streaming cursor: job j, tile t, chunk c of the tile.
+struct Cursor {
+  int j, t, c;
+};
+
+__device__ __forceinline__ void cp_async16_cg(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16_ca(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Stage `cnt` chunks starting at cursor `cur` into `slot` with cp.async
+// (every lane issues its own 16-byte copies: no TMA request-rate limit).
+// Runs split at job boundaries (weights are contiguous within a job); the
+// activation-record chunk index wraps at row-tile ends.
+constexpr int kIssueWeights = 1, kIssueRecords = 2, kIssueAll = 3;
+
+template <int FMT, int kWhat>
+__device__ void issue_chunks(const GemvBatch &b, Cursor cur, int cnt, uint8_t *slot, int lane) {
+  using F = Fmt<FMT>;
+  uint8_t *sign_slot = slot + kStageChunks * kTileChunkBytes;
+  uint8_t *act_slot = slot + kStageChunks * (kTileChunkBytes + F::kSignBytes);
+#ifdef TB_NO_LOADS  // profiling variant: compute on stale shared memory only
+  return;
+#endif
+  int done = 0;
+  while (done < cnt) {
+    GemvJob J = job_at(b, cur.j);
+    const int C = J.C;
+    const int left_in_job = J.end - (J.start + cur.t * C + cur.c);
+    const int run = min(cnt - done, left_in_job);
+    const int64_t g = (int64_t)cur.t * C + cur.c;  // chunk index in the job's tiled layout
+    // weights: lane = row, 16 B per chunk (a coalesced 512 B per warp instruction)
+    if (kWhat & kIssueWeights) {
+      for (int r = 0; r < run; ++r)
+        cp_async16_cg(slot + (done + r) * kTileChunkBytes + lane * 16,
+                      J.wmain + (g + r) * kTileChunkBytes + lane * 16);
+      if (FMT == TB_TL2 && lane < kTileSignBytes / 16)
+        for (int r = 0; r < run; ++r)
+          cp_async16_cg(sign_slot + (done + r) * kTileSignBytes + lane * 16,
+                        J.wsign + (g + r) * kTileSignBytes + lane * 16);
+    }
+    // activation records of every token (chunk index wraps at row-tile ends)
+    constexpr int RU = F::kRecBytes / 16;
+    const int units = (kWhat & kIssueRecords) ? J.M * run * RU : 0;
+    for (int u = lane; u < units; u += 32) {
+      const int m = u / (run * RU);
+      const int rem = u - m * run * RU;
+      const int d = rem / RU, q = rem - d * RU;
+      const int c = (cur.c + d) % C;
+      cp_async16_ca(act_slot + (m * kStageChunks + done + d) * F::kRecBytes + q * 16,
+                    J.rec + ((int64_t)m * C + c) * F::kRecBytes + q * 16);
+    }
+    done += run;
+    // advance the cursor
+    cur.c += run;
+    cur.t += cur.c / C;
+    cur.c %= C;
+    if (J.start + cur.t * C + cur.c >= J.end) {
+      ++cur.j;
+      cur.t = 0;
+      cur.c = 0;
+    }
+  }
+}
+
+__device__ __forceinline__ void advance(const GemvBatch &b, Cursor &cur, int k) {
+  GemvJob J = job_at(b, cur.j);
+  cur.c += k;
+  while (cur.c >= J.C) {
+    cur.c -= J.C;
+    ++cur.t;
+    if (J.start + cur.t * J.C >= J.end) {
+      ++cur.j;
+      cur.t = 0;
+      if (cur.j < b.njobs) J = job_at(b, cur.j);
+    }
+  }
+}
+
+// Issue cursor with the current job's pointers cached, so the common stage
+// (4 chunks inside one row tile of one job) is 4 weight copies + 1 record copy
+// per lane and no integer division.
+struct IssueState {
+  Cursor cur;
+  const uint8_t *w;    // weights of chunk `cur` in the job's tiled layout
+  const uint8_t *sgn;  // TL2 sign bits of chunk `cur`
+  const uint8_t *rec;  // the job's record base
+  int C, T, M;
+
+  __device__ __forceinline__ void reset(const GemvBatch &b, Cursor c) {
+    cur = c;
+    const GemvJob J = job_at(b, c.j);
+    C = J.C;
+    M = J.M;
+    T = (J.end - J.start) / J.C;
+    const int64_t g = (int64_t)c.t * C + c.c;
+    w = J.wmain + g * kTileChunkBytes;
+    sgn = J.wsign + g * kTileSignBytes;
+    rec = J.rec;
+  }
+
+  template <int FMT, int kWhat = kIssueAll>
+  __device__ __forceinline__ void issue(const GemvBatch &b, int cnt, uint8_t *slot, int lane) {
+    using F = Fmt<FMT>;
+    if (cnt == kStageChunks && cur.c + kStageChunks <= C) {
+      uint8_t *sign_slot = slot + kStageChunks * kTileChunkBytes;
+      uint8_t *act_slot = slot + kStageChunks * (kTileChunkBytes + F::kSignBytes);
+#ifndef TB_NO_LOADS
+      if (kWhat & kIssueWeights) {
+#pragma unroll
+        for (int r = 0; r < kStageChunks; ++r)
+          cp_async16_cg(slot + r * kTileChunkBytes + lane * 16,
+                        w + r * kTileChunkBytes + lane * 16);
+        if (FMT == TB_TL2 && lane < kTileSignBytes / 16) {
+#pragma unroll
+          for (int r = 0; r < kStageChunks; ++r)
+            cp_async16_cg(sign_slot + r * kTileSignBytes + lane * 16,
+                          sgn + r * kTileSignBytes + lane * 16);
+        }
+      }
+      if ((kWhat & kIssueRecords) && lane < kStageChunks * F::kRecBytes / 16)
+        for (int m = 0; m < M; ++m)  // the stage's 4 records are contiguous
+          cp_async16_ca(act_slot + m * kStageChunks * F::kRecBytes + lane * 16,
+                        rec + ((int64_t)m * C + cur.c) * F::kRecBytes + lane * 16);
+#endif
+      w += kStageChunks * kTileChunkBytes;
+      sgn += kStageChunks * kTileSignBytes;
+      cur.c += kStageChunks;
+      if (cur.c == C) {
+        cur.c = 0;
+        if (++cur.t == T) {
+          ++cur.j;
+          cur.t = 0;
+          if (cur.j < b.njobs) reset(b, cur);
+        }
+      }
+      return;
+    }
+    issue_chunks<FMT, kWhat>(b, cur, cnt, slot, lane);  // general path: tile / job boundaries
+    advance(b, cur, cnt);
+    if (cur.j < b.njobs) reset(b, cur);
+  }
+};
 
 template <int FMT, int MT>
-__global__ void __launch_bounds__(kThreads, 1) tgemv_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(Cfg<FMT, MT>::kThreads, 1)
+    tgemv_kernel(const __grid_constant__ GemvBatch b) {
   using F = Fmt<FMT>;
+  using CF = Cfg<FMT, MT>;
+  constexpr int kRing = CF::kRing;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t *st_main = smem;
-  uint8_t *st_sign = smem + kStages * kStageChunks * kTileChunkBytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * F::kStageBytes);
-  uint64_t *empty = full + kStages;
-  uint32_t *s_act = reinterpret_cast<uint32_t *>(empty + kStages);
-  int32_t *s_csum = reinterpret_cast<int32_t *>(s_act + (int64_t)p.M * p.Cs * F::kActWords);
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t G = gridDim.x;
-  const int64_t g0 = p.total * blockIdx.x / G;
-  const int64_t g1 = p.total * (blockIdx.x + 1) / G;
+  uint8_t *ring = smem + warp * kRing * CF::kStageBytes;
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kConsumerWarps);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t g = g0; g < g1; g += kStageChunks) {
-        const int n = (int)imin64(kStageChunks, g1 - g);
-        mbar_wait(empty + stage, phase ^ 1);
-        mbar_arrive_expect_tx(full + stage, n * (kTileChunkBytes + F::kSignBytes));
-        int done = 0;
-        int64_t gg = g;
-        while (done < n) {
-          const int64_t t = gg / p.Cs;
-          const int64_t cc = gg - t * p.Cs;
-          const int run = (int)imin64(n - done, p.Cs - cc);
-          const int64_t src = t * p.C + p.c0 + cc;  // chunk index in the tiled layout
-          bulk_g2s(st_main + (stage * kStageChunks + done) * kTileChunkBytes,
-                   p.wmain + src * kTileChunkBytes, run * kTileChunkBytes, full + stage);
-          if (FMT == TB_TL2)
-            bulk_g2s(st_sign + (stage * kStageChunks + done) * kTileSignBytes,
-                     p.wsign + src * kTileSignBytes, run * kTileSignBytes, full + stage);
-          done += run;
-          gg += run;
-        }
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
+  const int gw = blockIdx.x * CF::kWarps + warp;
+  TL_MARK(0);
+  // let the finalize kernel (our programmatic dependent) get launched early
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int w0 = gw * b.base + min(gw, b.rem);
+  const int n = b.base + (gw < b.rem ? 1 : 0);
+  if (n <= 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
+  const int nst = (n + kStageChunks - 1) / kStageChunks;
 
-  // ---------------------------------------------------------------- consumers
-  const int ctid = threadIdx.x - 32;
-  for (int64_t it = ctid; it < (int64_t)p.M * p.Cs; it += kConsumerWarps * 32) {
-    const int m = (int)(it / p.Cs), c = (int)(it % p.Cs);
-    stage_activation_chunk<FMT>(p.act + m * p.ld_act, p.act_len,
-                                (int64_t)(p.c0 + c) * chunk_weights(FMT),
-                                s_act + it * F::kActWords, s_csum + it);
+  // locate the first chunk
+  Cursor cur{0, 0, 0};
+  while (cur.j + 1 < b.njobs && job_at(b, cur.j + 1).start <= w0) ++cur.j;
+  {
+    GemvJob J = job_at(b, cur.j);
+    const int local = w0 - J.start;
+    cur.t = local / J.C;
+    cur.c = local - cur.t * J.C;
   }
-  named_bar_sync(1, kConsumerWarps * 32);
+  IssueState is;  // issue cursor + cached job pointers (identical in every lane)
+  is.reset(b, cur);
+  TL_MARK(1);
+  // Prologue.  Weights never depend on the previous kernel, so the first
+  // stages' weights are requested before griddepcontrol.wait (this kernel is
+  // a programmatic dependent of whatever produced the activation records);
+  // the records follow once the producer has completed.
+  {
+    IssueState wis = is;
+#pragma unroll 1
+    for (int k = 0; k < kRing && k < nst; ++k)
+      wis.issue<FMT, kIssueWeights>(b, min(kStageChunks, n - k * kStageChunks),
+                                    ring + k * CF::kStageBytes, lane);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#pragma unroll 1
+  for (int k = 0; k < kRing; ++k) {
+    if (k < nst) is.issue<FMT, kIssueRecords>(b, min(kStageChunks, n - k * kStageChunks),
+                                              ring + k * CF::kStageBytes, lane);
+    cp_async_commit();  // group 0 also holds every prologue weight copy
+  }
 
-  const int cw = warp - 1;
-  const int64_t act_tok_stride = (int64_t)p.Cs * F::kActWords;
+  int C, M, T;  // shape of the current job
+  {
+    const GemvJob J = job_at(b, cur.j);
+    C = J.C;
+    M = J.M;
+    T = (J.end - J.start) / J.C;
+  }
   Acc<FMT, MT> acc;
   acc.zero();
-  int cur_t = -1, nch = 0;
-  int stage = 0;
-  uint32_t phase = 0;
-  for (int64_t g = g0; g < g1; g += kStageChunks) {
-    const int n = (int)imin64(kStageChunks, g1 - g);
-    mbar_wait(full + stage, phase);
-    for (int j = cw; j < n; j += kConsumerWarps) {
-      const int64_t gg = g + j;
-      const int t = (int)(gg / p.Cs);
-      const int c = (int)(gg - (int64_t)t * p.Cs);
-      if (t != cur_t) {
-        if (cur_t >= 0) flush_tile<FMT, MT>(p, cur_t, nch, acc, lane);
-        cur_t = t;
-        nch = 0;
-        acc.zero();
+  int nch = 0;
+  for (int k = 0; k < nst; ++k) {
+    const int s = k % kRing;
+    uint8_t *slot = ring + s * CF::kStageBytes;
+    const uint8_t *slot_sign = slot + kStageChunks * kTileChunkBytes;
+    const uint8_t *slot_act = slot + kStageChunks * (kTileChunkBytes + F::kSignBytes);
+    const int nk = min(kStageChunks, n - k * kStageChunks);
+    cp_async_wait<kRing - 1>();  // this lane's copies of stage k have landed
+    __syncwarp();                 // ... and every other lane's
+    if (k == 0) TL_MARK(2);
+    if (nk == kStageChunks && cur.c + kStageChunks <= C) {
+      // fast path: four chunks of the current row tile, fully unrolled
+#pragma unroll
+      for (int j = 0; j < kStageChunks; ++j) {
+        const uint4 w4 = *reinterpret_cast<const uint4 *>(slot + j * kTileChunkBytes + lane * 16);
+        uint32_t sg = 0;
+        if (FMT == TB_TL2)
+          sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
+        process_chunk<FMT, MT>(w4, sg, slot_act + j * F::kRecBytes, M, acc);
       }
-      const int slot = stage * kStageChunks + j;
-      const uint4 w4 = *reinterpret_cast<const uint4 *>(st_main + slot * kTileChunkBytes + lane * 16);
-      uint32_t sg = 0;
-      if (FMT == TB_TL2)
-        sg = *reinterpret_cast<const uint32_t *>(st_sign + slot * kTileSignBytes + lane * 4);
-      process_chunk<FMT, MT>(w4, sg, s_act + (int64_t)c * F::kActWords, act_tok_stride, p.M, acc);
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-        if (m < p.M) acc.csum[m] += s_csum[(int64_t)m * p.Cs + c];
-      ++nch;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + stage);
-    if (++stage == kStages) {
-      stage = 0;
-      phase ^= 1;
-    }
-  }
-  if (cur_t >= 0) flush_tile<FMT, MT>(p, cur_t, nch, acc, lane);
-}
-
-// --------------------------------------------------------------------------
-// LUT-driven GEMV for a caller-supplied TL1/TL2 LUT (kernels.py:109-157).
-// lane = row; each warp walks a slice of one row tile's chunks.
-// --------------------------------------------------------------------------
-template <int FMT>
-__global__ void gemv_lut_kernel(const uint8_t *__restrict__ tiled,
-                                const uint8_t *__restrict__ tiled_sign, int N, int C,
-                                const int16_t *__restrict__ lut, int64_t groups,
-                                int chunks_per_warp, int32_t *__restrict__ acc_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int splits = (C + chunks_per_warp - 1) / chunks_per_warp;
-  const int64_t t = wid / splits;
-  const int cb = (int)(wid % splits) * chunks_per_warp;
-  const int64_t T = (N + kRowTile - 1) / kRowTile;
-  if (t >= T) return;
-  const int row = (int)(t * kRowTile + lane);
-  int32_t acc = 0;
-  const int ce = min(C, cb + chunks_per_warp);
-  for (int c = cb; c < ce; ++c) {
-    const uint8_t *src = tiled + ((t * C + c) * kRowTile + lane) * 16;
-    uint32_t sg = 0;
-    if (FMT == TB_TL2)
-      sg = *reinterpret_cast<const uint32_t *>(tiled_sign + ((t * C + c) * kRowTile + lane) * 4);
-    for (int b = 0; b < 16; ++b) {
-      const uint32_t byte = src[b];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t g = (int64_t)c * 32 + 2 * b + h;  // pair / triple index
-        const uint32_t idx = h ? (byte >> 4) : (byte & 15);
-        if (g >= groups) continue;
-        if (FMT == TB_TL1) {
-          if (idx <= 8) acc += lut[g * 9 + idx];
-        } else {
-          if (idx <= 13) {
-            const int32_t e = lut[g * 14 + idx];
-            acc += ((sg >> (2 * b + h)) & 1) ? -e : e;
+      nch += kStageChunks;
+      cur.c += kStageChunks;
+    } else {
+      for (int j = 0; j < nk; ++j) {
+        if (cur.c == C) {  // next row tile (or next job)
+          flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
+          nch = 0;
+          acc.zero();
+          cur.c = 0;
+          if (++cur.t >= T) {
+            ++cur.j;
+            cur.t = 0;
+            const GemvJob J = job_at(b, cur.j);
+            C = J.C;
+            M = J.M;
+            T = (J.end - J.start) / J.C;
           }
         }
+        const uint4 w4 = *reinterpret_cast<const uint4 *>(slot + j * kTileChunkBytes + lane * 16);
+        uint32_t sg = 0;
+        if (FMT == TB_TL2)
+          sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
+        process_chunk<FMT, MT>(w4, sg, slot_act + j * F::kRecBytes, M, acc);
+        ++nch;
+        ++cur.c;
       }
     }
+    if (cur.c == C && k + 1 < nst) {  // tile finished exactly at a stage boundary
+      flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
+      nch = 0;
+      acc.zero();
+      cur.c = 0;
+      if (++cur.t >= T) {
+        ++cur.j;
+        cur.t = 0;
+        const GemvJob J = job_at(b, cur.j);
+        C = J.C;
+        M = J.M;
+        T = (J.end - J.start) / J.C;
+      }
+    }
+    __syncwarp();  // every lane is done reading the slot before it is refilled
+    if (k + kRing < nst) is.issue<FMT>(b, min(kStageChunks, n - (k + kRing) * kStageChunks), slot, lane);
+    cp_async_commit();
   }
-  if (row < N && acc != 0) atomicAdd(acc_out + row, acc);
-}
-
-__global__ void gemv_ref_int32_kernel(const int8_t *__restrict__ v, int64_t rows, int64_t cols,
-                                      const int8_t *__restrict__ a, int32_t *__restrict__ out) {
-  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  int32_t s = 0;
-  for (int64_t k = lane; k < cols; k += 32) s += (int32_t)v[r * cols + k] * (int32_t)a[k];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[r] = s;
-}
-
-__global__ void gemv_f32_ref_kernel(const int8_t *__restrict__ v, int64_t rows, int64_t cols,
-                                    float ws, const float *__restrict__ x,
-                                    float *__restrict__ out) {
-  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  float s = 0.f;
-  for (int64_t k = lane; k < cols; k += 32) s += (static_cast<float>(v[r * cols + k]) * ws) * x[k];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[r] = s;
+  TL_MARK(3);
+  if (nch > 0) flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
+  TL_MARK(4);
 }
 
 // --------------------------------------------------------------------------
 // host side
 // --------------------------------------------------------------------------
-template <int FMT, int MT>
-static int launch_tgemv(const GemvParams &p, cudaStream_t s, int grid) {
-  static bool configured = false;
-  const size_t smem = gemv_smem_bytes<FMT>(p.M, p.Cs);
-  if (!configured) {
-    if (cudaFuncSetAttribute(tgemv_kernel<FMT, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024) != cudaSuccess)
-      return TB_ERR_CUDA;
-    configured = true;
-  }
-  tgemv_kernel<FMT, MT><<<grid, kThreads, smem, s>>>(p);
-  TB_CHECK_LAUNCH();
+
+// The finalize kernel is launched as a programmatic dependent of the GEMV, so
+// its launch latency overlaps the GEMV (it waits in griddepcontrol.wait).
+static int launch_finalize(const GemvBatch &b, cudaStream_t s) {
+  int64_t rows = 0;
+  for (int j = 0; j < b.njobs && !b.table; ++j) rows += (int64_t)b.jobs[j].M * b.jobs[j].Npad;
+  if (b.table) rows = (int64_t)b.njobs * 16 * 1024;  // device table: size unknown on the host
+  const int threads = 256;
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)sm_count_cached() * 4, ceil_div(rows, threads)));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, gemv_finalize_kernel, b) != cudaSuccess) return TB_ERR_CUDA;
   return TB_OK;
 }
 
+template <int FMT, int MT>
+static int launch_tgemv(GemvBatch &b, cudaStream_t s) {
+  using CF = Cfg<FMT, MT>;
+  static int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    if (cudaFuncSetAttribute(tgemv_kernel<FMT, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             CF::kSmem) != cudaSuccess)
+      return TB_ERR_CUDA;
+    configured_dev = dev;
+  }
+  // spread over every SM (latency-bound sizes want the parallelism), one CTA
+  // per SM, at least one chunk per warp
+  const int64_t want = ceil_div(b.total, (int64_t)CF::kWarps);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count_cached(), want));
+  const int nw = grid * CF::kWarps;
+  b.base = b.total / nw;
+  b.rem = b.total % nw;
+  // programmatic dependent launch: the prologue (job lookup, first weight
+  // stages) overlaps the tail of the kernel that produced the records
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(CF::kThreads);
+  cfg.dynamicSmemBytes = CF::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, tgemv_kernel<FMT, MT>, b) != cudaSuccess) return TB_ERR_CUDA;
+  return launch_finalize(b, s);
+}
+
 template <int FMT>
-static int dispatch_m(const GemvParams &p, cudaStream_t s, int grid) {
-  if (p.M <= 1) return launch_tgemv<FMT, 1>(p, s, grid);
-  if (p.M <= 2) return launch_tgemv<FMT, 2>(p, s, grid);
-  if (p.M <= 4) return launch_tgemv<FMT, 4>(p, s, grid);
-  if (p.M <= 8) return launch_tgemv<FMT, 8>(p, s, grid);
-  return launch_tgemv<FMT, 16>(p, s, grid);
+static int dispatch_m(GemvBatch &b, int maxM, cudaStream_t s) {
+  if (maxM <= 1) return launch_tgemv<FMT, 1>(b, s);
+  if (maxM <= 2) return launch_tgemv<FMT, 2>(b, s);
+  if (maxM <= 4) return launch_tgemv<FMT, 4>(b, s);
+  if (maxM <= 8) return launch_tgemv<FMT, 8>(b, s);
+  return launch_tgemv<FMT, 16>(b, s);
+}
+
+static int rec_bytes_of(int fmt) {
+  return fmt == TB_TL2 ? Fmt<TB_TL2>::kRecBytes : Fmt<TB_I2S>::kRecBytes;
+}
+
+static int64_t ws_counts_bytes(int64_t rows) {
+  const int64_t T = ceil_div(rows, kRowTile);
+  return pad_up((16 * T * kRowTile + T) * (int64_t)sizeof(int32_t), 256);
+}
+
+// Fill one job; returns TB_OK or an error.
+static int make_job(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign, int64_t rows,
+                    int64_t cols, const uint8_t *rec, int64_t M, const double *a_scale,
+                    double w_scale, void *workspace, int32_t *acc_out, double *out64,
+                    float *out32, int64_t start, GemvJob &J) {
+  if (!tiled || !rec || !workspace || rows < 1 || cols < 1 || M < 1 || M > 16 ||
+      (fmt == TB_TL2 && !tiled_sign) || ((out64 || out32) && !a_scale) ||
+      (reinterpret_cast<uintptr_t>(rec) & 15) || (reinterpret_cast<uintptr_t>(tiled) & 15))
+    return TB_ERR_ARGUMENT;
+  const int64_t C = ceil_div(ref_row_bytes(fmt, cols), kChunkBytes);
+  const int64_t T = ceil_div(rows, kRowTile);
+  if (start + T * C >= ((int64_t)1 << 31)) return TB_ERR_UNSUPPORTED;
+  J.wmain = tiled;
+  J.wsign = tiled_sign;
+  J.rec = rec;
+  J.a_scale = a_scale;
+  J.w_scale = w_scale;
+  J.ws_acc = static_cast<int32_t *>(workspace);
+  J.ws_cnt = J.ws_acc + 16 * T * kRowTile;
+  J.acc_out = acc_out;
+  J.out64 = out64;
+  J.out32 = out32;
+  J.N = (int)rows;
+  J.Npad = (int)(T * kRowTile);
+  J.C = (int)C;
+  J.M = (int)M;
+  J.start = (int)start;
+  J.end = (int)(start + T * C);
+  return TB_OK;
+}
+
+static int launch_batch(int fmt, GemvBatch &b, int maxM, cudaStream_t s) {
+  if (fmt == TB_I2S) return dispatch_m<TB_I2S>(b, maxM, s);
+  if (fmt == TB_TL1) return dispatch_m<TB_TL1>(b, maxM, s);
+  if (fmt == TB_TL2) return dispatch_m<TB_TL2>(b, maxM, s);
+  return TB_ERR_ARGUMENT;
 }
 
 }  // namespace tb
 
 using namespace tb;
 
+extern "C" int64_t tb_act_records_bytes(int fmt, int64_t M, int64_t cols) {
+  if (M < 1 || cols < 1 || fmt < TB_I2S || fmt > TB_TL2) return -1;
+  const int64_t C = ceil_div(ref_row_bytes(fmt, cols), kChunkBytes);
+  return M * C * rec_bytes_of(fmt);
+}
+
+extern "C" int tb_prep_activations(int fmt, const int8_t *act, int64_t M, int64_t ld_act,
+                                   int64_t act_len, int64_t cols, uint8_t *rec, void *stream) {
+  if (!act || !rec || M < 1 || M > 16 || cols < 1 || act_len < 0 || act_len > ld_act ||
+      fmt < TB_I2S || fmt > TB_TL2 || (reinterpret_cast<uintptr_t>(rec) & 15))
+    return TB_ERR_ARGUMENT;
+  const int64_t C = ceil_div(ref_row_bytes(fmt, cols), kChunkBytes);
+  const int64_t n4 = M * C * 4;
+  const int64_t cap = (int64_t)sm_count_cached() * 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cap, ceil_div(n4, 256)));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (fmt == TB_I2S)
+    act_prep_kernel<TB_I2S><<<grid, 256, 0, s>>>(act, (int)M, ld_act, act_len, (int)C, rec);
+  else if (fmt == TB_TL1)
+    act_prep_kernel<TB_TL1><<<grid, 256, 0, s>>>(act, (int)M, ld_act, act_len, (int)C, rec);
+  else
+    act_prep_kernel<TB_TL2><<<grid, 256, 0, s>>>(act, (int)M, ld_act, act_len, (int)C, rec);
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+template <int FMT, typename T>
+static void launch_qrec(const T *x, int64_t M, int64_t K, int64_t ldx, int8_t *q, int64_t ldq,
+                        double *scale, int C, uint8_t *rec, int32_t *flag, cudaStream_t s) {
+  if (K <= 8192)
+    quantize_records_kernel<FMT, T, 512><<<(unsigned)M, 512, 0, s>>>(x, K, ldx, q, ldq, scale, C,
+                                                                     rec, flag);
+  else
+    quantize_records_kernel<FMT, T, 1024><<<(unsigned)M, 1024, 0, s>>>(x, K, ldx, q, ldq, scale,
+                                                                       C, rec, flag);
+}
+
+template <typename T>
+static int qrec_impl(int fmt, const T *x, int64_t M, int64_t K, int64_t ldx, int8_t *q,
+                     int64_t ldq, double *scale, uint8_t *rec, int32_t *flag, void *stream) {
+  if (!x || !scale || !rec || M < 1 || K < 1 || ldx < K || (q && ldq < K) || fmt < TB_I2S ||
+      fmt > TB_TL2 || (reinterpret_cast<uintptr_t>(rec) & 15))
+    return TB_ERR_ARGUMENT;
+  const int C = (int)ceil_div(ref_row_bytes(fmt, K), kChunkBytes);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (fmt == TB_I2S) launch_qrec<TB_I2S>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
+  else if (fmt == TB_TL1) launch_qrec<TB_TL1>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
+  else launch_qrec<TB_TL2>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+extern "C" int tb_quantize_records_f32(int fmt, const float *x, int64_t M, int64_t K, int64_t ldx,
+                                       int8_t *q, int64_t ldq, double *scale, uint8_t *rec,
+                                       int32_t *flag, void *stream) {
+  return qrec_impl(fmt, x, M, K, ldx, q, ldq, scale, rec, flag, stream);
+}
+
+extern "C" int tb_quantize_records_f64(int fmt, const double *x, int64_t M, int64_t K,
+                                       int64_t ldx, int8_t *q, int64_t ldq, double *scale,
+                                       uint8_t *rec, int32_t *flag, void *stream) {
+  return qrec_impl(fmt, x, M, K, ldx, q, ldq, scale, rec, flag, stream);
+}
+
 extern "C" int64_t tb_gemv_workspace_bytes(int fmt, int64_t rows, int64_t cols) {
   if (rows < 1 || cols < 1 || fmt < TB_I2S || fmt > TB_TL2) return -1;
-  const int64_t T = ceil_div(rows, kRowTile);
-  return (16 * T * kRowTile + T) * (int64_t)sizeof(int32_t);
+  return ws_counts_bytes(rows) + tb_act_records_bytes(fmt, 16, cols);
+}
+
+extern "C" int tb_gemv_records(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
+                               int64_t rows, int64_t cols, const uint8_t *rec, int64_t M,
+                               const double *a_scale, double w_scale, void *workspace,
+                               int32_t *acc_out, double *out64, float *out32, void *stream) {
+  if (fmt < TB_I2S || fmt > TB_TL2) return TB_ERR_ARGUMENT;
+  GemvBatch b{};
+  int st = make_job(fmt, tiled, tiled_sign, rows, cols, rec, M, a_scale, w_scale, workspace,
+                    acc_out, out64, out32, 0, b.jobs[0]);
+  if (st != TB_OK) return st;
+  b.njobs = 1;
+  b.total = b.jobs[0].end;
+  return launch_batch(fmt, b, (int)M, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int64_t tb_gemv_job_bytes(void) { return (int64_t)sizeof(GemvJob); }
+
+extern "C" int tb_gemv_batch_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
+                                     void *table_host, int64_t *total_chunks, int32_t *max_m) {
+  if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !descs || !table_host || !total_chunks ||
+      !max_m)
+    return TB_ERR_ARGUMENT;
+  GemvJob *host = static_cast<GemvJob *>(table_host);
+  int64_t start = 0;
+  int maxM = 1;
+  for (int64_t j = 0; j < njobs; ++j) {
+    const tb_gemv_desc &d = descs[j];
+    int st = make_job(fmt, d.tiled, d.tiled_sign, d.rows, d.cols, d.rec, d.M, d.a_scale,
+                      d.w_scale, d.workspace, d.acc_out, d.out64, d.out32, start, host[j]);
+    if (st != TB_OK) return st;
+    start = host[j].end;
+    maxM = std::max(maxM, (int)d.M);
+  }
+  *total_chunks = start;
+  *max_m = maxM;
+  return TB_OK;
+}
+
+extern "C" int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t njobs,
+                                    int64_t total_chunks, int32_t max_m, void *stream) {
+  if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !table_device || total_chunks < 1 ||
+      total_chunks >= ((int64_t)1 << 31) || max_m < 1 || max_m > 16)
+    return TB_ERR_ARGUMENT;
+  GemvBatch b{};
+  b.table = static_cast<const GemvJob *>(table_device);
+  b.njobs = (int)njobs;
+  b.total = (int)total_chunks;
+  return launch_batch(fmt, b, max_m, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign, int64_t rows,
@@ -444,86 +688,23 @@ extern "C" int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
                        int64_t act_len, const double *a_scale, double w_scale, void *workspace,
                        int32_t *acc_out, double *out64, float *out32, void *stream) {
   if (!tiled || !act || !workspace || rows < 1 || cols < 1 || M < 1 || M > 16 || ld_act < 1 ||
-      act_len < 0 || act_len > ld_act || (fmt == TB_TL2 && !tiled_sign) ||
-      ((out64 || out32) && !a_scale) || fmt < TB_I2S || fmt > TB_TL2)
+      act_len < 0 || act_len > ld_act || fmt < TB_I2S || fmt > TB_TL2)
     return TB_ERR_ARGUMENT;
-  if (rows > (int64_t)1 << 30) return TB_ERR_UNSUPPORTED;
-  const int64_t C = ceil_div(ref_row_bytes(fmt, cols), kChunkBytes);
-  const int64_t T = ceil_div(rows, kRowTile);
-  const int act_words = fmt == TB_TL2 ? 24 : 16;
-  // split K into passes so the staged activations fit the SMEM budget
-  const int64_t per_chunk = M * (act_words * 4 + 4);
-  const int64_t passes = ceil_div(C * per_chunk, kActSmemBudget);
-  const int64_t Cs_nom = ceil_div(C, passes);
-  GemvParams p{};
-  p.wmain = tiled;
-  p.wsign = tiled_sign;
-  p.act = act;
-  p.ld_act = ld_act;
-  p.act_len = act_len;
-  p.a_scale = a_scale;
-  p.w_scale = w_scale;
-  p.ws_acc = static_cast<int32_t *>(workspace);
-  p.ws_cnt = p.ws_acc + 16 * T * kRowTile;
-  p.acc_out = acc_out;
-  p.out64 = out64;
-  p.out32 = out32;
-  p.N = (int)rows;
-  p.Npad = (int)(T * kRowTile);
-  p.T = (int)T;
-  p.C = (int)C;
-  p.M = (int)M;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int64_t c0 = 0; c0 < C; c0 += Cs_nom) {
-    p.c0 = (int)c0;
-    p.Cs = (int)std::min<int64_t>(Cs_nom, C - c0);
-    p.total = T * p.Cs;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count_cached(), p.total));
-    int st;
-    if (fmt == TB_I2S) st = dispatch_m<TB_I2S>(p, s, grid);
-    else if (fmt == TB_TL1) st = dispatch_m<TB_TL1>(p, s, grid);
-    else st = dispatch_m<TB_TL2>(p, s, grid);
-    if (st != TB_OK) return st;
-  }
-  return TB_OK;
+  uint8_t *rec = static_cast<uint8_t *>(workspace) + ws_counts_bytes(rows);
+  int st = tb_prep_activations(fmt, act, M, ld_act, act_len, cols, rec, stream);
+  if (st != TB_OK) return st;
+  return tb_gemv_records(fmt, tiled, tiled_sign, rows, cols, rec, M, a_scale, w_scale, workspace,
+                         acc_out, out64, out32, stream);
 }
 
-extern "C" int tb_gemv_lut(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
-                           int64_t rows, int64_t cols, const int16_t *lut, int64_t groups,
-                           int32_t *acc_out, void *stream) {
-  if (!tiled || !lut || !acc_out || rows < 1 || cols < 1 || groups < 1 ||
-      (fmt != TB_TL1 && fmt != TB_TL2) || (fmt == TB_TL2 && !tiled_sign))
-    return TB_ERR_ARGUMENT;
-  const int64_t C = ceil_div(ref_row_bytes(fmt, cols), kChunkBytes);
-  const int64_t T = ceil_div(rows, kRowTile);
-  const int cpw = 8;
-  const int64_t warps = T * ceil_div(C, cpw);
-  const int64_t blocks = ceil_div(warps * 32, 256);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (fmt == TB_TL1)
-    gemv_lut_kernel<TB_TL1><<<(unsigned)blocks, 256, 0, s>>>(tiled, tiled_sign, (int)rows, (int)C,
-                                                             lut, groups, cpw, acc_out);
-  else
-    gemv_lut_kernel<TB_TL2><<<(unsigned)blocks, 256, 0, s>>>(tiled, tiled_sign, (int)rows, (int)C,
-                                                             lut, groups, cpw, acc_out);
-  TB_CHECK_LAUNCH();
-  return TB_OK;
+#ifdef TB_TIMELINE
+extern "C" int tb_timeline_fetch(void *host, int64_t bytes) {
+  if (bytes > (int64_t)sizeof(g_timeline)) bytes = sizeof(g_timeline);
+  return cudaMemcpyFromSymbol(host, g_timeline, bytes) == cudaSuccess ? TB_OK : TB_ERR_CUDA;
 }
-
-extern "C" int tb_gemv_ref_int32(const int8_t *values, int64_t rows, int64_t cols,
-                                 const int8_t *act, int32_t *acc_out, void *stream) {
-  if (!values || !act || !acc_out || rows < 1 || cols < 1) return TB_ERR_ARGUMENT;
-  gemv_ref_int32_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0,
-                          static_cast<cudaStream_t>(stream)>>>(values, rows, cols, act, acc_out);
-  TB_CHECK_LAUNCH();
-  return TB_OK;
+extern "C" int tb_timeline_clear(void) {
+  void *p = nullptr;
+  if (cudaGetSymbolAddress(&p, g_timeline) != cudaSuccess) return TB_ERR_CUDA;
+  return cudaMemset(p, 0, sizeof(g_timeline)) == cudaSuccess ? TB_OK : TB_ERR_CUDA;
 }
-
-extern "C" int tb_gemv_f32_ref(const int8_t *values, int64_t rows, int64_t cols, float w_scale,
-                               const float *x, float *out, void *stream) {
-  if (!values || !x || !out || rows < 1 || cols < 1) return TB_ERR_ARGUMENT;
-  gemv_f32_ref_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0,
-                        static_cast<cudaStream_t>(stream)>>>(values, rows, cols, w_scale, x, out);
-  TB_CHECK_LAUNCH();
-  return TB_OK;
-}
+#endif

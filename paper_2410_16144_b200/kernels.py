@@ -30,7 +30,8 @@ from .lut import LutTL1, LutTL2, build_lut_tl1, build_lut_tl2  # noqa: F401
 from .packing import PackedI2S, PackedTL1, PackedTL2
 
 __all__ = ["KernelKind", "WIDEN_GROUPS", "gemv_ref_int32", "gemv_f32_ref", "gemv_i2s",
-           "gemv_tl1", "gemv_tl2", "gemv_parallel", "GemvPlan", "KERNEL_PAD"]
+           "gemv_tl1", "gemv_tl2", "gemv_parallel", "GemvPlan", "GemvBatch", "ActRecords",
+           "KERNEL_PAD"]
 
 WIDEN_GROUPS = 64  # kernels.py:34
 MAX_DECODE_TOKENS = 16
@@ -220,6 +221,7 @@ class GemvPlan:
         self._lib = L.load()
 
     def run(self, act: torch.Tensor, scales: torch.Tensor, stream_ptr: int | None = None):
+        """Natural int8 activations [M, K] (prep + GEMV: two launches)."""
         M, K = act.shape
         st = self._lib.tb_gemv(self.p.FMT, self.main.data_ptr(),
                                self.sign.data_ptr() if self.sign is not None else None,
@@ -230,3 +232,119 @@ class GemvPlan:
         if st:
             L.check(st, "gemv")
         return self.out32 if self.out32 is not None else self.out64
+
+    def run_records(self, rec: "ActRecords", stream_ptr: int | None = None):
+        """Prepared activation records (one launch)."""
+        st = self._lib.tb_gemv_records(self.p.FMT, self.main.data_ptr(),
+                                       self.sign.data_ptr() if self.sign is not None else None,
+                                       self.p.rows, self.p.cols, rec.buf.data_ptr(), rec.M,
+                                       rec.scales.data_ptr(), float(self.p.scale),
+                                       self.ws.data_ptr(), L.ptr(self.acc), L.ptr(self.out64),
+                                       L.ptr(self.out32),
+                                       stream_ptr if stream_ptr is not None else L.stream_ptr())
+        if st:
+            L.check(st, "gemv_records")
+        return self.out32 if self.out32 is not None else self.out64
+
+
+class GemvBatch:
+    """Several independent decode GEMVs of one format in ONE launch.
+
+    ``pairs`` is a list of (GemvPlan, ActRecords); the job table is built once
+    (tb_gemv_batch_prepare) and kept on the device, so ``run`` is a single
+    capture-safe launch.  Outputs land in each plan's buffers.
+    """
+
+    def __init__(self, pairs):
+        import ctypes as C
+        import numpy as np
+
+        lib = L.load()
+        fmts = {p.p.FMT for p, _ in pairs}
+        if len(fmts) != 1:
+            raise ValueError("one format per batch")
+        self.fmt = fmts.pop()
+        descs = (L.GemvDesc * len(pairs))()
+        for d, (plan, rec) in zip(descs, pairs):
+            d.tiled = plan.main.data_ptr()
+            d.tiled_sign = plan.sign.data_ptr() if plan.sign is not None else None
+            d.rows, d.cols = plan.p.rows, plan.p.cols
+            d.rec, d.M = rec.buf.data_ptr(), rec.M
+            d.a_scale, d.w_scale = rec.scales.data_ptr(), float(plan.p.scale)
+            d.workspace = plan.ws.data_ptr()
+            d.acc_out = L.ptr(plan.acc)
+            d.out64 = L.ptr(plan.out64)
+            d.out32 = L.ptr(plan.out32)
+        jb = lib.tb_gemv_job_bytes()
+        host = np.zeros(jb * len(pairs), dtype=np.uint8)
+        total = C.c_int64()
+        maxm = C.c_int32()
+        L.check(lib.tb_gemv_batch_prepare(self.fmt, len(pairs), C.cast(descs, C.c_void_p),
+                                          host.ctypes.data_as(C.c_void_p), C.byref(total),
+                                          C.byref(maxm)), "gemv_batch_prepare")
+        dev = pairs[0][0].main.device
+        self.table = torch.from_numpy(host).to(dev)
+        self.njobs, self.total, self.max_m = len(pairs), total.value, maxm.value
+        self.pairs = pairs  # keep every buffer alive
+        self._lib = lib
+
+    def run(self, stream_ptr: int | None = None):
+        st = self._lib.tb_gemv_batch_launch(self.fmt, self.table.data_ptr(), self.njobs,
+                                            self.total, self.max_m,
+                                            stream_ptr if stream_ptr is not None
+                                            else L.stream_ptr())
+        if st:
+            L.check(st, "gemv_batch_launch")
+
+
+class ActRecords:
+    """Device buffer of GEMV-ready activation records for M tokens of length K
+    in one packed format (shared by every GEMV that consumes the same input)."""
+
+    def __init__(self, fmt: int, M: int, K: int, device=None, keep_natural_pad: int = 0):
+        lib = L.load()
+        self.fmt, self.M, self.K = fmt, M, K
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        nbytes = lib.tb_act_records_bytes(fmt, M, K)
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.scales = torch.empty(M, dtype=torch.float64, device=dev)
+        self.natural = None
+        if keep_natural_pad:
+            kp = -(-K // keep_natural_pad) * keep_natural_pad
+            self.natural = torch.empty((M, kp), dtype=torch.int8, device=dev)
+        self._lib = lib
+
+    def quantize(self, x: torch.Tensor, stream_ptr: int | None = None, flag=None):
+        """x [M, K] float32/float64 on the device -> scales + records (one launch)."""
+        fn = (self._lib.tb_quantize_records_f32 if x.dtype == torch.float32
+              else self._lib.tb_quantize_records_f64)
+        nat = self.natural
+        st = fn(self.fmt, x.data_ptr(), self.M, self.K, x.stride(0), L.ptr(nat),
+                nat.stride(0) if nat is not None else 0, self.scales.data_ptr(),
+                self.buf.data_ptr(), L.ptr(flag),
+                stream_ptr if stream_ptr is not None else L.stream_ptr())
+        if st:
+            L.check(st, "quantize_records")
+        return self
+
+    def prep(self, act: torch.Tensor, stream_ptr: int | None = None):
+        """Natural int8 activations [M, K'] (K' >= K, zero beyond K) -> records."""
+        st = self._lib.tb_prep_activations(self.fmt, act.data_ptr(), self.M, act.stride(0),
+                                           act.shape[1], self.K, self.buf.data_ptr(),
+                                           stream_ptr if stream_ptr is not None else L.stream_ptr())
+        if st:
+            L.check(st, "prep_activations")
+        return self
+
+    def chunk_slice(self, c0: int, c1: int) -> "ActRecords":
+        """Records of chunks [c0, c1) (one token): the input of a K-sharded
+        (row-parallel) GEMV whose shard starts at chunk c0."""
+        if self.M != 1:
+            raise ValueError("chunk_slice needs a single-token record buffer")
+        rb = 112 if self.fmt == L.TL2 else 80
+        v = object.__new__(ActRecords)
+        v.fmt, v.M, v._lib, v.natural = self.fmt, 1, self._lib, None
+        v.K = self.K
+        v.buf = self.buf[c0 * rb: c1 * rb]
+        v.scales = self.scales
+        return v

@@ -1,0 +1,13 @@
+#!/bin/bash
+# Build a timeline-instrumented variant of the library with extra -D flags:
+#   tools/build_variant.sh NAME -DTB_MT1_RING=2 ...   -> tools/lib_NAME.so
+set -e
+name=$1; shift
+out=/tmp/variant_$name; mkdir -p $out
+for f in abi quantize pack gemv gemv_aux; do
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -DTB_TIMELINE "$@" \
+    -c paper_2410_16144_b200/csrc/$f.cu -o $out/$f.o &
+done
+wait
+nvcc -gencode arch=compute_100a,code=sm_100a -shared $out/*.o -o tools/lib_$name.so
+echo tools/lib_$name.so

@@ -1,0 +1,65 @@
+"""Per-warp timeline of one decode-GEMV launch (debug library built with
+-DTB_TIMELINE into tools/libternary_b200_timeline.so).
+
+Marks: 0 entry, 1 first stages issued, 2 first stage landed, 3 compute done,
+4 flush done.  Prints quantiles of each mark relative to the earliest entry.
+"""
+
+import argparse
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2410_16144_b200 import _lib as L  # noqa: E402
+
+lib = L.load(os.environ.get("TB_LIB", os.path.join(ROOT, "tools", "libternary_b200_timeline.so")))
+lib.tb_timeline_fetch.argtypes = [C.c_void_p, C.c_int64]
+lib.tb_timeline_clear.argtypes = []
+
+import torch  # noqa: E402
+
+import paper_2410_16144_b200 as tb  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--fmt", default="tl1")
+    ap.add_argument("--rows", type=int, default=14336)
+    ap.add_argument("--cols", type=int, default=4096)
+    a = ap.parse_args()
+    enc = {"i2s": tb.encode_i2s, "tl1": tb.encode_tl1, "tl2": tb.encode_tl2}[a.fmt]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    plans = []
+    for c in range(4):
+        w = torch.randn(a.rows, a.cols, generator=g, device="cuda") * 0.02
+        plans.append(tb.GemvPlan(enc(tb.ternarize_weights(w, a.rows, a.cols))))
+    x = torch.randn(1, a.cols, generator=g, device="cuda")
+    rec = tb.ActRecords(plans[0].p.FMT, 1, a.cols).quantize(x)
+    for i in range(6):
+        plans[i % 4].run_records(rec)
+    torch.cuda.synchronize()
+    for trial in range(3):
+        lib.tb_timeline_clear()
+        torch.cuda.synchronize()
+        plans[trial % 4].run_records(rec)
+        torch.cuda.synchronize()
+        buf = np.zeros((148 * 32, 5), dtype=np.uint64)
+        lib.tb_timeline_fetch(buf.ctypes.data_as(C.c_void_p), buf.nbytes)
+        used = buf[:, 0] > 0
+        t = buf[used].astype(np.int64)
+        t0 = t[:, 0].min()
+        rel = (t - t0) / 1000.0
+        print(f"trial {trial}: {used.sum()} warps; us since first entry  (min / p50 / p90 / max)")
+        for k, name in enumerate(["entry", "bar init", "first data", "compute done", "flushed"]):
+            col = rel[:, k]
+            print(f"  {name:13s} {col.min():7.2f} {np.median(col):7.2f} "
+                  f"{np.quantile(col, 0.9):7.2f} {col.max():7.2f}")
+
+
+if __name__ == "__main__":
+    main()
