@@ -253,22 +253,34 @@ def run_gpu(args, rank, world):
         pl["batch"] = tb.GemvBatch([(pl["gate"], rec_h), (pl["up"], rec_h),
                                     (pl["down"], rec_i_loc)])
 
-    def step(i):
+    # A decode step is TWO launches: one glue kernel (finalise the previous
+    # step's group -- scales -> outputs -- and quantise this step's inputs
+    # into records) and one grouped GEMV (gate+up+down).  With tp > 1 the
+    # down projection's int32 partials are all-reduced before finalising.
+    glues = [tb.StepGlue([(XH[j:j + 1], rec_h), (XI[j:j + 1], rec_i)]) for j in range(NX)]
+    tail = tb.StepGlue([])
+
+    def step(i, prev):
         pl = plans[i % NCOPY]
-        rec_h.quantize(XH[i % NX: i % NX + 1])
-        rec_i.quantize(XI[i % NX: i % NX + 1])
-        pl["batch"].run()
+        glues[i % NX].retarget(prev["batch"] if prev is not None else None).run()
+        pl["batch"].run(finalize=(tp > 1))
         if tp > 1:
             dist.all_reduce(pl["down"].acc, op=dist.ReduceOp.SUM)
             L.check(L.load().tb_scale_outputs(
                 pl["down"].acc.data_ptr(), 1, H, float(pl["mats"]["down"].scale),
                 rec_i.scales.data_ptr(), None, out_down.data_ptr(), L.stream_ptr()), "scale")
+        return None if tp > 1 else pl
 
-    launches_per_step = 3 + (1 if tp > 1 else 0)
+    def run_steps(n):
+        prev = None
+        for i in range(n):
+            prev = step(i, prev)
+        tail.retarget(prev["batch"] if prev is not None else None).run()  # last finalise
+
+    launches_per_step = 2 + (1 if tp > 1 else 0)  # glue + grouped GEMV (+ scale for tp)
 
     # ---- warm-up (eager, also configures kernel attributes before capture)
-    for i in range(max(args.warmup, NCOPY)):
-        step(i)
+    run_steps(max(args.warmup, NCOPY))
     torch.cuda.synchronize()
 
     # ---- device-resident timed region: K steps in one CUDA graph
@@ -277,8 +289,7 @@ def run_gpu(args, rank, world):
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
         with torch.cuda.graph(graph, stream=s):
-            for i in range(args.steps):
-                step(i)
+            run_steps(args.steps)
     torch.cuda.synchronize()
     graph.replay()  # untimed replay (first replay uploads the graph)
     torch.cuda.synchronize()

@@ -182,8 +182,30 @@ typedef struct tb_gemv_desc {
 int64_t tb_gemv_job_bytes(void);
 int tb_gemv_batch_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
                           void *table_host, int64_t *total_chunks, int32_t *max_m);
+/* finalize != 0: also launch the finalize pass (scales -> outputs, workspace
+ * reset); 0: the caller finalises, e.g. inside the next tb_step_glue.       */
 int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t njobs,
-                         int64_t total_chunks, int32_t max_m, void *stream);
+                         int64_t total_chunks, int32_t max_m, int32_t finalize,
+                         void *stream);
+
+/* Decode-step glue in ONE launch: finalise a prepared GEMV batch (may be
+ * empty: fin_njobs = 0) and quantise up to 4 activation matrices into
+ * records (quantize_activations, core.py:116-134, one 8-CTA cluster per
+ * token).  Both halves are independent, so a decode step is
+ * glue(previous outputs, next inputs) + one grouped GEMV launch.            */
+typedef struct tb_quant_desc {
+  const void *x; /* [M][ldx] float32 or float64 (x_is_f64)                  */
+  int32_t x_is_f64;
+  int32_t fmt; /* record layout of the consuming GEMVs                     */
+  int64_t M, K, ldx;
+  int8_t *q; /* optional natural codes [M][ldq]                             */
+  int64_t ldq;
+  double *scale;
+  uint8_t *rec;
+  int32_t *nonfinite_flag;
+} tb_quant_desc;
+int tb_step_glue(const void *fin_table_device, int64_t fin_njobs, int64_t nq,
+                 const tb_quant_desc *q, void *stream);
 /* Convenience: tb_prep_activations into the workspace + tb_gemv_records.   */
 int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
             int64_t rows, int64_t cols, const int8_t *act, int64_t M,

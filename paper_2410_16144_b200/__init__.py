@@ -23,6 +23,7 @@ from .kernels import (
     ActRecords,
     GemvBatch,
     GemvPlan,
+    StepGlue,
     KernelKind,
     gemv_f32_ref,
     gemv_i2s,

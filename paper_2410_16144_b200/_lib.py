@@ -54,7 +54,8 @@ _SIGS = {
                                _p]),
     "tb_gemv_job_bytes": (_i64, []),
     "tb_gemv_batch_prepare": (_i32, [_i32, _i64, _p, _p, _p, _p]),
-    "tb_gemv_batch_launch": (_i32, [_i32, _p, _i64, _i64, _i32, _p]),
+    "tb_gemv_batch_launch": (_i32, [_i32, _p, _i64, _i64, _i32, _i32, _p]),
+    "tb_step_glue": (_i32, [_p, _i64, _i64, _p, _p]),
     "tb_gemv_lut": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _p, _p]),
     "tb_gemv_ref_int32": (_i32, [_p, _i64, _i64, _p, _p, _p]),
     "tb_gemv_f32_ref": (_i32, [_p, _i64, _i64, _f32, _p, _p, _p]),
@@ -69,6 +70,14 @@ class GemvDesc(C.Structure):
     _fields_ = [("tiled", _p), ("tiled_sign", _p), ("rows", _i64), ("cols", _i64),
                 ("rec", _p), ("M", _i64), ("a_scale", _p), ("w_scale", _f64),
                 ("workspace", _p), ("acc_out", _p), ("out64", _p), ("out32", _p)]
+
+
+class QuantDesc(C.Structure):
+    """Mirror of tb_quant_desc (include/ternary_b200.h)."""
+
+    _fields_ = [("x", _p), ("x_is_f64", C.c_int32), ("fmt", C.c_int32), ("M", _i64),
+                ("K", _i64), ("ldx", _i64), ("q", _p), ("ldq", _i64), ("scale", _p),
+                ("rec", _p), ("nonfinite_flag", _p)]
 
 
 _lib = None

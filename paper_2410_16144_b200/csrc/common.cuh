@@ -128,6 +128,21 @@ __device__ __forceinline__ uint32_t lop3_sel(uint32_t p, uint32_t q, uint32_t m)
 // Round half away from zero in float64 exactly as core.py:24-27.
 __device__ __forceinline__ double rha(double v) { return trunc(v + copysign(0.5, v)); }
 
+// int8 code of one activation, bit-identical to clip(rha(x / s), -127, 127)
+// in float64 (core.py:24-27, 128-130) without a division per element: v' =
+// x * (1/s) is within a few ulp of the correctly rounded x / s, which decides
+// the same code unless v' sits within 1e-9 of a rounding tie (k + 0.5) -- then
+// the exact quotient is evaluated.  (|v| <= 127, so 1e-9 >> the few-ulp error.)
+__device__ __forceinline__ int quantize_one(double x, double s, double inv_s) {
+  const double v1 = x * inv_s;
+  const double a = fabs(v1);
+  const double f = a - floor(a);
+  const double v = fabs(f - 0.5) > 1e-9 ? v1 : x / s;
+  double y = rha(v);
+  y = fmin(fmax(y, -127.0), 127.0);
+  return static_cast<int>(y);
+}
+
 int sm_count_cached();
 
 }  // namespace tb

@@ -92,6 +92,7 @@ struct GemvBatch {
   int njobs;
   int total;  // flat chunks over all jobs
   int base, rem;  // warp w gets base + (w < rem) chunks
+  int defer_finalize;  // host: the caller finalises (e.g. in the next glue kernel)
 };
 
 // Job descriptor by value: inline jobs come from the (grid-constant) kernel
@@ -133,26 +134,84 @@ __device__ __forceinline__ void flush_tile(const GemvBatch &b, int j, int t,
 // 99-101), optional int32 / f32 copies, and the workspace is zeroed again.
 // Launched with programmatic dependent launch: griddepcontrol.wait blocks
 // until the GEMV grid has completed and its memory operations are visible.
-__global__ void gemv_finalize_kernel(const __grid_constant__ GemvBatch b) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  for (int j = 0; j < b.njobs; ++j) {
-    const GemvJob J = job_at(b, j);
-    const int64_t total = (int64_t)J.M * J.Npad;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      const int m = (int)(i / J.Npad), row = (int)(i - (int64_t)m * J.Npad);
-      const int32_t v = J.ws_acc[i];
-      J.ws_acc[i] = 0;
-      if (row < J.N) {
-        const int64_t o = (int64_t)m * J.N + row;
-        if (J.acc_out) J.acc_out[o] = v;
-        if (J.out64 || J.out32) {
-          const double y = static_cast<double>(v) * J.w_scale * J.a_scale[m];
-          if (J.out64) J.out64[o] = y;
-          if (J.out32) J.out32[o] = static_cast<float>(y);
-        }
+// Finalize job j with CTAs `part` of `nparts` (every thread of the CTA).
+__device__ __forceinline__ void finalize_job(const GemvBatch &b, int j, int part, int nparts) {
+  const GemvJob J = job_at(b, j);
+  const int64_t total = (int64_t)J.M * J.Npad;
+  for (int64_t i = part * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)nparts * blockDim.x) {
+    const int m = (int)(i / J.Npad), row = (int)(i - (int64_t)m * J.Npad);
+    const int32_t v = J.ws_acc[i];
+    J.ws_acc[i] = 0;
+    if (row < J.N) {
+      const int64_t o = (int64_t)m * J.N + row;
+      if (J.acc_out) J.acc_out[o] = v;
+      if (J.out64 || J.out32) {
+        const double y = static_cast<double>(v) * J.w_scale * J.a_scale[m];
+        if (J.out64) J.out64[o] = y;
+        if (J.out32) J.out32[o] = static_cast<float>(y);
       }
     }
+  }
+}
+
+// grid (parts, njobs): every job finalised concurrently.
+__global__ void gemv_finalize_kernel(const __grid_constant__ GemvBatch b) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  finalize_job(b, blockIdx.y, blockIdx.x, gridDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// "Glue" between two GEMV groups of a decode step, in ONE launch: finalize
+// the previous group (scales -> outputs, workspace reset) and quantise the
+// next group's input vectors into records.  Rows [0, q_tokens) of the grid
+// are per-token 8-CTA clusters (quantize_token), the remaining rows finalise
+// one job each.  Replaces 1 finalize + one quantise launch per input vector.
+// ---------------------------------------------------------------------------
+constexpr int kMaxGlueVecs = 4;
+
+struct QuantVec {
+  const void *x;
+  int8_t *qnat;
+  double *scale;
+  uint8_t *rec;
+  int32_t *flag;
+  int64_t K, ldx, ldq;
+  int M, C, fmt, is_f64;
+};
+
+struct GlueParams {
+  GemvBatch fin;  // fin.njobs == 0: nothing to finalise
+  QuantVec q[kMaxGlueVecs];
+  int nq, q_tokens;
+};
+
+template <int FMT>
+__device__ __forceinline__ void glue_quant(const QuantVec &Q, int m) {
+  if (Q.is_f64)
+    quantize_token<FMT, double, 256>(static_cast<const double *>(Q.x), Q.K, Q.ldx, Q.qnat, Q.ldq,
+                                     Q.scale, Q.C, Q.rec, Q.flag, m, blockIdx.x, gridDim.x);
+  else
+    quantize_token<FMT, float, 256>(static_cast<const float *>(Q.x), Q.K, Q.ldx, Q.qnat, Q.ldq,
+                                    Q.scale, Q.C, Q.rec, Q.flag, m, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueParams g) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the next GEMV group may launch now: its prologue prefetches weights (no
+  // dependence on us) and then waits for this grid before reading records
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int y = blockIdx.y;
+  if (y < g.q_tokens) {
+    int v = 0, m = y;
+    while (m >= g.q[v].M) {
+      m -= g.q[v].M;
+      ++v;
+    }
+    if (g.q[v].fmt == TB_TL2) glue_quant<TB_TL2>(g.q[v], m);
+    else glue_quant<TB_I2S>(g.q[v], m);  // I2_S and TL1 share the record layout
+  } else {
+    finalize_job(g.fin, y - g.q_tokens, blockIdx.x, gridDim.x);
   }
 }
 
@@ -449,15 +508,12 @@ __global__ void __launch_bounds__(Cfg<FMT, MT>::kThreads, 1)
 
 // The finalize kernel is launched as a programmatic dependent of the GEMV, so
 // its launch latency overlaps the GEMV (it waits in griddepcontrol.wait).
+constexpr int kFinalizeParts = 16;  // CTAs per job in the finalize pass
+
 static int launch_finalize(const GemvBatch &b, cudaStream_t s) {
-  int64_t rows = 0;
-  for (int j = 0; j < b.njobs && !b.table; ++j) rows += (int64_t)b.jobs[j].M * b.jobs[j].Npad;
-  if (b.table) rows = (int64_t)b.njobs * 16 * 1024;  // device table: size unknown on the host
   const int threads = 256;
-  const int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>((int64_t)sm_count_cached() * 4, ceil_div(rows, threads)));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3(kFinalizeParts, b.njobs);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
@@ -502,7 +558,7 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (cudaLaunchKernelEx(&cfg, tgemv_kernel<FMT, MT>, b) != cudaSuccess) return TB_ERR_CUDA;
-  return launch_finalize(b, s);
+  return b.defer_finalize ? TB_OK : launch_finalize(b, s);
 }
 
 template <int FMT>
@@ -592,14 +648,26 @@ extern "C" int tb_prep_activations(int fmt, const int8_t *act, int64_t M, int64_
 }
 
 template <int FMT, typename T>
-static void launch_qrec(const T *x, int64_t M, int64_t K, int64_t ldx, int8_t *q, int64_t ldq,
-                        double *scale, int C, uint8_t *rec, int32_t *flag, cudaStream_t s) {
-  if (K <= 8192)
-    quantize_records_kernel<FMT, T, 512><<<(unsigned)M, 512, 0, s>>>(x, K, ldx, q, ldq, scale, C,
-                                                                     rec, flag);
-  else
-    quantize_records_kernel<FMT, T, 1024><<<(unsigned)M, 1024, 0, s>>>(x, K, ldx, q, ldq, scale,
-                                                                       C, rec, flag);
+static cudaError_t launch_qrec(const T *x, int64_t M, int64_t K, int64_t ldx, int8_t *q,
+                               int64_t ldq, double *scale, int C, uint8_t *rec, int32_t *flag,
+                               cudaStream_t s) {
+  // one 8-CTA cluster per token (portable cluster size), PDL-launched
+  const int ncta = std::max(1, std::min(8, C));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ncta, (unsigned)M);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ncta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, quantize_records_kernel<FMT, T, 256>, x, K, ldx, q, ldq, scale,
+                            C, rec, flag);
 }
 
 template <typename T>
@@ -610,11 +678,11 @@ static int qrec_impl(int fmt, const T *x, int64_t M, int64_t K, int64_t ldx, int
     return TB_ERR_ARGUMENT;
   const int C = (int)ceil_div(ref_row_bytes(fmt, K), kChunkBytes);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (fmt == TB_I2S) launch_qrec<TB_I2S>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
-  else if (fmt == TB_TL1) launch_qrec<TB_TL1>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
-  else launch_qrec<TB_TL2>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
-  TB_CHECK_LAUNCH();
-  return TB_OK;
+  cudaError_t e;
+  if (fmt == TB_I2S) e = launch_qrec<TB_I2S>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
+  else if (fmt == TB_TL1) e = launch_qrec<TB_TL1>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
+  else e = launch_qrec<TB_TL2>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
+  return e == cudaSuccess ? TB_OK : TB_ERR_CUDA;
 }
 
 extern "C" int tb_quantize_records_f32(int fmt, const float *x, int64_t M, int64_t K, int64_t ldx,
@@ -672,7 +740,8 @@ extern "C" int tb_gemv_batch_prepare(int fmt, int64_t njobs, const tb_gemv_desc 
 }
 
 extern "C" int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t njobs,
-                                    int64_t total_chunks, int32_t max_m, void *stream) {
+                                    int64_t total_chunks, int32_t max_m, int32_t finalize,
+                                    void *stream) {
   if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !table_device || total_chunks < 1 ||
       total_chunks >= ((int64_t)1 << 31) || max_m < 1 || max_m > 16)
     return TB_ERR_ARGUMENT;
@@ -680,7 +749,58 @@ extern "C" int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t n
   b.table = static_cast<const GemvJob *>(table_device);
   b.njobs = (int)njobs;
   b.total = (int)total_chunks;
+  b.defer_finalize = finalize ? 0 : 1;
   return launch_batch(fmt, b, max_m, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int tb_step_glue(const void *fin_table_device, int64_t fin_njobs, int64_t nq,
+                            const tb_quant_desc *q, void *stream) {
+  if (nq < 0 || nq > kMaxGlueVecs || (nq > 0 && !q) || fin_njobs < 0 ||
+      (fin_njobs > 0 && !fin_table_device))
+    return TB_ERR_ARGUMENT;
+  GlueParams g{};
+  g.fin.table = static_cast<const GemvJob *>(fin_table_device);
+  g.fin.njobs = (int)fin_njobs;
+  g.nq = (int)nq;
+  int tokens = 0;
+  for (int64_t v = 0; v < nq; ++v) {
+    const tb_quant_desc &d = q[v];
+    if (!d.x || !d.scale || !d.rec || d.M < 1 || d.K < 1 || d.ldx < d.K ||
+        (d.q && d.ldq < d.K) || d.fmt < TB_I2S || d.fmt > TB_TL2 ||
+        (reinterpret_cast<uintptr_t>(d.rec) & 15))
+      return TB_ERR_ARGUMENT;
+    QuantVec &Q = g.q[v];
+    Q.x = d.x;
+    Q.qnat = d.q;
+    Q.scale = d.scale;
+    Q.rec = d.rec;
+    Q.flag = d.nonfinite_flag;
+    Q.K = d.K;
+    Q.ldx = d.ldx;
+    Q.ldq = d.ldq;
+    Q.M = (int)d.M;
+    Q.C = (int)ceil_div(ref_row_bytes(d.fmt, d.K), kChunkBytes);
+    Q.fmt = d.fmt;
+    Q.is_f64 = d.x_is_f64 ? 1 : 0;
+    tokens += Q.M;
+  }
+  g.q_tokens = tokens;
+  const int rows = tokens + (int)fin_njobs;
+  if (rows == 0) return TB_OK;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(8, rows);
+  cfg.blockDim = dim3(256);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 8;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, glue_kernel, g) == cudaSuccess ? TB_OK : TB_ERR_CUDA;
 }
 
 extern "C" int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign, int64_t rows,

@@ -94,23 +94,30 @@ __global__ void act_prep_kernel(const int8_t *__restrict__ act, int M, int64_t l
 // quantize_activations (core.py:116-134) fused with record construction:
 // one CTA per token, float64 absmax / divide / round-half-away, optional
 // natural int8 output (the reference's QuantizedActivations.data).
+// One thread-block CLUSTER per token (`ncta` CTAs of one cluster, this one
+// being `rank`): each CTA owns a contiguous chunk range, the per-token absmax
+// is combined through distributed shared memory, so a 14336-wide token is
+// quantised by 8 SMs instead of one.  Called by every thread of the CTA.
 template <int FMT, typename T, int kThreads>
-__global__ void __launch_bounds__(kThreads) quantize_records_kernel(
+__device__ __forceinline__ void quantize_token(
     const T *__restrict__ x, int64_t K, int64_t ldx, int8_t *__restrict__ qnat, int64_t ldq,
-    double *__restrict__ scale, int C, uint8_t *__restrict__ rec, int32_t *nonfinite) {
+    double *__restrict__ scale, int C, uint8_t *__restrict__ rec, int32_t *nonfinite, int m,
+    int rank, int ncta) {
   using F = Fmt<FMT>;
-  const int m = blockIdx.x;
+  const int cb = (int)((int64_t)C * rank / ncta), ce = (int)((int64_t)C * (rank + 1) / ncta);
   const T *row = x + m * ldx;
   const int lane = threadIdx.x & 31;
+  const int64_t kb = (int64_t)cb * F::kWeights;
+  const int64_t ke = min((int64_t)ce * F::kWeights, K);
   double amax = 0.0;
   bool bad = false;
-  for (int64_t k = threadIdx.x; k < K; k += kThreads) {
+  for (int64_t k = kb + threadIdx.x; k < ke; k += kThreads) {
     const double v = static_cast<double>(row[k]);
     bad |= !isfinite(v);
     amax = fmax(amax, fabs(v));
   }
   __shared__ double red[kThreads / 32];
-  __shared__ double s_scale;
+  __shared__ double s_part;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   if (lane == 0) red[threadIdx.x >> 5] = amax;
@@ -119,17 +126,31 @@ __global__ void __launch_bounds__(kThreads) quantize_records_kernel(
   if (threadIdx.x == 0) {
     double a = 0.0;
     for (int i = 0; i < kThreads / 32; ++i) a = fmax(a, red[i]);
-    const double s = a > 0.0 ? a / 127.0 : 1.0;
-    s_scale = s;
-    scale[m] = s;
+    s_part = a;
   }
-  __syncthreads();
-  const double s = s_scale;
-  const int64_t n4 = (int64_t)C * 4;
+  // cluster-wide max: every CTA reads every CTA's partial through DSMEM
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  double a = 0.0;
+  {
+    const uint32_t local = smem_u32(&s_part);
+    for (int r = 0; r < ncta; ++r) {
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+      double v;
+      asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote));
+      a = fmax(a, v);
+    }
+  }
+  // keep every CTA's shared memory alive until all remote reads are done
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  const double s = a > 0.0 ? a / 127.0 : 1.0;
+  const double inv_s = 1.0 / s;
+  if (rank == 0 && threadIdx.x == 0) scale[m] = s;
+  const int64_t n4 = (int64_t)(ce - cb) * 4;
   for (int64_t base = threadIdx.x - lane; base < n4; base += kThreads) {
     const int64_t idx = base + lane;
     const bool on = idx < n4;
-    const int c = (int)(idx >> 2), i = (int)(idx & 3);
+    const int c = cb + (int)(idx >> 2), i = (int)(idx & 3);
     const int64_t k0 = (int64_t)c * F::kWeights + i * 4 * F::kGroup;
     uint32_t r[F::kGroup];
     int32_t gs = 0;
@@ -140,11 +161,7 @@ __global__ void __launch_bounds__(kThreads) quantize_records_kernel(
       for (int b = 0; b < 4; ++b) {
         const int64_t k = k0 + 4 * v + b;
         int q = 0;
-        if (on && k < K) {
-          double y = rha(static_cast<double>(row[k]) / s);
-          y = fmin(fmax(y, -127.0), 127.0);
-          q = static_cast<int>(y);
-        }
+        if (on && k < K) q = quantize_one(static_cast<double>(row[k]), s, inv_s);
         if (on && qnat && k < ldq) qnat[m * ldq + k] = static_cast<int8_t>(q);
         gs += q;
         word |= (uint32_t)(q & 0xFF) << (8 * b);
@@ -154,9 +171,19 @@ __global__ void __launch_bounds__(kThreads) quantize_records_kernel(
     write_group<FMT>(rec + ((int64_t)m * C + (on ? c : 0)) * F::kRecBytes, i, r, gs, on);
   }
   // natural padding beyond the record coverage (only when ldq > C * kWeights)
-  if (qnat)
+  if (qnat && rank == ncta - 1)
     for (int64_t k = (int64_t)C * F::kWeights + threadIdx.x; k < ldq; k += kThreads)
       qnat[m * ldq + k] = 0;
+}
+
+// Stand-alone launch form: grid (ncta, M), cluster (ncta, 1, 1).
+template <int FMT, typename T, int kThreads>
+__global__ void __launch_bounds__(kThreads) quantize_records_kernel(
+    const T *__restrict__ x, int64_t K, int64_t ldx, int8_t *__restrict__ qnat, int64_t ldq,
+    double *__restrict__ scale, int C, uint8_t *__restrict__ rec, int32_t *nonfinite) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // x may come from the previous kernel
+  quantize_token<FMT, T, kThreads>(x, K, ldx, qnat, ldq, scale, C, rec, nonfinite, blockIdx.y,
+                                   blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -41,15 +41,9 @@ __global__ void __launch_bounds__(kThreads) quantize_kernel(const T *__restrict_
   }
   __syncthreads();
   const double s = s_scale;
-  for (int64_t k = threadIdx.x; k < ldq; k += kThreads) {
-    int8_t out = 0;
-    if (k < K) {
-      double v = rha(static_cast<double>(row[k]) / s);
-      v = fmin(fmax(v, -127.0), 127.0);
-      out = static_cast<int8_t>(static_cast<int>(v));
-    }
-    qrow[k] = out;
-  }
+  const double inv_s = 1.0 / s;
+  for (int64_t k = threadIdx.x; k < ldq; k += kThreads)
+    qrow[k] = k < K ? static_cast<int8_t>(quantize_one(static_cast<double>(row[k]), s, inv_s)) : 0;
 }
 
 // ----------------------------------------------------------------------------

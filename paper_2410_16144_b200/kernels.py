@@ -30,8 +30,8 @@ from .lut import LutTL1, LutTL2, build_lut_tl1, build_lut_tl2  # noqa: F401
 from .packing import PackedI2S, PackedTL1, PackedTL2
 
 __all__ = ["KernelKind", "WIDEN_GROUPS", "gemv_ref_int32", "gemv_f32_ref", "gemv_i2s",
-           "gemv_tl1", "gemv_tl2", "gemv_parallel", "GemvPlan", "GemvBatch", "ActRecords",
-           "KERNEL_PAD"]
+           "gemv_tl1", "gemv_tl2", "gemv_parallel", "GemvPlan", "GemvBatch", "StepGlue",
+           "ActRecords", "KERNEL_PAD"]
 
 WIDEN_GROUPS = 64  # kernels.py:34
 MAX_DECODE_TOKENS = 16
@@ -288,13 +288,53 @@ class GemvBatch:
         self.pairs = pairs  # keep every buffer alive
         self._lib = lib
 
-    def run(self, stream_ptr: int | None = None):
+    def run(self, stream_ptr: int | None = None, finalize: bool = True):
+        """One grouped GEMV launch (+ the finalize pass unless ``finalize`` is
+        False, in which case a later StepGlue must finalise this batch)."""
         st = self._lib.tb_gemv_batch_launch(self.fmt, self.table.data_ptr(), self.njobs,
-                                            self.total, self.max_m,
+                                            self.total, self.max_m, 1 if finalize else 0,
                                             stream_ptr if stream_ptr is not None
                                             else L.stream_ptr())
         if st:
             L.check(st, "gemv_batch_launch")
+
+
+class StepGlue:
+    """ONE launch between GEMV groups: finalise a batch and quantise inputs.
+
+    ``inputs`` is a list of (x_device_tensor [M, K] f32/f64, ActRecords);
+    the x tensors are read at ``run`` time through their data pointers, so
+    they must stay allocated (e.g. a fixed buffer refilled every step).
+    """
+
+    def __init__(self, inputs, finalize: "GemvBatch | None" = None):
+        import ctypes as C
+
+        self._lib = L.load()
+        self.inputs = inputs
+        self.fin = finalize
+        self.descs = (L.QuantDesc * max(1, len(inputs)))()
+        for d, (x, rec) in zip(self.descs, inputs):
+            d.x = x.data_ptr()
+            d.x_is_f64 = 1 if x.dtype == torch.float64 else 0
+            d.fmt, d.M, d.K, d.ldx = rec.fmt, rec.M, rec.K, x.stride(0)
+            d.q = L.ptr(rec.natural)
+            d.ldq = rec.natural.stride(0) if rec.natural is not None else 0
+            d.scale, d.rec, d.nonfinite_flag = rec.scales.data_ptr(), rec.buf.data_ptr(), None
+        self._descs_ptr = C.cast(self.descs, C.c_void_p)
+
+    def retarget(self, finalize: "GemvBatch | None"):
+        self.fin = finalize
+        return self
+
+    def run(self, stream_ptr: int | None = None):
+        fin = self.fin
+        st = self._lib.tb_step_glue(fin.table.data_ptr() if fin is not None else None,
+                                    fin.njobs if fin is not None else 0, len(self.inputs),
+                                    self._descs_ptr,
+                                    stream_ptr if stream_ptr is not None else L.stream_ptr())
+        if st:
+            L.check(st, "step_glue")
 
 
 class ActRecords:

@@ -64,6 +64,22 @@ def test_quantize_batch_and_errors(tb):
         tb.quantize_activations(np.zeros(0))
 
 
+def test_records_quantizer_golden(tb):
+    """The fused quantise->records kernel (the GEMV's hot input path) produces
+    the reference's int8 codes and scales, and the same records as building
+    them from the natural codes."""
+    xs = split(SMALL["q_x"], SMALL["q_xoff"])
+    want = split(SMALL["q_data_p4"], SMALL["q_doff_p4"])
+    for fmt in (1, 2, 3):
+        for x, d, s in zip(xs, want, SMALL["q_scale_p4"]):
+            r = tb.ActRecords(fmt, 1, x.size, keep_natural_pad=4)
+            r.quantize(torch.from_numpy(np.ascontiguousarray(x)).cuda().reshape(1, -1))
+            assert np.array_equal(host(r.natural)[0], d)
+            assert host(r.scales)[0] == s
+            r2 = tb.ActRecords(fmt, 1, x.size).prep(r.natural)
+            assert torch.equal(r.buf, r2.buf)
+
+
 def test_ternarize_golden(tb):
     offs = np.cumsum([0] + [r * c for r, c in SMALL["t_shape"]])
     ws, qs = split(SMALL["t_w"], offs), split(SMALL["t_q"], offs)
