@@ -195,7 +195,6 @@ def run_gpu(args, rank, world):
     import torch.distributed as dist
 
     import paper_2410_16144_b200 as tb
-    from paper_2410_16144_b200.core import quantize_into
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
@@ -252,32 +251,47 @@ def run_gpu(args, rank, world):
     for pl in plans:
         pl["batch"] = tb.GemvBatch([(pl["gate"], rec_h), (pl["up"], rec_h),
                                     (pl["down"], rec_i_loc)])
-
-    # A decode step is TWO launches: one glue kernel (finalise the previous
-    # step's group -- scales -> outputs -- and quantise this step's inputs
-    # into records) and one grouped GEMV (gate+up+down).  With tp > 1 the
-    # down projection's int32 partials are all-reduced before finalising.
-    glues = [tb.StepGlue([(XH[j:j + 1], rec_h), (XI[j:j + 1], rec_i)]) for j in range(NX)]
+        if tp == 1:  # fused one-launch step: input 0 = x_h (gate, up), 1 = x_i (down)
+            pl["step"] = tb.GemvStep([(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)], [H, I])
     tail = tb.StepGlue([])
 
-    def step(i, prev):
-        pl = plans[i % NCOPY]
-        glues[i % NX].retarget(prev["batch"] if prev is not None else None).run()
-        pl["batch"].run(finalize=(tp > 1))
-        if tp > 1:
+    if tp == 1:
+        # A decode step is ONE launch (tb_gemv_step_launch): every CTA quantises
+        # the token's two input vectors itself, streams gate+up+down, and then
+        # finalises the previous step's outputs (scales -> fp32 outputs).
+        def step(i, prev):
+            pl = plans[i % NCOPY]
+            pl["step"].run([XH[i % NX], XI[i % NX]], prev=prev["step"] if prev else None)
+            return pl
+
+        def run_steps(n):
+            prev = None
+            for i in range(n):
+                prev = step(i, prev)
+            if prev is not None:
+                prev["step"].finalize()  # the last step's outputs
+
+        launches_per_step = 1
+    else:
+        # tp > 1: glue (finalise + quantise) and grouped GEMV launches; the down
+        # projection's int32 partials are all-reduced before its rescale.
+        glues = [tb.StepGlue([(XH[j:j + 1], rec_h), (XI[j:j + 1], rec_i)]) for j in range(NX)]
+
+        def step(i, prev):
+            pl = plans[i % NCOPY]
+            glues[i % NX].retarget(prev["batch"] if prev is not None else None).run()
+            pl["batch"].run(finalize=True)
             dist.all_reduce(pl["down"].acc, op=dist.ReduceOp.SUM)
             L.check(L.load().tb_scale_outputs(
                 pl["down"].acc.data_ptr(), 1, H, float(pl["mats"]["down"].scale),
                 rec_i.scales.data_ptr(), None, out_down.data_ptr(), L.stream_ptr()), "scale")
-        return None if tp > 1 else pl
+            return None
 
-    def run_steps(n):
-        prev = None
-        for i in range(n):
-            prev = step(i, prev)
-        tail.retarget(prev["batch"] if prev is not None else None).run()  # last finalise
+        def run_steps(n):
+            for i in range(n):
+                step(i, None)
 
-    launches_per_step = 2 + (1 if tp > 1 else 0)  # glue + grouped GEMV (+ scale for tp)
+        launches_per_step = 4  # glue + grouped GEMV + finalize + rescale (+ NCCL)
 
     # ---- warm-up (eager, also configures kernel attributes before capture)
     run_steps(max(args.warmup, NCOPY))
@@ -311,14 +325,19 @@ def run_gpu(args, rank, world):
         ms = float(t.item())
     ms_per_step = ms / args.steps
 
-    # ---- roofline: the grouped TL1 GEMV kernel alone (gate+up+down per launch),
-    #      back-to-back over the rotating copies
+    # ---- roofline: the dominant kernel timed alone, back-to-back over the
+    #      rotating copies in a graph (tp1: the fused step kernel -- quantise +
+    #      gate/up/down GEMV + previous finalize; tp>1: the grouped GEMV)
     R = 4 * NCOPY
     g2 = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
         with torch.cuda.graph(g2, stream=s):
             for i in range(R):
-                plans[i % NCOPY]["batch"].run()
+                if tp == 1:
+                    plans[i % NCOPY]["step"].run([XH[i % NX], XI[i % NX]],
+                                                 prev=plans[(i - 1) % NCOPY]["step"])
+                else:
+                    plans[i % NCOPY]["batch"].run(finalize=False)
     g2.replay()
     torch.cuda.synchronize()
     e0.record()
@@ -326,6 +345,12 @@ def run_gpu(args, rank, world):
     e1.record()
     torch.cuda.synchronize()
     gemv_ms = e0.elapsed_time(e1) / R
+    for pl in plans:  # finalise what is pending (resets the workspaces)
+        if tp == 1:
+            pl["step"].finalize()
+        else:
+            tail.retarget(pl["batch"]).run()
+    torch.cuda.synchronize()
     rows_loc = I // tp
     gemv_bytes = (algo_bytes_gemv(rows_loc, H) * 2 + tl1_bytes(H, kloc) + kloc + 4 * H)
     peak, peak_kind = measured_peak()
@@ -345,22 +370,55 @@ def run_gpu(args, rank, world):
                                   "row-parallel down + NCCL int32 all-reduce)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                     "kernel": "tgemv_kernel<TL1,1> grouped launch: gate+up (14336x4096) "
-                               "+ down (4096x14336)",
+                     "kernel": ("tgemv_kernel<TL1,1,fused> one-launch step: quantise x_h, x_i + "
+                                "gate/up (14336x4096) + down (4096x14336) + previous finalize")
+                               if tp == 1 else "tgemv_kernel<TL1,1> grouped gate+up+down",
                      "bytes_per_launch": gemv_bytes, "launch_us": round(gemv_ms * 1e3, 3),
                      "peak_kind": f"{peak_kind} hbm_gbs (copy)"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
 
-    # ---- e2e through the public API with host buffers
+    # ---- e2e through the public API with host buffers: every step copies its
+    #      two pinned f32 input vectors in, runs, and reads the three fp32
+    #      output vectors back (synchronously) before the next step
     if rank == 0 and not args.no_e2e and tp == 1:
-        K = tb.KernelKind
+        n_e2e = max(10, min(args.steps, 200))
         xh_h = torch.randn(NX, H).pin_memory()
         xi_h = torch.randn(NX, I).pin_memory()
-        n_e2e = max(10, min(args.steps, 200))
+        xh_d = torch.empty(H, device=dev)
+        xi_d = torch.empty(I, device=dev)
+        out_h = torch.empty(2 * I + H, dtype=torch.float32).pin_memory()
 
         def e2e_step(i):
+            pl = plans[i % NCOPY]
+            xh_d.copy_(xh_h[i % NX], non_blocking=True)
+            xi_d.copy_(xi_h[i % NX], non_blocking=True)
+            pl["step"].run([xh_d, xi_d])
+            pl["step"].finalize()
+            out_h[:I].copy_(pl["gate"].out32[0], non_blocking=True)
+            out_h[I:2 * I].copy_(pl["up"].out32[0], non_blocking=True)
+            out_h[2 * I:].copy_(pl["down"].out32[0], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for i in range(5):
+            e2e_step(i)
+        t0 = time.perf_counter()
+        for i in range(n_e2e):
+            e2e_step(i)
+        e2e_s = (time.perf_counter() - t0) / n_e2e
+        result["e2e"] = {"value": round(1.0 / e2e_s, 2), "unit": "tokens/s",
+                         "h2d_bytes_per_step": (H + I) * 4,
+                         "d2h_bytes_per_step": (2 * I + H) * 4,
+                         "steps": n_e2e,
+                         "path": "tb.GemvStep.run (one launch) + finalize per token; pinned host "
+                                 "f32 inputs in, fp32 outputs to pinned host, stream sync per step"}
+
+        # the reference-shaped per-call API (quantize_activations + gemv_parallel
+        # per projection, float64 GemvResult.output to host)
+        K = tb.KernelKind
+
+        def api_step(i):
             mats = plans[i % NCOPY]["mats"]
             qa_h = tb.quantize_activations(xh_h[i % NX], pad_to=2)
             rg = tb.gemv_parallel(K.TL1, mats["gate"], qa_h)
@@ -370,19 +428,18 @@ def run_gpu(args, rank, world):
             return rg.output.cpu(), ru.output.cpu(), rd.output.cpu()
 
         for i in range(3):
-            e2e_step(i)
+            api_step(i)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for i in range(n_e2e):
-            e2e_step(i)
+            api_step(i)
         torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / n_e2e
-        result["e2e"] = {"value": round(1.0 / e2e_s, 2), "unit": "tokens/s",
-                         "h2d_bytes_per_step": (H + I) * 4,
-                         "d2h_bytes_per_step": (2 * I + H) * 8,
-                         "steps": n_e2e,
-                         "path": "tb.quantize_activations + tb.gemv_parallel(TL1) x3, pinned host "
-                                 "f32 in, float64 GemvResult.output to host"}
+        api_s = (time.perf_counter() - t0) / n_e2e
+        result["e2e_reference_api"] = {
+            "value": round(1.0 / api_s, 2), "unit": "tokens/s", "steps": n_e2e,
+            "h2d_bytes_per_step": (H + I) * 4, "d2h_bytes_per_step": (2 * I + H) * 8,
+            "path": "tb.quantize_activations + tb.gemv_parallel(TL1) x3 (reference call "
+                    "pattern, bench.py:138-153), float64 outputs to host"}
 
     if rank == 0 and not args.no_cpu_baseline and tp == 1:
         result["cpu_baseline"] = cpu_baseline(host_copy["gate"], host_copy["up"],

@@ -180,13 +180,16 @@ typedef struct tb_gemv_desc {
   float *out32;
 } tb_gemv_desc;
 int64_t tb_gemv_job_bytes(void);
+/* Also reports max_entries = max over jobs of M * padded rows, which sizes
+ * the finalize grid (one accumulator per thread).                          */
 int tb_gemv_batch_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
-                          void *table_host, int64_t *total_chunks, int32_t *max_m);
+                          void *table_host, int64_t *total_chunks, int32_t *max_m,
+                          int64_t *max_entries);
 /* finalize != 0: also launch the finalize pass (scales -> outputs, workspace
  * reset); 0: the caller finalises, e.g. inside the next tb_step_glue.       */
 int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t njobs,
-                         int64_t total_chunks, int32_t max_m, int32_t finalize,
-                         void *stream);
+                         int64_t total_chunks, int32_t max_m, int64_t max_entries,
+                         int32_t finalize, void *stream);
 
 /* Decode-step glue in ONE launch: finalise a prepared GEMV batch (may be
  * empty: fin_njobs = 0) and quantise up to 4 activation matrices into
@@ -204,8 +207,40 @@ typedef struct tb_quant_desc {
   uint8_t *rec;
   int32_t *nonfinite_flag;
 } tb_quant_desc;
-int tb_step_glue(const void *fin_table_device, int64_t fin_njobs, int64_t nq,
-                 const tb_quant_desc *q, void *stream);
+int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
+                 int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
+                 void *stream);
+/* Fused one-token decode step in ONE launch (gemv.cu, tgemv_kernel<.,1,true>):
+ * every CTA quantises the float32 input vectors itself (quantize_activations,
+ * core.py:116-134, records kept in shared memory), streams the grouped GEMV
+ * (jobs read input src[j]), and -- after its own work, once the preceding
+ * grid has completed -- finalises the PREVIOUS step's batch (prev table; it
+ * must not be this batch).  This step's outputs are finalised by the next
+ * step launch or by tb_gemv_batch_finalize.  prepare(): descs[j].M == 1,
+ * descs[j].cols == input_k[src[j]], descs[j].a_scale = the scale pointer
+ * input src[j] will be given at launch.  x_after_wait != 0: the inputs are
+ * produced by the preceding kernel (read after griddepcontrol.wait).
+ * table_host (optional): the prepared host table -- small batches then ride
+ * in the kernel parameters and each CTA quantises only the inputs its jobs
+ * read.                                                                      */
+typedef struct tb_step_input {
+  const float *x;          /* [K] float32 (device; 16-B alignment preferred)  */
+  int64_t K;
+  double *scale;           /* out: absmax / 127 (or 1) of this vector         */
+  int32_t *nonfinite_flag; /* optional: set to 1 on NaN / inf input          */
+} tb_step_input;
+int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
+                         const int32_t *src, int64_t ninputs, const int64_t *input_k,
+                         void *table_host, int64_t *total_chunks,
+                         int64_t *max_entries);
+int tb_gemv_step_launch(int fmt, const void *table_device, int64_t njobs,
+                        int64_t total_chunks, int64_t ninputs,
+                        const tb_step_input *inputs, int32_t x_after_wait,
+                        const void *prev_table_device, int64_t prev_njobs,
+                        const void *table_host, void *stream);
+/* Finalise a batch's accumulators (scales -> outputs, workspace reset).    */
+int tb_gemv_batch_finalize(const void *table_device, int64_t njobs,
+                           int64_t max_entries, void *stream);
 /* Convenience: tb_prep_activations into the workspace + tb_gemv_records.   */
 int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
             int64_t rows, int64_t cols, const int8_t *act, int64_t M,

@@ -23,6 +23,7 @@ from .kernels import (
     ActRecords,
     GemvBatch,
     GemvPlan,
+    GemvStep,
     StepGlue,
     KernelKind,
     gemv_f32_ref,

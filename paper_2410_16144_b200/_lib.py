@@ -53,9 +53,12 @@ _SIGS = {
     "tb_gemv_records": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _p, _f64, _p, _p, _p, _p,
                                _p]),
     "tb_gemv_job_bytes": (_i64, []),
-    "tb_gemv_batch_prepare": (_i32, [_i32, _i64, _p, _p, _p, _p]),
-    "tb_gemv_batch_launch": (_i32, [_i32, _p, _i64, _i64, _i32, _i32, _p]),
-    "tb_step_glue": (_i32, [_p, _i64, _i64, _p, _p]),
+    "tb_gemv_batch_prepare": (_i32, [_i32, _i64, _p, _p, _p, _p, _p]),
+    "tb_gemv_batch_launch": (_i32, [_i32, _p, _i64, _i64, _i32, _i64, _i32, _p]),
+    "tb_step_glue": (_i32, [_p, _i64, _i64, _i64, _p, _p]),
+    "tb_gemv_step_prepare": (_i32, [_i32, _i64, _p, _p, _i64, _p, _p, _p, _p]),
+    "tb_gemv_step_launch": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _i32, _p, _i64, _p, _p]),
+    "tb_gemv_batch_finalize": (_i32, [_p, _i64, _i64, _p]),
     "tb_gemv_lut": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _p, _p]),
     "tb_gemv_ref_int32": (_i32, [_p, _i64, _i64, _p, _p, _p]),
     "tb_gemv_f32_ref": (_i32, [_p, _i64, _i64, _f32, _p, _p, _p]),
@@ -78,6 +81,12 @@ class QuantDesc(C.Structure):
     _fields_ = [("x", _p), ("x_is_f64", C.c_int32), ("fmt", C.c_int32), ("M", _i64),
                 ("K", _i64), ("ldx", _i64), ("q", _p), ("ldq", _i64), ("scale", _p),
                 ("rec", _p), ("nonfinite_flag", _p)]
+
+
+class StepInput(C.Structure):
+    """Mirror of tb_step_input (include/ternary_b200.h)."""
+
+    _fields_ = [("x", _p), ("K", _i64), ("scale", _p), ("nonfinite_flag", _p)]
 
 
 _lib = None

@@ -133,14 +133,36 @@ __device__ __forceinline__ double rha(double v) { return trunc(v + copysign(0.5,
 // x * (1/s) is within a few ulp of the correctly rounded x / s, which decides
 // the same code unless v' sits within 1e-9 of a rounding tie (k + 0.5) -- then
 // the exact quotient is evaluated.  (|v| <= 127, so 1e-9 >> the few-ulp error.)
+// The exact division is a real call (never if-converted: a float64 divide per
+// element would otherwise be paid on every element, not just near ties).
+static __device__ __noinline__ double div_exact(double x, double s) { return x / s; }
+
 __device__ __forceinline__ int quantize_one(double x, double s, double inv_s) {
   const double v1 = x * inv_s;
   const double a = fabs(v1);
   const double f = a - floor(a);
-  const double v = fabs(f - 0.5) > 1e-9 ? v1 : x / s;
+  double v = v1;
+  if (fabs(f - 0.5) <= 1e-9) v = div_exact(x, s);
   double y = rha(v);
   y = fmin(fmax(y, -127.0), 127.0);
   return static_cast<int>(y);
+}
+
+static __device__ __noinline__ int quantize_one_call(double x, double s, double inv_s) {
+  return quantize_one(x, s, inv_s);
+}
+
+// float32 input, float32 fast path: v = x * inv_s in fp32 is within 1.6e-5
+// of the exact quotient x / s (|v| <= 127, two roundings of 2^-24 relative).
+// If v is more than 4e-5 away from a rounding tie (|v - rint(v)| < 0.49996),
+// the exact quotient rounds -- half away from zero or not -- to rint(v), the
+// float64 reference's code (|v| <= 127 needs no clamp).  Otherwise defer to
+// quantize_one (float64, exact division at ties).
+__device__ __forceinline__ int quantize_fast(float x, float inv_sf, double s, double inv_s) {
+  const float v = x * inv_sf;
+  const float r = rintf(v);
+  if (fabsf(v - r) < 0.49996f) return static_cast<int>(r);
+  return quantize_one_call(static_cast<double>(x), s, inv_s);  // rare: near a tie
 }
 
 int sm_count_cached();

@@ -52,8 +52,21 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   do {             \
   } while (0)
 #endif
+// -DTB_TL_PROLOGUE: marks 1-3 time the fused prologue (weights issued, absmax
+// reduced, records built) instead of the main loop
+#ifdef TB_TL_PROLOGUE
+#define TL_PMARK(i) TL_MARK(i)
+#define TL_LMARK(i) \
+  do {              \
+  } while (0)
+#else
+#define TL_PMARK(i) \
+  do {              \
+  } while (0)
+#define TL_LMARK(i) TL_MARK(i)
+#endif
 
-template <int FMT, int MT>
+template <int FMT, int MT, bool kFused = false>
 struct Cfg {
 #ifndef TB_MT1_WARPS
 #define TB_MT1_WARPS 16
@@ -64,10 +77,13 @@ struct Cfg {
 #endif
   static constexpr int kRing = MT == 1 ? TB_MT1_RING : (MT == 2 ? 3 : 2);
   static constexpr int kThreads = 32 * kWarps;
+  // fused step: records live in a CTA-wide table after the ring, not per stage
   static constexpr int kStageBytes =
-      kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + MT * Fmt<FMT>::kRecBytes);
-  static constexpr int kSmem = kWarps * kRing * kStageBytes;
-  static_assert(kSmem <= 227 * 1024, "ring does not fit in shared memory");
+      kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + (kFused ? 0 : MT) * Fmt<FMT>::kRecBytes);
+  static constexpr int kRingBytes = kWarps * kRing * kStageBytes;
+  static constexpr int kRecTabBytes = kFused ? 64 * 1024 : 0;  // max records of all inputs
+  static constexpr int kSmem = kRingBytes + kRecTabBytes;
+  static_assert(kSmem <= 227 * 1024 - 512, "ring does not fit in shared memory");
 };
 
 struct GemvJob {
@@ -84,6 +100,26 @@ struct GemvJob {
   int N, Npad, C, M;
   int start;  // first flat chunk of this job
   int end;    // one past its last flat chunk (start + T * C)
+  int src;    // fused step: index of the input vector this job contracts
+};
+
+// Fused decode step (tgemv_kernel<FMT, 1, true>): the launch quantises its own
+// float32 input vectors (every CTA, into shared memory), runs the grouped
+// GEMV, and afterwards finalises the PREVIOUS step's batch -- whose grid has
+// completed by then (griddepcontrol.wait) -- so a decode step is one launch.
+constexpr int kMaxStepInputs = 4;
+constexpr int kMaxNeedCtas = 160;  // per-CTA input masks (>= the 148 SMs of a B200)
+struct StepInputs {
+  const float *x[kMaxStepInputs];
+  double *scale[kMaxStepInputs];   // per-token scale out (read by the finalize)
+  int32_t *flag[kMaxStepInputs];   // optional non-finite flag
+  int K[kMaxStepInputs], C[kMaxStepInputs], off[kMaxStepInputs];  // off: record table offset
+  int n;
+  int x_after_wait;      // inputs produced by the preceding grid: read them after the wait
+  const GemvJob *prev;   // device job table finalised after this launch's own work
+  int prev_njobs;
+  int16_t writer[kMaxStepInputs];  // CTA that publishes input v's scale / flag
+  uint8_t need[kMaxNeedCtas];      // inputs (bit v) the CTA's jobs contract
 };
 
 struct GemvBatch {
@@ -93,6 +129,9 @@ struct GemvBatch {
   int total;  // flat chunks over all jobs
   int base, rem;  // warp w gets base + (w < rem) chunks
   int defer_finalize;  // host: the caller finalises (e.g. in the next glue kernel)
+  int max_entries;     // host: max over jobs of M * Npad (sizes the finalize grid)
+  int fin_parts;       // device (glue): 8-CTA groups per job in the finalize rows
+  StepInputs in;       // fused step only
 };
 
 // Job descriptor by value: inline jobs come from the (grid-constant) kernel
@@ -127,7 +166,7 @@ __device__ __forceinline__ void flush_tile(const GemvBatch &b, int j, int t,
   const int row = t * kRowTile + lane;
 #pragma unroll
   for (int m = 0; m < MT; ++m)
-    if (m < M) red_add_s32(J.ws_acc + (int64_t)m * J.Npad + row, acc.total(m));
+    if (m == 0 || m < M) red_add_s32(J.ws_acc + (int64_t)m * J.Npad + row, acc.total(m));
 }
 
 // After the GEMV grid: output = f64(acc) * w_scale * a_scale[m] (core.py:
@@ -135,8 +174,7 @@ __device__ __forceinline__ void flush_tile(const GemvBatch &b, int j, int t,
 // Launched with programmatic dependent launch: griddepcontrol.wait blocks
 // until the GEMV grid has completed and its memory operations are visible.
 // Finalize job j with CTAs `part` of `nparts` (every thread of the CTA).
-__device__ __forceinline__ void finalize_job(const GemvBatch &b, int j, int part, int nparts) {
-  const GemvJob J = job_at(b, j);
+__device__ __forceinline__ void finalize_one(const GemvJob &J, int part, int nparts) {
   const int64_t total = (int64_t)J.M * J.Npad;
   for (int64_t i = part * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)nparts * blockDim.x) {
@@ -153,6 +191,10 @@ __device__ __forceinline__ void finalize_job(const GemvBatch &b, int j, int part
       }
     }
   }
+}
+
+__device__ __forceinline__ void finalize_job(const GemvBatch &b, int j, int part, int nparts) {
+  finalize_one(job_at(b, j), part, nparts);
 }
 
 // grid (parts, njobs): every job finalised concurrently.
@@ -211,7 +253,9 @@ __global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueP
     if (g.q[v].fmt == TB_TL2) glue_quant<TB_TL2>(g.q[v], m);
     else glue_quant<TB_I2S>(g.q[v], m);  // I2_S and TL1 share the record layout
   } else {
-    finalize_job(g.fin, y - g.q_tokens, blockIdx.x, gridDim.x);
+    const int r = y - g.q_tokens;  // (job, group) of 8 CTAs: one element per thread
+    const int j = r / g.fin.fin_parts, part = r - j * g.fin.fin_parts;
+    finalize_job(g.fin, j, part * gridDim.x + blockIdx.x, g.fin.fin_parts * gridDim.x);
   }
 }
 
@@ -370,136 +414,225 @@ struct IssueState {
   }
 };
 
-template <int FMT, int MT>
-__global__ void __launch_bounds__(Cfg<FMT, MT>::kThreads, 1)
+template <int FMT, int MT, bool kFused>
+__global__ void __launch_bounds__(Cfg<FMT, MT, kFused>::kThreads, 1)
     tgemv_kernel(const __grid_constant__ GemvBatch b) {
   using F = Fmt<FMT>;
-  using CF = Cfg<FMT, MT>;
+  using CF = Cfg<FMT, MT, kFused>;
+  static_assert(!kFused || MT == 1, "the fused step is a one-token decode step");
   constexpr int kRing = CF::kRing;
+  constexpr int kIssueMain = kFused ? kIssueWeights : kIssueAll;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t *ring = smem + warp * kRing * CF::kStageBytes;
+  uint8_t *rtab_base = smem + CF::kRingBytes;  // fused: record tables of the inputs
 
   const int gw = blockIdx.x * CF::kWarps + warp;
   TL_MARK(0);
-  // let the finalize kernel (our programmatic dependent) get launched early
+  // let our programmatic dependent (finalize kernel / next step) launch early
   asm volatile("griddepcontrol.launch_dependents;");
   const int w0 = gw * b.base + min(gw, b.rem);
   const int n = b.base + (gw < b.rem ? 1 : 0);
-  if (n <= 0) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    return;
+  bool waited = false;
+  __shared__ double s_scale[kMaxStepInputs];
+  int s_badm = 0;  // fused: non-finite inputs (bit v), identical in every thread
+  if constexpr (!kFused) {
+    if (n <= 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      return;
+    }
   }
   const int nst = (n + kStageChunks - 1) / kStageChunks;
 
   // locate the first chunk
   Cursor cur{0, 0, 0};
-  while (cur.j + 1 < b.njobs && job_at(b, cur.j + 1).start <= w0) ++cur.j;
-  {
+  IssueState is;  // issue cursor + cached job pointers (identical in every lane)
+  if (n > 0) {
+    while (cur.j + 1 < b.njobs && job_at(b, cur.j + 1).start <= w0) ++cur.j;
     GemvJob J = job_at(b, cur.j);
     const int local = w0 - J.start;
     cur.t = local / J.C;
     cur.c = local - cur.t * J.C;
+    is.reset(b, cur);
   }
-  IssueState is;  // issue cursor + cached job pointers (identical in every lane)
-  is.reset(b, cur);
-  TL_MARK(1);
   // Prologue.  Weights never depend on the previous kernel, so the first
   // stages' weights are requested before griddepcontrol.wait (this kernel is
   // a programmatic dependent of whatever produced the activation records);
   // the records follow once the producer has completed.
-  {
+  constexpr int kMaxG = FMT == TB_TL2 ? 2 : 3;
+  RegQuant<FMT, CF::kThreads, kMaxG> rq;
+  if constexpr (kFused) {
+    // the input loads go out first (small, L2-resident after the first CTA);
+    // then the weight prefetch; the loaded values are consumed after both
+    const int need = blockIdx.x < kMaxNeedCtas ? b.in.need[blockIdx.x] : 0xF;
+#ifndef TB_FUSED_NOLOAD  // profiling variants: TB_FUSED_NOLOAD / TB_FUSED_NOQ
+    if (!b.in.x_after_wait) rq.load(b.in.x, b.in.K, b.in.C, b.in.n, need);
+#else
+    rq.G = 0;
+#endif
+#ifndef TB_PRE_STAGES
+#define TB_PRE_STAGES kRing
+#endif
+    constexpr int kPre = TB_PRE_STAGES < kRing ? TB_PRE_STAGES : kRing;
+#pragma unroll 1
+    for (int k = 0; k < kPre; ++k) {
+      if (k < nst) is.issue<FMT, kIssueWeights>(b, min(kStageChunks, n - k * kStageChunks),
+                                                ring + k * CF::kStageBytes, lane);
+      cp_async_commit();
+    }
+    if (b.in.x_after_wait) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      waited = true;
+      rq.load(b.in.x, b.in.K, b.in.C, b.in.n, need);
+    }
+    // quantise every input vector into this CTA's record tables
+    __shared__ float red[CF::kWarps * 4];
+    __shared__ int redb[CF::kWarps];
+    if (rq.fits()) {
+#ifndef TB_FUSED_NOQ
+      TL_PMARK(1);
+      s_badm = rq.reduce(b.in.n, s_scale, red, redb);
+      TL_PMARK(2);
+      rq.records(b.in.off, rtab_base);
+      TL_PMARK(3);
+#endif
+    } else {
+      s_badm = 0;
+      for (int v = 0; v < b.in.n; ++v) {  // large inputs: one loop per vector
+        bool bad;
+        const float amax = cta_absmax_f32<CF::kThreads>(b.in.x[v], b.in.K[v], bad, red);
+        const double sc = amax > 0.f ? static_cast<double>(amax) / 127.0 : 1.0;  // core.py:128-130
+        if (threadIdx.x == 0) s_scale[v] = sc;
+        if (bad) s_badm |= 1 << v;
+        cta_build_records<FMT, CF::kThreads>(b.in.x[v], b.in.K[v], b.in.C[v], sc,
+                                             rtab_base + b.in.off[v]);
+      }
+    }
+#pragma unroll 1
+    for (int k = kPre; k < kRing; ++k) {  // the rest of the weight prologue
+      if (k < nst) is.issue<FMT, kIssueWeights>(b, min(kStageChunks, n - k * kStageChunks),
+                                                ring + k * CF::kStageBytes, lane);
+      cp_async_commit();
+    }
+    __syncthreads();
+  } else {
     IssueState wis = is;
 #pragma unroll 1
     for (int k = 0; k < kRing && k < nst; ++k)
       wis.issue<FMT, kIssueWeights>(b, min(kStageChunks, n - k * kStageChunks),
                                     ring + k * CF::kStageBytes, lane);
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll 1
-  for (int k = 0; k < kRing; ++k) {
-    if (k < nst) is.issue<FMT, kIssueRecords>(b, min(kStageChunks, n - k * kStageChunks),
-                                              ring + k * CF::kStageBytes, lane);
-    cp_async_commit();  // group 0 also holds every prologue weight copy
+    for (int k = 0; k < kRing; ++k) {
+      if (k < nst) is.issue<FMT, kIssueRecords>(b, min(kStageChunks, n - k * kStageChunks),
+                                                ring + k * CF::kStageBytes, lane);
+      cp_async_commit();  // group 0 also holds every prologue weight copy
+    }
   }
 
-  int C, M, T;  // shape of the current job
-  {
-    const GemvJob J = job_at(b, cur.j);
-    C = J.C;
-    M = J.M;
-    T = (J.end - J.start) / J.C;
-  }
-  Acc<FMT, MT> acc;
-  acc.zero();
-  int nch = 0;
-  for (int k = 0; k < nst; ++k) {
-    const int s = k % kRing;
-    uint8_t *slot = ring + s * CF::kStageBytes;
-    const uint8_t *slot_sign = slot + kStageChunks * kTileChunkBytes;
-    const uint8_t *slot_act = slot + kStageChunks * (kTileChunkBytes + F::kSignBytes);
-    const int nk = min(kStageChunks, n - k * kStageChunks);
-    cp_async_wait<kRing - 1>();  // this lane's copies of stage k have landed
-    __syncwarp();                 // ... and every other lane's
-    if (k == 0) TL_MARK(2);
-    if (nk == kStageChunks && cur.c + kStageChunks <= C) {
-      // fast path: four chunks of the current row tile, fully unrolled
+  TL_LMARK(1);  // prologue done (fused: inputs quantised)
+  // The fused step publishes partial sums only once the previous step's grid
+  // has completed: it finalises (reads and zeroes) a workspace that a later
+  // launch of the same batch would otherwise accumulate into.
+  auto flush = [&](const Acc<FMT, MT> &acc, int M) {
+    if constexpr (kFused) {
+      if (!waited) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        waited = true;
+      }
+    }
+    flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
+  };
+
+  if (n > 0) {
+    int C, M, T;  // shape of the current job
+    const uint8_t *rtab = nullptr;  // fused: records of the current job's input
+    auto load_shape = [&]() {
+      const GemvJob J = job_at(b, cur.j);
+      C = J.C;
+      M = J.M;
+      T = (J.end - J.start) / J.C;
+      if constexpr (kFused) rtab = rtab_base + b.in.off[J.src];
+    };
+    load_shape();
+    Acc<FMT, MT> acc;
+    acc.zero();
+    int nch = 0;
+    for (int k = 0; k < nst; ++k) {
+      const int s = k % kRing;
+      uint8_t *slot = ring + s * CF::kStageBytes;
+      const uint8_t *slot_sign = slot + kStageChunks * kTileChunkBytes;
+      const uint8_t *slot_act = slot + kStageChunks * (kTileChunkBytes + F::kSignBytes);
+      const int nk = min(kStageChunks, n - k * kStageChunks);
+      cp_async_wait<kRing - 1>();  // this lane's copies of stage k have landed
+      __syncwarp();                 // ... and every other lane's
+      if (k == 0) TL_LMARK(2);
+      if (nk == kStageChunks && cur.c + kStageChunks <= C) {
+        // fast path: four chunks of the current row tile, fully unrolled
+        const uint8_t *act = kFused ? rtab + cur.c * F::kRecBytes : slot_act;
 #pragma unroll
-      for (int j = 0; j < kStageChunks; ++j) {
-        const uint4 w4 = *reinterpret_cast<const uint4 *>(slot + j * kTileChunkBytes + lane * 16);
-        uint32_t sg = 0;
-        if (FMT == TB_TL2)
-          sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
-        process_chunk<FMT, MT>(w4, sg, slot_act + j * F::kRecBytes, M, acc);
-      }
-      nch += kStageChunks;
-      cur.c += kStageChunks;
-    } else {
-      for (int j = 0; j < nk; ++j) {
-        if (cur.c == C) {  // next row tile (or next job)
-          flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
-          nch = 0;
-          acc.zero();
-          cur.c = 0;
-          if (++cur.t >= T) {
-            ++cur.j;
-            cur.t = 0;
-            const GemvJob J = job_at(b, cur.j);
-            C = J.C;
-            M = J.M;
-            T = (J.end - J.start) / J.C;
-          }
+        for (int j = 0; j < kStageChunks; ++j) {
+          const uint4 w4 = *reinterpret_cast<const uint4 *>(slot + j * kTileChunkBytes + lane * 16);
+          uint32_t sg = 0;
+          if (FMT == TB_TL2)
+            sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
+          process_chunk<FMT, MT>(w4, sg, act + j * F::kRecBytes, M, acc);
         }
-        const uint4 w4 = *reinterpret_cast<const uint4 *>(slot + j * kTileChunkBytes + lane * 16);
-        uint32_t sg = 0;
-        if (FMT == TB_TL2)
-          sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
-        process_chunk<FMT, MT>(w4, sg, slot_act + j * F::kRecBytes, M, acc);
-        ++nch;
-        ++cur.c;
+        nch += kStageChunks;
+        cur.c += kStageChunks;
+      } else {
+        for (int j = 0; j < nk; ++j) {
+          if (cur.c == C) {  // next row tile (or next job)
+            flush(acc, M);
+            nch = 0;
+            acc.zero();
+            cur.c = 0;
+            if (++cur.t >= T) {
+              ++cur.j;
+              cur.t = 0;
+              load_shape();
+            }
+          }
+          const uint4 w4 = *reinterpret_cast<const uint4 *>(slot + j * kTileChunkBytes + lane * 16);
+          uint32_t sg = 0;
+          if (FMT == TB_TL2)
+            sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
+          const uint8_t *act = kFused ? rtab + cur.c * F::kRecBytes : slot_act + j * F::kRecBytes;
+          process_chunk<FMT, MT>(w4, sg, act, M, acc);
+          ++nch;
+          ++cur.c;
+        }
       }
-    }
-    if (cur.c == C && k + 1 < nst) {  // tile finished exactly at a stage boundary
-      flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
-      nch = 0;
-      acc.zero();
-      cur.c = 0;
-      if (++cur.t >= T) {
-        ++cur.j;
-        cur.t = 0;
-        const GemvJob J = job_at(b, cur.j);
-        C = J.C;
-        M = J.M;
-        T = (J.end - J.start) / J.C;
+      if (cur.c == C && k + 1 < nst) {  // tile finished exactly at a stage boundary
+        flush(acc, M);
+        nch = 0;
+        acc.zero();
+        cur.c = 0;
+        if (++cur.t >= T) {
+          ++cur.j;
+          cur.t = 0;
+          load_shape();
+        }
       }
+      __syncwarp();  // every lane is done reading the slot before it is refilled
+      if (k + kRing < nst)
+        is.issue<FMT, kIssueMain>(b, min(kStageChunks, n - (k + kRing) * kStageChunks), slot, lane);
+      cp_async_commit();
     }
-    __syncwarp();  // every lane is done reading the slot before it is refilled
-    if (k + kRing < nst) is.issue<FMT>(b, min(kStageChunks, n - (k + kRing) * kStageChunks), slot, lane);
-    cp_async_commit();
+    TL_LMARK(3);
+    if (nch > 0) flush(acc, M);
   }
-  TL_MARK(3);
-  if (nch > 0) flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
   TL_MARK(4);
+  if constexpr (kFused) {
+    if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // this step's scales (read by whoever finalises this batch), then the
+    // previous step's outputs: its grid has completed, its sums are visible
+    if (threadIdx.x < b.in.n && b.in.writer[threadIdx.x] == (int)blockIdx.x) {
+      *b.in.scale[threadIdx.x] = s_scale[threadIdx.x];
+      if (((s_badm >> threadIdx.x) & 1) && b.in.flag[threadIdx.x]) atomicOr(b.in.flag[threadIdx.x], 1);
+    }
+    for (int j = 0; j < b.in.prev_njobs; ++j) finalize_one(b.in.prev[j], blockIdx.x, gridDim.x);
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -508,12 +641,12 @@ __global__ void __launch_bounds__(Cfg<FMT, MT>::kThreads, 1)
 
 // The finalize kernel is launched as a programmatic dependent of the GEMV, so
 // its launch latency overlaps the GEMV (it waits in griddepcontrol.wait).
-constexpr int kFinalizeParts = 16;  // CTAs per job in the finalize pass
-
 static int launch_finalize(const GemvBatch &b, cudaStream_t s) {
   const int threads = 256;
+  // one element per thread: every job's accumulators are read concurrently
+  const int parts = (int)std::max<int64_t>(1, ceil_div(b.max_entries, threads));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(kFinalizeParts, b.njobs);
+  cfg.gridDim = dim3(parts, b.njobs);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
@@ -526,15 +659,15 @@ static int launch_finalize(const GemvBatch &b, cudaStream_t s) {
   return TB_OK;
 }
 
-template <int FMT, int MT>
-static int launch_tgemv(GemvBatch &b, cudaStream_t s) {
-  using CF = Cfg<FMT, MT>;
+template <int FMT, int MT, bool kFused = false>
+static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
+  using CF = Cfg<FMT, MT, kFused>;
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    if (cudaFuncSetAttribute(tgemv_kernel<FMT, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             CF::kSmem) != cudaSuccess)
+    if (cudaFuncSetAttribute(tgemv_kernel<FMT, MT, kFused>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, CF::kSmem) != cudaSuccess)
       return TB_ERR_CUDA;
     configured_dev = dev;
   }
@@ -545,20 +678,44 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s) {
   const int nw = grid * CF::kWarps;
   b.base = b.total / nw;
   b.rem = b.total % nw;
+  if (kFused) {
+    // which inputs each CTA's chunk range touches (needs the jobs on the host)
+    const int all = (1 << b.in.n) - 1;
+    for (int v = 0; v < kMaxStepInputs; ++v) b.in.writer[v] = 0;
+    if (b.table == nullptr && grid <= kMaxNeedCtas) {
+      int seen = 0;
+      for (int c = 0; c < grid; ++c) {
+        const int64_t w0 = (int64_t)c * CF::kWarps, w1 = w0 + CF::kWarps;
+        const int64_t lo = w0 * b.base + std::min<int64_t>(w0, b.rem);
+        const int64_t hi = w1 * b.base + std::min<int64_t>(w1, b.rem);
+        int m = 0;
+        for (int j = 0; j < b.njobs; ++j)
+          if (b.jobs[j].start < hi && b.jobs[j].end > lo) m |= 1 << b.jobs[j].src;
+        b.in.need[c] = (uint8_t)m;
+        for (int v = 0; v < b.in.n; ++v)
+          if (((m >> v) & 1) && !((seen >> v) & 1)) b.in.writer[v] = (int16_t)c;
+        seen |= m;
+      }
+      b.in.need[0] |= (uint8_t)(all & ~seen);  // unused inputs: CTA 0 still publishes a scale
+    } else {
+      for (int c = 0; c < kMaxNeedCtas; ++c) b.in.need[c] = (uint8_t)all;
+    }
+  }
   // programmatic dependent launch: the prologue (job lookup, first weight
   // stages) overlaps the tail of the kernel that produced the records
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(CF::kThreads);
-  cfg.dynamicSmemBytes = CF::kSmem;
+  cfg.dynamicSmemBytes = kFused ? CF::kRingBytes + rec_tab_bytes : CF::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, tgemv_kernel<FMT, MT>, b) != cudaSuccess) return TB_ERR_CUDA;
-  return b.defer_finalize ? TB_OK : launch_finalize(b, s);
+  if (cudaLaunchKernelEx(&cfg, tgemv_kernel<FMT, MT, kFused>, b) != cudaSuccess)
+    return TB_ERR_CUDA;
+  return (kFused || b.defer_finalize) ? TB_OK : launch_finalize(b, s);
 }
 
 template <int FMT>
@@ -583,8 +740,8 @@ static int64_t ws_counts_bytes(int64_t rows) {
 static int make_job(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign, int64_t rows,
                     int64_t cols, const uint8_t *rec, int64_t M, const double *a_scale,
                     double w_scale, void *workspace, int32_t *acc_out, double *out64,
-                    float *out32, int64_t start, GemvJob &J) {
-  if (!tiled || !rec || !workspace || rows < 1 || cols < 1 || M < 1 || M > 16 ||
+                    float *out32, int64_t start, GemvJob &J, bool fused = false) {
+  if (!tiled || (!rec && !fused) || !workspace || rows < 1 || cols < 1 || M < 1 || M > 16 ||
       (fmt == TB_TL2 && !tiled_sign) || ((out64 || out32) && !a_scale) ||
       (reinterpret_cast<uintptr_t>(rec) & 15) || (reinterpret_cast<uintptr_t>(tiled) & 15))
     return TB_ERR_ARGUMENT;
@@ -607,6 +764,7 @@ static int make_job(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign, in
   J.M = (int)M;
   J.start = (int)start;
   J.end = (int)(start + T * C);
+  J.src = 0;
   return TB_OK;
 }
 
@@ -614,6 +772,13 @@ static int launch_batch(int fmt, GemvBatch &b, int maxM, cudaStream_t s) {
   if (fmt == TB_I2S) return dispatch_m<TB_I2S>(b, maxM, s);
   if (fmt == TB_TL1) return dispatch_m<TB_TL1>(b, maxM, s);
   if (fmt == TB_TL2) return dispatch_m<TB_TL2>(b, maxM, s);
+  return TB_ERR_ARGUMENT;
+}
+
+static int launch_step(int fmt, GemvBatch &b, int rec_tab_bytes, cudaStream_t s) {
+  if (fmt == TB_I2S) return launch_tgemv<TB_I2S, 1, true>(b, s, rec_tab_bytes);
+  if (fmt == TB_TL1) return launch_tgemv<TB_TL1, 1, true>(b, s, rec_tab_bytes);
+  if (fmt == TB_TL2) return launch_tgemv<TB_TL2, 1, true>(b, s, rec_tab_bytes);
   return TB_ERR_ARGUMENT;
 }
 
@@ -713,19 +878,22 @@ extern "C" int tb_gemv_records(int fmt, const uint8_t *tiled, const uint8_t *til
   if (st != TB_OK) return st;
   b.njobs = 1;
   b.total = b.jobs[0].end;
+  b.max_entries = b.jobs[0].M * b.jobs[0].Npad;
   return launch_batch(fmt, b, (int)M, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int64_t tb_gemv_job_bytes(void) { return (int64_t)sizeof(GemvJob); }
 
 extern "C" int tb_gemv_batch_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
-                                     void *table_host, int64_t *total_chunks, int32_t *max_m) {
+                                     void *table_host, int64_t *total_chunks, int32_t *max_m,
+                                     int64_t *max_entries) {
   if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !descs || !table_host || !total_chunks ||
-      !max_m)
+      !max_m || !max_entries)
     return TB_ERR_ARGUMENT;
   GemvJob *host = static_cast<GemvJob *>(table_host);
   int64_t start = 0;
   int maxM = 1;
+  int64_t maxE = 1;
   for (int64_t j = 0; j < njobs; ++j) {
     const tb_gemv_desc &d = descs[j];
     int st = make_job(fmt, d.tiled, d.tiled_sign, d.rows, d.cols, d.rec, d.M, d.a_scale,
@@ -733,30 +901,114 @@ extern "C" int tb_gemv_batch_prepare(int fmt, int64_t njobs, const tb_gemv_desc 
     if (st != TB_OK) return st;
     start = host[j].end;
     maxM = std::max(maxM, (int)d.M);
+    maxE = std::max(maxE, (int64_t)host[j].M * host[j].Npad);
   }
   *total_chunks = start;
   *max_m = maxM;
+  *max_entries = maxE;
   return TB_OK;
 }
 
 extern "C" int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t njobs,
-                                    int64_t total_chunks, int32_t max_m, int32_t finalize,
-                                    void *stream) {
+                                    int64_t total_chunks, int32_t max_m, int64_t max_entries,
+                                    int32_t finalize, void *stream) {
   if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !table_device || total_chunks < 1 ||
-      total_chunks >= ((int64_t)1 << 31) || max_m < 1 || max_m > 16)
+      total_chunks >= ((int64_t)1 << 31) || max_m < 1 || max_m > 16 || max_entries < 1 ||
+      max_entries >= ((int64_t)1 << 31))
     return TB_ERR_ARGUMENT;
   GemvBatch b{};
   b.table = static_cast<const GemvJob *>(table_device);
   b.njobs = (int)njobs;
   b.total = (int)total_chunks;
   b.defer_finalize = finalize ? 0 : 1;
+  b.max_entries = (int)max_entries;
   return launch_batch(fmt, b, max_m, static_cast<cudaStream_t>(stream));
 }
 
-extern "C" int tb_step_glue(const void *fin_table_device, int64_t fin_njobs, int64_t nq,
-                            const tb_quant_desc *q, void *stream) {
+extern "C" int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
+                                    const int32_t *src, int64_t ninputs, const int64_t *input_k,
+                                    void *table_host, int64_t *total_chunks,
+                                    int64_t *max_entries) {
+  if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !descs || !src || !input_k ||
+      ninputs < 1 || ninputs > kMaxStepInputs || !table_host || !total_chunks || !max_entries)
+    return TB_ERR_ARGUMENT;
+  GemvJob *host = static_cast<GemvJob *>(table_host);
+  int64_t start = 0, maxE = 1;
+  for (int64_t j = 0; j < njobs; ++j) {
+    const tb_gemv_desc &d = descs[j];
+    if (src[j] < 0 || src[j] >= ninputs || d.M != 1 || d.cols != input_k[src[j]])
+      return TB_ERR_ARGUMENT;
+    int st = make_job(fmt, d.tiled, d.tiled_sign, d.rows, d.cols, nullptr, 1, d.a_scale,
+                      d.w_scale, d.workspace, d.acc_out, d.out64, d.out32, start, host[j], true);
+    if (st != TB_OK) return st;
+    host[j].src = src[j];
+    start = host[j].end;
+    maxE = std::max(maxE, (int64_t)host[j].Npad);
+  }
+  *total_chunks = start;
+  *max_entries = maxE;
+  return TB_OK;
+}
+
+extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t njobs,
+                                   int64_t total_chunks, int64_t ninputs,
+                                   const tb_step_input *inputs, int32_t x_after_wait,
+                                   const void *prev_table_device, int64_t prev_njobs,
+                                   const void *table_host, void *stream) {
+  if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !table_device || total_chunks < 1 ||
+      total_chunks >= ((int64_t)1 << 31) || ninputs < 1 || ninputs > kMaxStepInputs ||
+      !inputs || prev_njobs < 0 || (prev_njobs > 0 && !prev_table_device) ||
+      (prev_njobs > 0 && prev_table_device == table_device))
+    return TB_ERR_ARGUMENT;
+  GemvBatch b{};
+  b.table = static_cast<const GemvJob *>(table_device);
+  b.njobs = (int)njobs;
+  b.total = (int)total_chunks;
+  const int rec = fmt == TB_TL2 ? Fmt<TB_TL2>::kRecBytes : Fmt<TB_I2S>::kRecBytes;
+  int64_t off = 0;
+  for (int64_t v = 0; v < ninputs; ++v) {
+    const tb_step_input &in = inputs[v];
+    if (!in.x || !in.scale || in.K < 1) return TB_ERR_ARGUMENT;
+    const int64_t C = ceil_div(ref_row_bytes(fmt, in.K), kChunkBytes);
+    b.in.x[v] = in.x;
+    b.in.scale[v] = in.scale;
+    b.in.flag[v] = in.nonfinite_flag;
+    b.in.K[v] = (int)in.K;
+    b.in.C[v] = (int)C;
+    b.in.off[v] = (int)off;
+    off += C * rec;
+  }
+  if (off > 64 * 1024) return TB_ERR_UNSUPPORTED;  // record tables must fit in shared memory
+  b.in.n = (int)ninputs;
+  b.in.x_after_wait = x_after_wait ? 1 : 0;
+  b.in.prev = static_cast<const GemvJob *>(prev_table_device);
+  b.in.prev_njobs = (int)prev_njobs;
+  if (table_host && njobs <= kMaxInlineJobs) {  // jobs inline in the kernel parameters
+    const GemvJob *h = static_cast<const GemvJob *>(table_host);
+    for (int j = 0; j < njobs; ++j) b.jobs[j] = h[j];
+    b.table = nullptr;
+  }
+  return launch_step(fmt, b, (int)off, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int tb_gemv_batch_finalize(const void *table_device, int64_t njobs,
+                                      int64_t max_entries, void *stream) {
+  if (!table_device || njobs < 1 || njobs > 65535 || max_entries < 1 ||
+      max_entries >= ((int64_t)1 << 31))
+    return TB_ERR_ARGUMENT;
+  GemvBatch b{};
+  b.table = static_cast<const GemvJob *>(table_device);
+  b.njobs = (int)njobs;
+  b.max_entries = (int)max_entries;
+  return launch_finalize(b, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
+                            int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
+                            void *stream) {
   if (nq < 0 || nq > kMaxGlueVecs || (nq > 0 && !q) || fin_njobs < 0 ||
-      (fin_njobs > 0 && !fin_table_device))
+      (fin_njobs > 0 && (!fin_table_device || fin_max_entries < 1 ||
+                         fin_max_entries >= ((int64_t)1 << 31))))
     return TB_ERR_ARGUMENT;
   GlueParams g{};
   g.fin.table = static_cast<const GemvJob *>(fin_table_device);
@@ -785,7 +1037,11 @@ extern "C" int tb_step_glue(const void *fin_table_device, int64_t fin_njobs, int
     tokens += Q.M;
   }
   g.q_tokens = tokens;
-  const int rows = tokens + (int)fin_njobs;
+  // finalize rows: 8 CTAs x 256 threads per group, one accumulator per thread
+  g.fin.fin_parts = fin_njobs > 0 ? (int)ceil_div(fin_max_entries, (int64_t)8 * 256) : 0;
+  const int64_t rows64 = tokens + fin_njobs * g.fin.fin_parts;
+  if (rows64 > 65535) return TB_ERR_ARGUMENT;
+  const int rows = (int)rows64;
   if (rows == 0) return TB_OK;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(8, rows);

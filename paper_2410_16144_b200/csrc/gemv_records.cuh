@@ -146,6 +146,7 @@ __device__ __forceinline__ void quantize_token(
   const double s = a > 0.0 ? a / 127.0 : 1.0;
   const double inv_s = 1.0 / s;
   if (rank == 0 && threadIdx.x == 0) scale[m] = s;
+  const float inv_sf = static_cast<float>(inv_s);
   const int64_t n4 = (int64_t)(ce - cb) * 4;
   for (int64_t base = threadIdx.x - lane; base < n4; base += kThreads) {
     const int64_t idx = base + lane;
@@ -161,7 +162,10 @@ __device__ __forceinline__ void quantize_token(
       for (int b = 0; b < 4; ++b) {
         const int64_t k = k0 + 4 * v + b;
         int q = 0;
-        if (on && k < K) q = quantize_one(static_cast<double>(row[k]), s, inv_s);
+        if (on && k < K) {
+          if constexpr (sizeof(T) == 4) q = quantize_fast(row[k], inv_sf, s, inv_s);
+          else q = quantize_one(static_cast<double>(row[k]), s, inv_s);
+        }
         if (on && qnat && k < ldq) qnat[m * ldq + k] = static_cast<int8_t>(q);
         gs += q;
         word |= (uint32_t)(q & 0xFF) << (8 * b);
@@ -185,6 +189,282 @@ __global__ void __launch_bounds__(kThreads) quantize_records_kernel(
   quantize_token<FMT, T, kThreads>(x, K, ldx, qnat, ldq, scale, C, rec, nonfinite, blockIdx.y,
                                    blockIdx.x, gridDim.x);
 }
+
+// ---------------------------------------------------------------------------
+// CTA-local quantisation (the fused decode step of gemv.cu): every CTA of the
+// GEMV grid quantises the whole input vector itself -- absmax over K floats
+// (L2-resident after the first CTA) and the records of every chunk into its
+// own shared memory -- so no separate quantise launch and no grid-wide
+// dependency precede the weight stream.  Results are identical in every CTA.
+// ---------------------------------------------------------------------------
+template <int kThreads>
+__device__ __forceinline__ float cta_absmax_f32(const float *__restrict__ x, int K, bool &bad,
+                                                float *red) {
+  float amax = 0.f;
+  bool nf = false;
+  const int lane = threadIdx.x & 31;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const int K4 = K >> 2;
+    const float4 *x4 = reinterpret_cast<const float4 *>(x);
+    for (int i = threadIdx.x; i < K4; i += kThreads) {
+      const float4 v = __ldg(x4 + i);
+      nf |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+      amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    for (int k = (K4 << 2) + threadIdx.x; k < K; k += kThreads) {
+      const float v = __ldg(x + k);
+      nf |= !isfinite(v);
+      amax = fmaxf(amax, fabsf(v));
+    }
+  } else {
+    for (int k = threadIdx.x; k < K; k += kThreads) {
+      const float v = __ldg(x + k);
+      nf |= !isfinite(v);
+      amax = fmaxf(amax, fabsf(v));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  nf = __syncthreads_or(nf);
+  if (lane == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  float a = 0.f;
+#pragma unroll
+  for (int i = 0; i < kThreads / 32; ++i) a = fmaxf(a, red[i]);
+  __syncthreads();  // red may be reused
+  bad = nf;
+  return a;  // |x| max in float32 is exact, as is its float64 widening
+}
+
+// Records of every chunk of one token into `rtab` ([C][kRecBytes], shared).
+template <int FMT, int kThreads>
+__device__ __forceinline__ void cta_build_records(const float *__restrict__ x, int K, int C,
+                                                  double s, uint8_t *rtab) {
+  using F = Fmt<FMT>;
+  const int lane = threadIdx.x & 31;
+  const double inv_s = 1.0 / s;
+  const float inv_sf = static_cast<float>(inv_s);
+  const int n4 = C * 4;
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  for (int base = threadIdx.x - lane; base < n4; base += kThreads) {  // warp-uniform
+    const int idx = base + lane;
+    const bool on = idx < n4;
+    const int c = on ? idx >> 2 : 0, i = idx & 3;
+    const int k0 = c * F::kWeights + i * 4 * F::kGroup;
+    uint32_t r[F::kGroup];
+    int32_t gs = 0;
+#pragma unroll
+    for (int v = 0; v < F::kGroup; ++v) {
+      const int kv = k0 + 4 * v;
+      float xv[4];
+      if (on && vec && kv + 3 < K) {
+        const float4 t = __ldg(reinterpret_cast<const float4 *>(x + kv));
+        xv[0] = t.x, xv[1] = t.y, xv[2] = t.z, xv[3] = t.w;
+      } else {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) xv[b] = (on && kv + b < K) ? __ldg(x + kv + b) : 0.f;
+      }
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int q = quantize_fast(xv[b], inv_sf, s, inv_s);  // 0.f -> 0
+        gs += q;
+        word |= (uint32_t)(q & 0xFF) << (8 * b);
+      }
+      r[v] = word;
+    }
+    write_group<FMT>(rtab + c * F::kRecBytes, i, r, gs, on);
+  }
+}
+
+// All inputs of a step at once, values held in registers: every thread loads
+// its record groups (group g = 4 * chunk + i of the concatenated inputs,
+// g = tid + r * kThreads) in ONE round of independent loads -- issued before
+// the weight prefetch so they do not queue behind it -- then the per-input
+// absmax is reduced through shared memory and the records are quantised from
+// the registers.  fits() is false when the inputs exceed kMaxG groups per
+// thread (the caller then uses the looped cta_absmax / cta_build_records).
+template <int FMT, int kThreads, int kMaxG>
+struct RegQuant {
+  using F = Fmt<FMT>;
+  float4 xr[kMaxG][F::kGroup];
+  // Only the inputs this CTA's jobs contract are quantised (`need`, bit v):
+  // they occupy compact slots 0.. in input order; vmap holds slot -> input.
+  int gb1, gb2, gb3;  // first global group of slots 1..3 (INT_MAX past the last)
+  int G;
+  int vmap;
+  const float *const *xs_;
+
+  __device__ __forceinline__ int slot_of(int g) const { return (g >= gb1) + (g >= gb2) + (g >= gb3); }
+  __device__ __forceinline__ int base_of(int c) const {
+    return c == 0 ? 0 : (c == 1 ? gb1 : (c == 2 ? gb2 : gb3));
+  }
+  __device__ __forceinline__ int vid(int c) const { return (vmap >> (4 * c)) & 15; }
+  __device__ __forceinline__ bool fits() const { return G <= kMaxG * kThreads; }
+
+  __device__ __forceinline__ void load(const float *const *xs, const int *Ks, const int *Cs, int n,
+                                       int need) {
+    int acc = 0, gbv[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff}, ns = 0;
+    vmap = 0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      if (v < n && ((need >> v) & 1)) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c == ns) gbv[c] = acc;
+        vmap |= v << (4 * ns);
+        ++ns;
+        acc += 4 * Cs[v];
+      }
+    }
+    gb1 = gbv[1], gb2 = gbv[2], gb3 = gbv[3];
+    G = acc;
+    xs_ = xs;
+    if (!fits()) return;
+#pragma unroll
+    for (int r = 0; r < kMaxG; ++r) {
+      const int g = threadIdx.x + r * kThreads;
+      const int c = g < G ? slot_of(g) : 0;
+      const int v = vid(c);
+      const int local = g - base_of(c);
+      const int k0 = (local >> 2) * F::kWeights + (local & 3) * 4 * F::kGroup;
+      const float *x = xs[v];
+      const int K = Ks[v];
+      const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+#pragma unroll
+      for (int u = 0; u < F::kGroup; ++u) {
+        const int kv = k0 + 4 * u;
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (g < G) {
+          if (vec && kv + 3 < K) {
+            t = __ldg(reinterpret_cast<const float4 *>(x + kv));
+          } else {
+            if (kv < K) t.x = __ldg(x + kv);
+            if (kv + 1 < K) t.y = __ldg(x + kv + 1);
+            if (kv + 2 < K) t.z = __ldg(x + kv + 2);
+            if (kv + 3 < K) t.w = __ldg(x + kv + 3);
+          }
+        }
+        xr[r][u] = t;
+      }
+    }
+  }
+
+  float amx[4], invf[4];  // per-input absmax and 127 / absmax (after reduce)
+
+  // Every thread of the CTA.  Writes s_scale[v] (thread v) and returns the
+  // non-finite mask (bit v) in every thread.
+  __device__ __forceinline__ int reduce(int n, double *s_scale,
+                                        float *red /* [kThreads/32][4] */,
+                                        int *redb /* [kThreads/32] */) {
+    constexpr int kW = kThreads / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float am[4] = {0.f, 0.f, 0.f, 0.f};
+    int badm = 0;
+#pragma unroll
+    for (int r = 0; r < kMaxG; ++r) {
+      const int g = threadIdx.x + r * kThreads;
+      const int v = g < G ? vid(slot_of(g)) : 0;
+      float m = 0.f;
+      bool nf = false;
+#pragma unroll
+      for (int u = 0; u < F::kGroup; ++u) {
+        const float4 t = xr[r][u];
+        nf |= !(isfinite(t.x) && isfinite(t.y) && isfinite(t.z) && isfinite(t.w));
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(t.x), fabsf(t.y)), fmaxf(fabsf(t.z), fabsf(t.w))));
+      }
+#pragma unroll
+      for (int vv = 0; vv < 4; ++vv)
+        if (vv == v) am[vv] = fmaxf(am[vv], m);
+      if (nf) badm |= 1 << v;
+    }
+#pragma unroll
+    for (int vv = 0; vv < 4; ++vv)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) am[vv] = fmaxf(am[vv], __shfl_xor_sync(0xffffffffu, am[vv], o));
+    badm = __reduce_or_sync(0xffffffffu, badm);
+    if (lane == 0) {
+#pragma unroll
+      for (int vv = 0; vv < 4; ++vv) red[warp * 4 + vv] = am[vv];
+      redb[warp] = badm;
+    }
+    __syncthreads();
+    int badmask = 0;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) badmask |= redb[w];
+    // per-input absmax; the scale itself (float64, core.py:128-130) is only
+    // needed by thread v (output) and on the rare near-tie path
+#pragma unroll
+    for (int vv = 0; vv < 4; ++vv) {
+      float a = 0.f;
+#pragma unroll
+      for (int w = 0; w < kW; ++w) a = fmaxf(a, red[w * 4 + vv]);
+      amx[vv] = a;
+      invf[vv] = a > 0.f ? 127.0f / a : 1.0f;  // within 2^-24 of 1/s: quantize_fast's bound
+    }
+#pragma unroll
+    for (int vv = 0; vv < 4; ++vv)
+      if (threadIdx.x == vv && vv < n)
+        s_scale[vv] = amx[vv] > 0.f ? static_cast<double>(amx[vv]) / 127.0 : 1.0;
+    return badmask;
+  }
+
+  // Records of this thread's groups from the registers (after reduce()).
+  __device__ __forceinline__ void records(const int *offs, uint8_t *rtab) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < kMaxG; ++r) {
+      const int gw = (threadIdx.x - lane) + r * kThreads;  // warp-uniform
+      if (gw < G) {
+        const int g = gw + lane;
+        const bool on = g < G;
+        const int c = on ? slot_of(g) : 0;
+        const int v = vid(c);
+        const int local = on ? g - base_of(c) : 0;
+        float inv = invf[0], am = amx[0];
+#pragma unroll
+        for (int vv = 1; vv < 4; ++vv)
+          if (vv == v) inv = invf[vv], am = amx[vv];
+        uint32_t words[F::kGroup];
+        uint32_t tie = 0;  // bit 4u+b: element within 4e-5 of a rounding tie
+#pragma unroll
+        for (int u = 0; u < F::kGroup; ++u) {
+          const float4 t = xr[r][u];
+          const float e[4] = {t.x, t.y, t.z, t.w};
+          uint32_t wd = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const float q = e[b] * inv;
+            const float rq = rintf(q);
+            if (!(fabsf(q - rq) < 0.49996f)) tie |= 1u << (4 * u + b);
+            wd |= ((uint32_t)static_cast<int>(rq) & 0xFFu) << (8 * b);
+          }
+          words[u] = wd;
+        }
+        if (tie) {  // rare: redo the flagged elements in float64 (exact at ties)
+          const double s = am > 0.f ? static_cast<double>(am) / 127.0 : 1.0;
+          const double inv_s = 1.0 / s;
+          const int k0 = (local >> 2) * F::kWeights + (local & 3) * 4 * F::kGroup;
+#pragma unroll 1
+          while (tie) {
+            const int bit = __ffs(tie) - 1;
+            tie &= tie - 1;
+            const float xv = xs_[v][k0 + bit];  // the element itself (cached)
+            const uint32_t qb = (uint32_t)quantize_one(static_cast<double>(xv), s, inv_s) & 0xFFu;
+            const int sh = 8 * (bit & 3);
+#pragma unroll
+            for (int u = 0; u < F::kGroup; ++u)
+              if (u == (bit >> 2)) words[u] = (words[u] & ~(0xFFu << sh)) | (qb << sh);
+          }
+        }
+        int32_t gs = 0;
+#pragma unroll
+        for (int u = 0; u < F::kGroup; ++u) gs = __dp4a((int)words[u], 0x01010101, gs);
+        write_group<FMT>(rtab + offs[v] + (local >> 2) * F::kRecBytes, local & 3, words, gs, on);
+      }
+    }
+  }
+};
 
 // ---------------------------------------------------------------------------
 // decode GEMV
@@ -239,7 +519,7 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
       const uint32_t x2 = W & 0x30303030u, x3 = W & 0xC0C0C0C0u;
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
-        if (m < M) {
+        if (m == 0 || m < M) {  // token 0 always exists: no branch for MT == 1
           const uint4 A = *reinterpret_cast<const uint4 *>(rec0 + m * kTokStride + 16 * i);
           acc.v[m][0] = dp4a_us(x0, A.x, acc.v[m][0]);
           acc.v[m][1] = dp4a_us(x1, A.y, acc.v[m][1]);
@@ -257,7 +537,7 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
       const uint32_t ahi = __umulhi(hi16, 11u << 23) & 0x03030303u;
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
-        if (m < M) {
+        if (m == 0 || m < M) {  // token 0 always exists: no branch for MT == 1
           const uint4 A = *reinterpret_cast<const uint4 *>(rec0 + m * kTokStride + 16 * i);
           acc.v[m][0] = dp4a_us(lo, A.y, acc.v[m][0]);
           acc.v[m][1] = dp4a_us(alo, A.x, acc.v[m][1]);
@@ -290,7 +570,7 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
       }
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
-        if (m < M) {
+        if (m == 0 || m < M) {  // token 0 always exists: no branch for MT == 1
           const uint2 *A = reinterpret_cast<const uint2 *>(rec0 + m * kTokStride + 24 * i);
           const uint2 a01 = A[0], a23 = A[1], a45 = A[2];
           const uint32_t a[6] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y};
@@ -302,7 +582,8 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
   }
 #pragma unroll
   for (int m = 0; m < MT; ++m)
-    if (m < M) acc.csum[m] += *reinterpret_cast<const int32_t *>(rec0 + m * kTokStride + F::kActWords * 4);
+    if (m == 0 || m < M)
+      acc.csum[m] += *reinterpret_cast<const int32_t *>(rec0 + m * kTokStride + F::kActWords * 4);
 }
 
 

@@ -42,8 +42,15 @@ __global__ void __launch_bounds__(kThreads) quantize_kernel(const T *__restrict_
   __syncthreads();
   const double s = s_scale;
   const double inv_s = 1.0 / s;
-  for (int64_t k = threadIdx.x; k < ldq; k += kThreads)
-    qrow[k] = k < K ? static_cast<int8_t>(quantize_one(static_cast<double>(row[k]), s, inv_s)) : 0;
+  const float inv_sf = static_cast<float>(inv_s);
+  for (int64_t k = threadIdx.x; k < ldq; k += kThreads) {
+    int q = 0;
+    if (k < K) {
+      if constexpr (sizeof(T) == 4) q = quantize_fast(row[k], inv_sf, s, inv_s);
+      else q = quantize_one(static_cast<double>(row[k]), s, inv_s);
+    }
+    qrow[k] = static_cast<int8_t>(q);
+  }
 }
 
 // ----------------------------------------------------------------------------

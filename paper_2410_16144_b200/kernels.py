@@ -31,7 +31,7 @@ from .packing import PackedI2S, PackedTL1, PackedTL2
 
 __all__ = ["KernelKind", "WIDEN_GROUPS", "gemv_ref_int32", "gemv_f32_ref", "gemv_i2s",
            "gemv_tl1", "gemv_tl2", "gemv_parallel", "GemvPlan", "GemvBatch", "StepGlue",
-           "ActRecords", "KERNEL_PAD"]
+           "ActRecords", "GemvStep", "KERNEL_PAD"]
 
 WIDEN_GROUPS = 64  # kernels.py:34
 MAX_DECODE_TOKENS = 16
@@ -279,12 +279,14 @@ class GemvBatch:
         host = np.zeros(jb * len(pairs), dtype=np.uint8)
         total = C.c_int64()
         maxm = C.c_int32()
+        maxe = C.c_int64()
         L.check(lib.tb_gemv_batch_prepare(self.fmt, len(pairs), C.cast(descs, C.c_void_p),
                                           host.ctypes.data_as(C.c_void_p), C.byref(total),
-                                          C.byref(maxm)), "gemv_batch_prepare")
+                                          C.byref(maxm), C.byref(maxe)), "gemv_batch_prepare")
         dev = pairs[0][0].main.device
         self.table = torch.from_numpy(host).to(dev)
         self.njobs, self.total, self.max_m = len(pairs), total.value, maxm.value
+        self.max_entries = maxe.value
         self.pairs = pairs  # keep every buffer alive
         self._lib = lib
 
@@ -292,7 +294,8 @@ class GemvBatch:
         """One grouped GEMV launch (+ the finalize pass unless ``finalize`` is
         False, in which case a later StepGlue must finalise this batch)."""
         st = self._lib.tb_gemv_batch_launch(self.fmt, self.table.data_ptr(), self.njobs,
-                                            self.total, self.max_m, 1 if finalize else 0,
+                                            self.total, self.max_m, self.max_entries,
+                                            1 if finalize else 0,
                                             stream_ptr if stream_ptr is not None
                                             else L.stream_ptr())
         if st:
@@ -330,11 +333,118 @@ class StepGlue:
     def run(self, stream_ptr: int | None = None):
         fin = self.fin
         st = self._lib.tb_step_glue(fin.table.data_ptr() if fin is not None else None,
-                                    fin.njobs if fin is not None else 0, len(self.inputs),
+                                    fin.njobs if fin is not None else 0,
+                                    fin.max_entries if fin is not None else 0, len(self.inputs),
                                     self._descs_ptr,
                                     stream_ptr if stream_ptr is not None else L.stream_ptr())
         if st:
             L.check(st, "step_glue")
+
+
+class GemvStep:
+    """A one-token decode step in ONE launch (tb_gemv_step_launch).
+
+    ``pairs`` is a list of (GemvPlan, input index) and ``input_k`` the lengths
+    of the (at most 4) float32 input vectors the jobs contract; gate and up
+    typically share input 0.  Every CTA quantises the inputs itself
+    (quantize_activations, core.py:116-134), so there is no separate
+    quantise launch, and after its own work the launch finalises ``prev`` --
+    the step (or GemvBatch) launched just before it -- whose grid has
+    completed by then.  This step's outputs therefore land in the plans'
+    buffers when the NEXT step runs, or on ``finalize()``.
+    ``x_after_wait``: the inputs are written by the preceding kernel.
+    """
+
+    def __init__(self, pairs, input_k, x_after_wait: bool = False):
+        import ctypes as C
+        import numpy as np
+
+        lib = L.load()
+        fmts = {p.p.FMT for p, _ in pairs}
+        if len(fmts) != 1:
+            raise ValueError("one format per step")
+        if not 1 <= len(input_k) <= 4:
+            raise ValueError("a step takes 1 to 4 input vectors")
+        self.fmt = fmts.pop()
+        self.input_k = [int(k) for k in input_k]
+        dev = pairs[0][0].main.device
+        self.scales = torch.empty(len(input_k), dtype=torch.float64, device=dev)
+        self.flags = torch.zeros(len(input_k), dtype=torch.int32, device=dev)
+        descs = (L.GemvDesc * len(pairs))()
+        src = (C.c_int32 * len(pairs))()
+        ks = (C.c_int64 * len(input_k))(*self.input_k)
+        for i, (d, (plan, v)) in enumerate(zip(descs, pairs)):
+            if not 0 <= v < len(input_k):
+                raise ValueError("input index out of range")
+            if plan.p.cols != self.input_k[v]:
+                raise ValueError("dimension mismatch: input length != matrix cols")
+            d.tiled = plan.main.data_ptr()
+            d.tiled_sign = plan.sign.data_ptr() if plan.sign is not None else None
+            d.rows, d.cols = plan.p.rows, plan.p.cols
+            d.rec, d.M = None, 1
+            d.a_scale, d.w_scale = self.scales[v].data_ptr(), float(plan.p.scale)
+            d.workspace = plan.ws.data_ptr()
+            d.acc_out = L.ptr(plan.acc)
+            d.out64 = L.ptr(plan.out64)
+            d.out32 = L.ptr(plan.out32)
+            src[i] = v
+        host = np.zeros(lib.tb_gemv_job_bytes() * len(pairs), dtype=np.uint8)
+        total = C.c_int64()
+        maxe = C.c_int64()
+        L.check(lib.tb_gemv_step_prepare(self.fmt, len(pairs), C.cast(descs, C.c_void_p),
+                                         C.cast(src, C.c_void_p), len(input_k),
+                                         C.cast(ks, C.c_void_p),
+                                         host.ctypes.data_as(C.c_void_p), C.byref(total),
+                                         C.byref(maxe)), "gemv_step_prepare")
+        self.table = torch.from_numpy(host).to(dev)
+        self._host = host  # also passed at launch: jobs inline, per-CTA input masks
+        self._host_ptr = host.ctypes.data
+        self.njobs, self.total, self.max_entries = len(pairs), total.value, maxe.value
+        self.x_after_wait = bool(x_after_wait)
+        self.inputs = (L.StepInput * len(input_k))()
+        for i, k in enumerate(self.input_k):
+            self.inputs[i].K = k
+            self.inputs[i].scale = self.scales[i].data_ptr()
+            self.inputs[i].nonfinite_flag = self.flags[i].data_ptr()
+        self._inputs_ptr = C.cast(self.inputs, C.c_void_p)
+        self.pairs = pairs  # keep every buffer alive
+        self._lib = lib
+
+    def bind(self, xs):
+        """Point the step at device float32 vectors ``xs`` (read at launch)."""
+        if len(xs) != len(self.input_k):
+            raise ValueError(f"expected {len(self.input_k)} input vectors")
+        for i, (x, k) in enumerate(zip(xs, self.input_k)):
+            if x.dtype != torch.float32 or not x.is_cuda or x.numel() != k or \
+                    not x.is_contiguous():
+                raise ValueError("step inputs must be contiguous CUDA float32 vectors "
+                                 "of the declared lengths")
+            self.inputs[i].x = x.data_ptr()
+        self._bound = xs  # keep alive
+        return self
+
+    def run(self, xs=None, prev=None, stream_ptr: int | None = None):
+        if xs is not None:
+            self.bind(xs)
+        if prev is self:
+            raise ValueError("a step cannot finalise its own previous launch")
+        st = self._lib.tb_gemv_step_launch(
+            self.fmt, self.table.data_ptr(), self.njobs, self.total, len(self.input_k),
+            self._inputs_ptr, 1 if self.x_after_wait else 0,
+            prev.table.data_ptr() if prev is not None else None,
+            prev.njobs if prev is not None else 0, self._host_ptr,
+            stream_ptr if stream_ptr is not None else L.stream_ptr())
+        if st:
+            L.check(st, "gemv_step_launch")
+
+    def finalize(self, stream_ptr: int | None = None):
+        """Finalise this step's outputs now (e.g. after the last step)."""
+        st = self._lib.tb_gemv_batch_finalize(self.table.data_ptr(), self.njobs,
+                                              self.max_entries,
+                                              stream_ptr if stream_ptr is not None
+                                              else L.stream_ptr())
+        if st:
+            L.check(st, "gemv_batch_finalize")
 
 
 class ActRecords:

@@ -348,6 +348,98 @@ def test_grouped_gemv_batch(tb):
                 np.testing.assert_array_equal(host(plan.out64)[:M], w * 0.3 * s[:, None])
 
 
+def _tie_vector(rng, k):
+    """Random f32 vector with amax 127 (scale 1) and exact / near rounding ties."""
+    x = rng.standard_normal(k).astype(np.float32) * 20
+    x[0] = 127.0
+    ties = np.array([0.5, -0.5, 1.5, -2.5, 126.5, -126.5, np.nextafter(np.float32(0.5), 1),
+                     np.nextafter(np.float32(0.5), 0), np.nextafter(np.float32(-2.5), 0)],
+                    dtype=np.float32)
+    x[1:1 + len(ties)] = ties[: max(0, min(len(ties), k - 1))]
+    return x
+
+
+def test_fused_step_sequence(tb):
+    """One-launch decode steps (quantise + grouped GEMV + previous finalize),
+    chained A -> B -> A with the last one finalised explicitly."""
+    rng = np.random.default_rng(21)
+    for fmt, enc in ((1, tb.encode_i2s), (2, tb.encode_tl1), (3, tb.encode_tl2)):
+        k0, k1 = (1000, 97) if fmt != 1 else (1000, 100)
+        shapes = [((70, k0), 0), ((33, k0), 0), ((300, k1), 1), ((4096, k0), 0), ((1, k1), 1)]
+        steps, truth = [], []
+        for sidx in range(2):
+            pairs, vals = [], []
+            for (rows, cols), src in shapes:
+                v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+                ws = 0.3 + 0.1 * sidx
+                plan = tb.GemvPlan(enc(tb.TernaryMatrix(rows, cols, v, ws)),
+                                   out_dtype=torch.float64, want_acc=True)
+                pairs.append((plan, src))
+                vals.append((v, ws))
+            steps.append(tb.GemvStep(pairs, [k0, k1]))
+            truth.append(vals)
+        xs_host = [[_tie_vector(rng, k0), rng.standard_normal(k1).astype(np.float32)]
+                   for _ in range(3)]
+        xs_dev = [[torch.from_numpy(x).cuda() for x in xs] for xs in xs_host]
+
+        def check(si, xi):
+            st = steps[si]
+            q = [O.quantize(x, 1) for x in xs_host[xi]]
+            np.testing.assert_array_equal(host(st.scales), [q[0][1], q[1][1]])
+            for (plan, src), (v, ws) in zip(st.pairs, truth[si]):
+                want = O.gemv_ref_int32(v, q[src][0])
+                assert np.array_equal(host(plan.acc)[0], want), (fmt, si, v.shape)
+                np.testing.assert_array_equal(host(plan.out64)[0],
+                                              want.astype(np.float64) * ws * q[src][1])
+
+        steps[0].run(xs_dev[0])
+        steps[1].run(xs_dev[1], prev=steps[0])
+        torch.cuda.synchronize()
+        check(0, 0)
+        steps[0].run(xs_dev[2], prev=steps[1])
+        torch.cuda.synchronize()
+        check(1, 1)
+        steps[0].finalize()
+        torch.cuda.synchronize()
+        check(0, 2)
+        assert int(host(steps[0].flags).sum()) == 0
+        with pytest.raises(ValueError):
+            steps[0].run(xs_dev[0], prev=steps[0])
+
+
+def test_fused_step_large_input(tb):
+    """Inputs too large for the register-held quantiser take the looped path."""
+    rng = np.random.default_rng(5)
+    for enc in (tb.encode_i2s, tb.encode_tl1, tb.encode_tl2):
+        k = 30001
+        v = rng.integers(-1, 2, size=(45, k), dtype=np.int8)
+        plan = tb.GemvPlan(enc(tb.TernaryMatrix(45, k, v, 0.5)), out_dtype=torch.float64,
+                           want_acc=True)
+        st = tb.GemvStep([(plan, 0)], [k])
+        x = _tie_vector(rng, k)
+        x[17] = 3e-3  # a tiny magnitude as well
+        st.run([torch.from_numpy(x).cuda()])
+        st.finalize()
+        torch.cuda.synchronize()
+        q, s, _ = O.quantize(x, 1)
+        want = O.gemv_ref_int32(v, q)
+        assert host(st.scales)[0] == s
+        assert np.array_equal(host(plan.acc)[0], want)
+        np.testing.assert_array_equal(host(plan.out64)[0], want.astype(np.float64) * 0.5 * s)
+
+
+def test_fused_step_nonfinite_flag(tb):
+    v = np.ones((40, 64), dtype=np.int8)
+    plan = tb.GemvPlan(tb.encode_tl1(tb.TernaryMatrix(40, 64, v, 1.0)), out_dtype=torch.float64)
+    st = tb.GemvStep([(plan, 0)], [64])
+    x = torch.ones(64, device="cuda")
+    x[5] = float("nan")
+    st.run([x])
+    st.finalize()
+    torch.cuda.synchronize()
+    assert int(host(st.flags)[0]) == 1
+
+
 # ------------------------------------------------------- config-sized pins
 
 def _run_large(tb, cname, formats=("i2s", "tl1", "tl2")):

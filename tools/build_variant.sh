@@ -4,10 +4,13 @@
 set -e
 name=$1; shift
 out=/tmp/variant_$name; mkdir -p $out
+pids=()
 for f in abi quantize pack gemv gemv_aux; do
+  rm -f $out/$f.o
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -DTB_TIMELINE "$@" \
     -c paper_2410_16144_b200/csrc/$f.cu -o $out/$f.o &
+  pids+=($!)
 done
-wait
+for p in "${pids[@]}"; do wait $p || { echo "compile failed" >&2; exit 1; }; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared $out/*.o -o tools/lib_$name.so
 echo tools/lib_$name.so

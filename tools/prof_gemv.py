@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--iters", type=int, default=48)
     ap.add_argument("--copies", type=int, default=8)
     ap.add_argument("--eager", action="store_true", help="no graph (for ncu)")
+    ap.add_argument("--with-finalize", action="store_true",
+                    help="time GEMV + finalize pass (default: the GEMV kernel alone)")
     a = ap.parse_args()
     enc = {"i2s": tb.encode_i2s, "tl1": tb.encode_tl1, "tl2": tb.encode_tl2}[a.fmt]
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -41,13 +43,19 @@ def main():
         del w
     x = torch.randn(a.m, a.cols, generator=g, device="cuda")
     rec = tb.ActRecords(plans[0].p.FMT, a.m, a.cols).quantize(x)
+    batches = [tb.GemvBatch([(p, rec)]) for p in plans]
+    fin = a.with_finalize
+
+    def launch(i):
+        batches[i % a.copies].run(finalize=fin)
+
     for i in range(3):
-        plans[i % a.copies].run_records(rec)
+        launch(i)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if a.eager:
         for i in range(a.iters):
-            plans[i % a.copies].run_records(rec)
+            launch(i)
         torch.cuda.synchronize()
         return
     s = torch.cuda.Stream()
@@ -56,7 +64,7 @@ def main():
     with torch.cuda.stream(s):
         with torch.cuda.graph(gr, stream=s):
             for i in range(a.iters):
-                plans[i % a.copies].run_records(rec)
+                launch(i)
     gr.replay()
     torch.cuda.synchronize()
     e0.record()
@@ -69,7 +77,7 @@ def main():
         packed = p.index_data.numel() + p.sign_data.numel()
     else:
         packed = p.data.numel()
-    print(f"{a.fmt} {a.rows}x{a.cols} M={a.m}: graph {us:.2f} us/launch = "
+    print(f"{a.fmt} {a.rows}x{a.cols} M={a.m}{' +fin' if fin else ''}: graph {us:.2f} us/launch = "
           f"{packed / us / 1e3:.1f} GB/s of reference packed bytes")
 
 

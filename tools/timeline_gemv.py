@@ -1,8 +1,9 @@
 """Per-warp timeline of one decode-GEMV launch (debug library built with
 -DTB_TIMELINE into tools/libternary_b200_timeline.so).
 
-Marks: 0 entry, 1 first stages issued, 2 first stage landed, 3 compute done,
-4 flush done.  Prints quantiles of each mark relative to the earliest entry.
+Marks: 0 entry, 1 prologue done (fused step: inputs quantised), 2 first
+stage landed, 3 compute done, 4 flush done.  --step: one fused decode step of
+the bench workload (gate/up/down, two inputs).  Prints quantiles of each mark relative to the earliest entry.
 """
 
 import argparse
@@ -31,7 +32,10 @@ def main():
     ap.add_argument("--fmt", default="tl1")
     ap.add_argument("--rows", type=int, default=14336)
     ap.add_argument("--cols", type=int, default=4096)
+    ap.add_argument("--step", action="store_true")
     a = ap.parse_args()
+    if a.step:
+        return step_timeline()
     enc = {"i2s": tb.encode_i2s, "tl1": tb.encode_tl1, "tl2": tb.encode_tl2}[a.fmt]
     g = torch.Generator(device="cuda").manual_seed(0)
     plans = []
@@ -59,6 +63,43 @@ def main():
             col = rel[:, k]
             print(f"  {name:13s} {col.min():7.2f} {np.median(col):7.2f} "
                   f"{np.quantile(col, 0.9):7.2f} {col.max():7.2f}")
+
+
+def report(name):
+    buf = np.zeros((148 * 32, 5), dtype=np.uint64)
+    lib.tb_timeline_fetch(buf.ctypes.data_as(C.c_void_p), buf.nbytes)
+    used = buf[:, 0] > 0
+    t = buf[used].astype(np.int64)
+    rel = (t - t[:, 0].min()) / 1000.0
+    print(f"{name}: {used.sum()} warps; us since first entry  (min / p50 / p90 / max)")
+    for k, nm in enumerate(["entry", "prologue", "first data", "compute done", "flushed"]):
+        col = rel[:, k]
+        print(f"  {nm:13s} {col.min():7.2f} {np.median(col):7.2f} "
+              f"{np.quantile(col, 0.9):7.2f} {col.max():7.2f}")
+
+
+def step_timeline():
+    H, I = 4096, 14336
+    g = torch.Generator(device="cuda").manual_seed(0)
+    steps = []
+    for c in range(4):
+        plans = []
+        for rows, cols in ((I, H), (I, H), (H, I)):
+            w = torch.randn(rows, cols, generator=g, device="cuda") * 0.02
+            plans.append(tb.GemvPlan(tb.encode_tl1(tb.ternarize_weights(w, rows, cols))))
+            del w
+        steps.append(tb.GemvStep([(plans[0], 0), (plans[1], 0), (plans[2], 1)], [H, I]))
+    xh = torch.randn(H, generator=g, device="cuda")
+    xi = torch.randn(I, generator=g, device="cuda")
+    for i in range(8):
+        steps[i % 4].run([xh, xi], prev=steps[(i - 1) % 4])
+    torch.cuda.synchronize()
+    for trial in range(3):
+        lib.tb_timeline_clear()
+        torch.cuda.synchronize()
+        steps[trial % 4].run([xh, xi], prev=steps[(trial - 1) % 4])
+        torch.cuda.synchronize()
+        report(f"isolated step {trial}")
 
 
 if __name__ == "__main__":
