@@ -55,6 +55,17 @@ def algo_bytes_gemv(rows, cols, m=1):
     return tl1_bytes(rows, cols) + m * cols + 4 * m * rows
 
 
+def measured_traffic():
+    """DRAM bytes per launch of the step kernel from the committed ncu --set full
+    capture (profiles/r1_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            d = json.load(f)
+        return int(d["dram_bytes_read"] + d["dram_bytes_write"])
+    except Exception:
+        return None
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -178,16 +189,19 @@ def make_tl1(tb, torch, rows, cols, seed):
 
 
 def shard_rows(p, tb, torch, r0, r1):
-    """Column-parallel shard: rows [r0, r1) of a packed TL1 matrix (byte slice)."""
+    """Column-parallel shard: rows [r0, r1) of a packed TL1 matrix (tp.column_shard)."""
+    from paper_2410_16144_b200 import tp
+    (data,) = tp.column_shard((p.data,), r0, r1)
     return tb.PackedTL1(rows=r1 - r0, cols=p.cols, padded_cols=p.padded_cols,
-                        data=p.data[r0:r1].contiguous(), scale=p.scale, trusted=True)
+                        data=data.contiguous(), scale=p.scale, trusted=True)
 
 
-def shard_cols(tb, torch, m, k0, k1):
-    """Row-parallel shard: K-slice [k0, k1) (k0 even -> pairs stay whole)."""
-    sub = tb.TernaryMatrix(m.rows, k1 - k0, m.values[:, k0:k1].contiguous(), m.scale,
-                           _checked=True)
-    return tb.encode_tl1(sub)
+def shard_cols(p, tb, torch, k0, k1):
+    """Row-parallel shard: K-slice [k0, k1) as a byte slice (tp.row_shard)."""
+    from paper_2410_16144_b200 import tp
+    (data,), cols = tp.row_shard("tl1", (p.data,), p.cols, k0, k1)
+    return tb.PackedTL1(rows=p.rows, cols=cols, padded_cols=cols + (cols & 1),
+                        data=data.contiguous(), scale=p.scale, trusted=True)
 
 
 def run_gpu(args, rank, world):
@@ -217,7 +231,7 @@ def run_gpu(args, rank, world):
                 p = shard_rows(full, tb, torch, rank * per, (rank + 1) * per)
             else:
                 per = cols // tp
-                p = shard_cols(tb, torch, m, rank * per, (rank + 1) * per)
+                p = shard_cols(tb.encode_tl1(m), tb, torch, rank * per, (rank + 1) * per)
             p.tiled()
             mats[name] = p
         if c == 0:
@@ -369,13 +383,14 @@ def run_gpu(args, rank, world):
                    "parallelism": "tp1" if tp == 1 else f"tp{tp} (col-parallel gate/up, "
                                   "row-parallel down + NCCL int32 all-reduce)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": measured_traffic() if tp == 1 else None,
                      "kernel": ("tgemv_kernel<TL1,1,fused> one-launch step: quantise x_h, x_i + "
                                 "gate/up (14336x4096) + down (4096x14336) + previous finalize")
                                if tp == 1 else "tgemv_kernel<TL1,1> grouped gate+up+down",
                      "bytes_per_launch": gemv_bytes, "launch_us": round(gemv_ms * 1e3, 3),
                      "peak_kind": f"{peak_kind} hbm_gbs (copy)"},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches_per_step * args.steps + (1 if tp == 1 else 0),
         "clocks": clk.summary(),
     }
 
@@ -386,20 +401,11 @@ def run_gpu(args, rank, world):
         n_e2e = max(10, min(args.steps, 200))
         xh_h = torch.randn(NX, H).pin_memory()
         xi_h = torch.randn(NX, I).pin_memory()
-        xh_d = torch.empty(H, device=dev)
-        xi_d = torch.empty(I, device=dev)
-        out_h = torch.empty(2 * I + H, dtype=torch.float32).pin_memory()
+        hosts = [tb.HostStep([(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)], [H, I])
+                 for pl in plans]
 
         def e2e_step(i):
-            pl = plans[i % NCOPY]
-            xh_d.copy_(xh_h[i % NX], non_blocking=True)
-            xi_d.copy_(xi_h[i % NX], non_blocking=True)
-            pl["step"].run([xh_d, xi_d])
-            pl["step"].finalize()
-            out_h[:I].copy_(pl["gate"].out32[0], non_blocking=True)
-            out_h[I:2 * I].copy_(pl["up"].out32[0], non_blocking=True)
-            out_h[2 * I:].copy_(pl["down"].out32[0], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            return hosts[i % NCOPY]([xh_h[i % NX], xi_h[i % NX]])
 
         for i in range(5):
             e2e_step(i)
@@ -411,8 +417,9 @@ def run_gpu(args, rank, world):
                          "h2d_bytes_per_step": (H + I) * 4,
                          "d2h_bytes_per_step": (2 * I + H) * 4,
                          "steps": n_e2e,
-                         "path": "tb.GemvStep.run (one launch) + finalize per token; pinned host "
-                                 "f32 inputs in, fp32 outputs to pinned host, stream sync per step"}
+                         "path": "tb.HostStep: host f32 inputs -> pinned staging -> one CUDA graph "
+                                 "(H2D, fused step kernel, finalize, D2H) -> fp32 outputs on the "
+                                 "host, stream sync per token"}
 
         # the reference-shaped per-call API (quantize_activations + gemv_parallel
         # per projection, float64 GemvResult.output to host)

@@ -227,7 +227,8 @@ typedef struct tb_step_input {
   const float *x;          /* [K] float32 (device; 16-B alignment preferred)  */
   int64_t K;
   double *scale;           /* out: absmax / 127 (or 1) of this vector         */
-  int32_t *nonfinite_flag; /* optional: set to 1 on NaN / inf input          */
+  int32_t *nonfinite_flag; /* optional: 1 if this launch saw NaN / inf, else 0
+                            (device or mapped pinned host memory)            */
 } tb_step_input;
 int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
                          const int32_t *src, int64_t ninputs, const int64_t *input_k,

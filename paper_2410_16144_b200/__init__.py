@@ -24,6 +24,7 @@ from .kernels import (
     GemvBatch,
     GemvPlan,
     GemvStep,
+    HostStep,
     StepGlue,
     KernelKind,
     gemv_f32_ref,

@@ -629,7 +629,8 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, kFused>::kThreads, 1)
     // previous step's outputs: its grid has completed, its sums are visible
     if (threadIdx.x < b.in.n && b.in.writer[threadIdx.x] == (int)blockIdx.x) {
       *b.in.scale[threadIdx.x] = s_scale[threadIdx.x];
-      if (((s_badm >> threadIdx.x) & 1) && b.in.flag[threadIdx.x]) atomicOr(b.in.flag[threadIdx.x], 1);
+      // plain store (this launch's verdict): the flag may live in mapped host memory
+      if (b.in.flag[threadIdx.x]) *b.in.flag[threadIdx.x] = (s_badm >> threadIdx.x) & 1;
     }
     for (int j = 0; j < b.in.prev_njobs; ++j) finalize_one(b.in.prev[j], blockIdx.x, gridDim.x);
   }

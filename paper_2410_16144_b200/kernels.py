@@ -31,7 +31,7 @@ from .packing import PackedI2S, PackedTL1, PackedTL2
 
 __all__ = ["KernelKind", "WIDEN_GROUPS", "gemv_ref_int32", "gemv_f32_ref", "gemv_i2s",
            "gemv_tl1", "gemv_tl2", "gemv_parallel", "GemvPlan", "GemvBatch", "StepGlue",
-           "ActRecords", "GemvStep", "KERNEL_PAD"]
+           "ActRecords", "GemvStep", "HostStep", "KERNEL_PAD"]
 
 WIDEN_GROUPS = 64  # kernels.py:34
 MAX_DECODE_TOKENS = 16
@@ -355,7 +355,7 @@ class GemvStep:
     ``x_after_wait``: the inputs are written by the preceding kernel.
     """
 
-    def __init__(self, pairs, input_k, x_after_wait: bool = False):
+    def __init__(self, pairs, input_k, x_after_wait: bool = False, flags=None):
         import ctypes as C
         import numpy as np
 
@@ -369,7 +369,9 @@ class GemvStep:
         self.input_k = [int(k) for k in input_k]
         dev = pairs[0][0].main.device
         self.scales = torch.empty(len(input_k), dtype=torch.float64, device=dev)
-        self.flags = torch.zeros(len(input_k), dtype=torch.int32, device=dev)
+        # per-input non-finite verdict of the last launch (device, or pinned host)
+        self.flags = (flags if flags is not None
+                      else torch.zeros(len(input_k), dtype=torch.int32, device=dev))
         descs = (L.GemvDesc * len(pairs))()
         src = (C.c_int32 * len(pairs))()
         ks = (C.c_int64 * len(input_k))(*self.input_k)
@@ -445,6 +447,80 @@ class GemvStep:
                                               else L.stream_ptr())
         if st:
             L.check(st, "gemv_batch_finalize")
+
+
+class HostStep:
+    """A decode step driven from HOST memory: ``__call__(xs)`` copies the
+    float32 input vectors in, runs the one-launch step and its finalize, and
+    returns the outputs on the host.
+
+    ``pairs`` / ``input_k`` are as for GemvStep.  The inputs travel in ONE
+    host-to-device copy (one pinned staging buffer); the finalize writes the
+    outputs and the step its non-finite verdict straight into mapped pinned
+    host memory (zero-copy), so a token is one captured graph -- copy, step
+    kernel, finalize -- and one stream synchronisation.
+    """
+
+    def __init__(self, pairs, input_k, out_dtype=torch.float32):
+        import types
+
+        if out_dtype not in (torch.float32, torch.float64):
+            raise ValueError("out_dtype must be float32 or float64")
+        dev = pairs[0][0].main.device
+        offs, n = [], 0
+        for k in input_k:
+            offs.append(n)
+            n += -(-int(k) // 4) * 4  # 16-byte aligned vectors
+        self.x_host_all = torch.empty(n, dtype=torch.float32).pin_memory()
+        self.x_dev_all = torch.empty(n, dtype=torch.float32, device=dev)
+        self.x_host = [self.x_host_all[o:o + k] for o, k in zip(offs, input_k)]
+        self.x_dev = [self.x_dev_all[o:o + k] for o, k in zip(offs, input_k)]
+        self.out_host = []
+        host_pairs = []
+        for plan, v in pairs:
+            o = torch.empty((1, plan.p.rows), dtype=out_dtype).pin_memory()
+            self.out_host.append(o[0])
+            host_pairs.append((types.SimpleNamespace(
+                p=plan.p, main=plan.main, sign=plan.sign, ws=plan.ws, acc=None,
+                out32=o if out_dtype == torch.float32 else None,
+                out64=o if out_dtype == torch.float64 else None), v))
+        self.flags_host = torch.zeros(len(input_k), dtype=torch.int32).pin_memory()
+        self._flags_np = self.flags_host.numpy()  # shares the pinned buffer
+        self.step = GemvStep(host_pairs, input_k, flags=self.flags_host)
+        self._record = self._capture()
+        self._stream = torch.cuda.current_stream()
+
+    def _issue(self):
+        self.x_dev_all.copy_(self.x_host_all, non_blocking=True)
+        self.step.run(self.x_dev)
+        self.step.finalize()
+
+    def _capture(self):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self._issue()  # warm-up (kernel attributes) outside the capture
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self._issue()
+        torch.cuda.synchronize()
+        return g
+
+    def __call__(self, xs):
+        if len(xs) != len(self.x_host):
+            raise ValueError(f"expected {len(self.x_host)} input vectors")
+        try:
+            for h, x in zip(self.x_host, xs):
+                h.copy_(x if isinstance(x, torch.Tensor) else torch.from_numpy(x))
+        except RuntimeError as e:
+            raise ValueError("dimension mismatch: input length != matrix cols") from e
+        self._record.replay()
+        self._stream.synchronize()
+        if self._flags_np.any():
+            raise ValueError("activations must be finite")  # core.py:116-134
+        return self.out_host
 
 
 class ActRecords:

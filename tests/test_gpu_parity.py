@@ -428,6 +428,77 @@ def test_fused_step_large_input(tb):
         np.testing.assert_array_equal(host(plan.out64)[0], want.astype(np.float64) * 0.5 * s)
 
 
+def test_tp_shards_through_kernels(tb):
+    """Row-parallel K-slices (byte slices of the reference planes) through the
+    CUDA GEMV: the int32 partials sum to the unsharded result (what the NCCL
+    all-reduce computes across ranks); column shards concatenate to it."""
+    from paper_2410_16144_b200 import tp
+    rng = np.random.default_rng(8)
+    rows, cols = 300, 2000
+    v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    x = rng.standard_normal(cols).astype(np.float32)
+    q, s, _ = O.quantize(x, 1)
+    want = O.gemv_ref_int32(v, q)
+    K = tb.KernelKind
+    for name, enc, kind in (("i2s", tb.encode_i2s, K.I2_S), ("tl1", tb.encode_tl1, K.TL1),
+                            ("tl2", tb.encode_tl2, K.TL2)):
+        full = enc(tb.TernaryMatrix(rows, cols, v, 1.0))
+        planes = (full.index_data, full.sign_data) if name == "tl2" else (full.data,)
+        cls = type(full)
+        for world in (2, 4):
+            total = np.zeros(rows, dtype=np.int64)
+            for r in range(world):
+                k0, k1 = tp.shard_range(cols, world, r, tp.K_ALIGN[full.FMT])
+                sp, sc = tp.row_shard(name, planes, cols, k0, k1)
+                pc = -(-sc // {1: 4, 2: 2, 3: 6}[full.FMT]) * {1: 4, 2: 2, 3: 6}[full.FMT]
+                if name == "tl2":
+                    shard = cls(rows=rows, cols=sc, padded_cols=pc, index_data=sp[0].contiguous(),
+                                sign_data=sp[1].contiguous(), scale=1.0)
+                else:
+                    shard = cls(rows=rows, cols=sc, padded_cols=pc, data=sp[0].contiguous(),
+                                scale=1.0)
+                # the shard's activations are the full vector's codes (one scale)
+                qa = tb.QuantizedActivations(data=torch.from_numpy(q[k0:k1]).cuda(), scale=s,
+                                             original_len=k1 - k0)
+                total += host(tb.gemv_parallel(kind, shard, qa).accumulators).astype(np.int64)
+            assert np.array_equal(total, want), (name, world)
+            r0, r1 = tp.shard_range(rows, world, 1)
+            cs = tp.column_shard(planes, r0, r1)
+            if name == "tl2":
+                shard = cls(rows=r1 - r0, cols=cols, padded_cols=full.padded_cols,
+                            index_data=cs[0].contiguous(), sign_data=cs[1].contiguous(), scale=1.0)
+            else:
+                shard = cls(rows=r1 - r0, cols=cols, padded_cols=full.padded_cols,
+                            data=cs[0].contiguous(), scale=1.0)
+            qa = tb.QuantizedActivations(data=torch.from_numpy(q).cuda(), scale=s,
+                                         original_len=cols)
+            assert np.array_equal(host(tb.gemv_parallel(kind, shard, qa).accumulators),
+                                  want[r0:r1])
+
+
+def test_host_step(tb):
+    """Host-memory decode step (one graph: H2D, step, finalize, D2H)."""
+    rng = np.random.default_rng(31)
+    v0 = rng.integers(-1, 2, size=(200, 640), dtype=np.int8)
+    v1 = rng.integers(-1, 2, size=(64, 300), dtype=np.int8)
+    p0 = tb.GemvPlan(tb.encode_tl1(tb.TernaryMatrix(200, 640, v0, 0.25)), out_dtype=torch.float32)
+    p1 = tb.GemvPlan(tb.encode_tl1(tb.TernaryMatrix(64, 300, v1, 0.5)), out_dtype=torch.float64)
+    hs = tb.HostStep([(p0, 0), (p1, 1)], [640, 300])
+    for _ in range(3):
+        x0 = rng.standard_normal(640).astype(np.float32)
+        x1 = rng.standard_normal(300).astype(np.float32)
+        o0, o1 = hs([x0, x1])
+        (q0, s0, _), (q1, s1, _) = O.quantize(x0, 1), O.quantize(x1, 1)
+        w0 = O.gemv_ref_int32(v0, q0).astype(np.float64) * 0.25 * s0
+        w1 = O.gemv_ref_int32(v1, q1).astype(np.float64) * 0.5 * s1
+        np.testing.assert_array_equal(o0.numpy(), w0.astype(np.float32))
+        np.testing.assert_array_equal(o1.numpy(), w1.astype(np.float32))
+    bad = np.ones(640, np.float32)
+    bad[3] = np.inf
+    with pytest.raises(ValueError, match="activations must be finite"):
+        hs([bad, x1])
+
+
 def test_fused_step_nonfinite_flag(tb):
     v = np.ones((40, 64), dtype=np.int8)
     plan = tb.GemvPlan(tb.encode_tl1(tb.TernaryMatrix(40, 64, v, 1.0)), out_dtype=torch.float64)
