@@ -249,6 +249,33 @@ int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
             double w_scale, void *workspace, int32_t *acc_out, double *out64,
             float *out32, void *stream);
 
+/* Prefill GEMM (BASELINE configs[3]) on the tcgen05 int8 tensor cores:
+ * D[m][n] = sum_k act[m][k] * w[n][k], exact int32, for M tokens at once --
+ * each row m equals the reference's gemv_parallel of token m (kernels.py:
+ * 189-268; the reference has no GEMM, a batch is M GEMV calls).  Weights in
+ * the tiled layout (tb_repack; I2_S or TL1), act int8 [M][lda] with lda a
+ * multiple of 16, >= cols, zero beyond cols (tb_quantize_* padding).
+ * Outputs as tb_gemv, [M][rows] row-major per job, each may be NULL.
+ * tb_gemm_batch: up to 8 GEMMs over the same M in one launch (e.g. a layer's
+ * projections), M <= 512 per launch; tb_gemm_i8 loops over M.              */
+typedef struct tb_gemm_desc {
+  const uint8_t *tiled;
+  int64_t rows, cols;
+  const int8_t *act;
+  int64_t lda;
+  const double *a_scale;
+  double w_scale;
+  int32_t *acc_out;
+  double *out64;
+  float *out32;
+} tb_gemm_desc;
+int tb_gemm_batch(int fmt, int64_t njobs, const tb_gemm_desc *descs, int64_t M,
+                  void *stream);
+int tb_gemm_i8(int fmt, const uint8_t *tiled, int64_t rows, int64_t cols,
+               const int8_t *act, int64_t M, int64_t lda, const double *a_scale,
+               double w_scale, int32_t *acc_out, double *out64, float *out32,
+               void *stream);
+
 /* LUT-driven TL1/TL2 GEMV for a caller-supplied LUT (gemv_tl1/gemv_tl2 with
  * an explicit LutTL1/LutTL2, kernels.py:109-157): lut int16 [groups][9|14];
  * every lookup reads the given entries, so corrupted tables behave exactly

@@ -27,6 +27,7 @@ from .kernels import (
     HostStep,
     StepGlue,
     KernelKind,
+    gemm_prefill,
     gemv_f32_ref,
     gemv_i2s,
     gemv_parallel,

@@ -62,9 +62,8 @@ _SIGS = {
     "tb_gemv_lut": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _p, _p]),
     "tb_gemv_ref_int32": (_i32, [_p, _i64, _i64, _p, _p, _p]),
     "tb_gemv_f32_ref": (_i32, [_p, _i64, _i64, _f32, _p, _p, _p]),
-    "tb_gemm_i8": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _i64, _p, _f64, _p, _p, _p,
-                          _p, _p]),
-    "tb_gemm_workspace_bytes": (_i64, [_i32, _i64, _i64, _i64]),
+    "tb_gemm_batch": (_i32, [_i32, _i64, _p, _i64, _p]),
+    "tb_gemm_i8": (_i32, [_i32, _p, _i64, _i64, _p, _i64, _i64, _p, _f64, _p, _p, _p, _p]),
 }
 
 class GemvDesc(C.Structure):
@@ -81,6 +80,14 @@ class QuantDesc(C.Structure):
     _fields_ = [("x", _p), ("x_is_f64", C.c_int32), ("fmt", C.c_int32), ("M", _i64),
                 ("K", _i64), ("ldx", _i64), ("q", _p), ("ldq", _i64), ("scale", _p),
                 ("rec", _p), ("nonfinite_flag", _p)]
+
+
+class GemmDesc(C.Structure):
+    """Mirror of tb_gemm_desc (include/ternary_b200.h)."""
+
+    _fields_ = [("tiled", _p), ("rows", _i64), ("cols", _i64), ("act", _p), ("lda", _i64),
+                ("a_scale", _p), ("w_scale", _f64), ("acc_out", _p), ("out64", _p),
+                ("out32", _p)]
 
 
 class StepInput(C.Structure):

@@ -31,7 +31,7 @@ from .packing import PackedI2S, PackedTL1, PackedTL2
 
 __all__ = ["KernelKind", "WIDEN_GROUPS", "gemv_ref_int32", "gemv_f32_ref", "gemv_i2s",
            "gemv_tl1", "gemv_tl2", "gemv_parallel", "GemvPlan", "GemvBatch", "StepGlue",
-           "ActRecords", "GemvStep", "HostStep", "KERNEL_PAD"]
+           "ActRecords", "GemvStep", "HostStep", "KERNEL_PAD", "gemm_prefill"]
 
 WIDEN_GROUPS = 64  # kernels.py:34
 MAX_DECODE_TOKENS = 16
@@ -85,8 +85,46 @@ def gemv_f32_ref(m: TernaryMatrix, x) -> GemvResult:
     return GemvResult(accumulators=None, output=out.to(torch.float64))
 
 
+GEMM_MIN_TOKENS = 64  # from this many tokens on, I2_S / TL1 batches use the tensor cores
+
+
+def _gemm_operand(acts: torch.Tensor) -> torch.Tensor:
+    """int8 [M, K] with a 16-byte-multiple row stride (zero padded), as the
+    tcgen05 GEMM's A operand."""
+    M, K = acts.shape
+    if acts.is_contiguous() and K % 16 == 0 and acts.data_ptr() % 16 == 0:
+        return acts
+    buf = torch.zeros((M, -(-K // 16) * 16), dtype=torch.int8, device=acts.device)
+    buf[:, :K] = acts
+    return buf
+
+
+def gemm_prefill(p, a: QuantizedActivations, want_out64: bool = True) -> GemvResult:
+    """Prefill: all M tokens of ``a`` against one packed I2_S / TL1 matrix on
+    the tcgen05 int8 tensor cores (tb_gemm_i8).  Row m of the result is the
+    reference's gemv_parallel for token m (kernels.py:189-268)."""
+    if p.FMT not in (L.I2S, L.TL1):
+        raise ValueError("tensor-core GEMM supports I2_S and TL1 weights")
+    lib = L.load()
+    main, _ = p.tiled()
+    acts = _gemm_operand(a.data.reshape(a.tokens, -1))
+    M, lda = acts.shape
+    dev = main.device
+    acc = torch.empty((M, p.rows), dtype=torch.int32, device=dev)
+    out = torch.empty((M, p.rows), dtype=torch.float64, device=dev) if want_out64 else None
+    L.check(lib.tb_gemm_i8(p.FMT, L.ptr(main), p.rows, p.cols, L.ptr(acts), M, lda,
+                           L.ptr(a.scales), float(p.scale), L.ptr(acc), L.ptr(out), None,
+                           L.stream_ptr()), "gemm_i8")
+    shape = _out_shape(a, p.rows)
+    return GemvResult(accumulators=acc.reshape(shape),
+                      output=out.reshape(shape) if out is not None else None)
+
+
 def _tiled_gemv(p, a: QuantizedActivations, want_out64: bool = True) -> GemvResult:
-    """Decode GEMV through the C ABI (LUT implicit; M <= 16 tokens per launch)."""
+    """Decode GEMV through the C ABI (LUT implicit; M <= 16 tokens per launch);
+    batches of GEMM_MIN_TOKENS or more I2_S / TL1 tokens go to the GEMM."""
+    if a.tokens >= GEMM_MIN_TOKENS and p.FMT in (L.I2S, L.TL1):
+        return gemm_prefill(p, a, want_out64)
     lib = L.load()
     main, sign = p.tiled()
     acts = a.data.reshape(a.tokens, -1)

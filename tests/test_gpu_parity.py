@@ -476,6 +476,58 @@ def test_tp_shards_through_kernels(tb):
                                   want[r0:r1])
 
 
+@pytest.mark.parametrize("M,rows,cols", [(1, 130, 256), (64, 128, 128), (128, 256, 512),
+                                         (200, 300, 1000), (512, 129, 4096), (700, 64, 192)])
+def test_prefill_gemm_tensor_cores(tb, M, rows, cols):
+    """tcgen05 kind::i8 GEMM: every token's row equals the reference GEMV of
+    that token (exact int32, f64 outputs), I2_S and TL1, ragged M/N/K."""
+    rng = np.random.default_rng(M * 7 + rows)
+    v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    x = rng.standard_normal((M, cols)).astype(np.float32)
+    x[0, : min(cols, 4)] = [127.0, -0.5, 0.5, 2.5][: min(cols, 4)]
+    qa = tb.quantize_activations(torch.from_numpy(x).cuda())
+    q = host(qa.data.reshape(M, -1))
+    scales = host(qa.scales)
+    want = np.stack([O.gemv_ref_int32(v, q[m]) for m in range(M)])
+    for enc in (tb.encode_i2s, tb.encode_tl1):
+        p = enc(tb.TernaryMatrix(rows, cols, v, 0.75))
+        r = tb.gemm_prefill(p, qa)
+        acc = host(r.accumulators).reshape(M, rows)
+        assert np.array_equal(acc, want), (enc.__name__, M, rows, cols)
+        np.testing.assert_array_equal(host(r.output).reshape(M, rows),
+                                      want.astype(np.float64) * 0.75 * scales[:, None])
+
+
+def test_prefill_gemm_batch_grouped(tb):
+    """One launch over several projections with two inputs (a layer's q/k/v/o/
+    gate/up on x_h, down on x_i), through the C ABI."""
+    from paper_2410_16144_b200 import _lib as L
+    import ctypes as C
+    lib = L.load()
+    rng = np.random.default_rng(3)
+    M, H, I = 256, 512, 1024
+    xh = tb.quantize_activations(torch.from_numpy(rng.standard_normal((M, H)).astype(np.float32)).cuda())
+    xi = tb.quantize_activations(torch.from_numpy(rng.standard_normal((M, I)).astype(np.float32)).cuda())
+    shapes = [(H, H, xh), (128, H, xh), (128, H, xh), (H, H, xh), (I, H, xh), (I, H, xh), (H, I, xi)]
+    descs = (L.GemmDesc * len(shapes))()
+    keep, wants = [], []
+    for d, (n, k, qa) in zip(descs, shapes):
+        v = rng.integers(-1, 2, size=(n, k), dtype=np.int8)
+        p = tb.encode_i2s(tb.TernaryMatrix(n, k, v, 1.0))
+        main, _ = p.tiled()
+        acc = torch.empty((M, n), dtype=torch.int32, device="cuda")
+        d.tiled, d.rows, d.cols = main.data_ptr(), n, k
+        d.act, d.lda = qa.data.data_ptr(), qa.data.stride(0)
+        d.a_scale, d.w_scale, d.acc_out = qa.scales.data_ptr(), 1.0, acc.data_ptr()
+        keep.append((p, main, acc, qa))
+        q = host(qa.data)
+        wants.append(np.stack([O.gemv_ref_int32(v, q[m]) for m in range(M)]))
+    L.check(lib.tb_gemm_batch(1, len(shapes), C.cast(descs, C.c_void_p), M, L.stream_ptr()))
+    torch.cuda.synchronize()
+    for (p, main, acc, qa), want in zip(keep, wants):
+        assert np.array_equal(host(acc), want)
+
+
 def test_host_step(tb):
     """Host-memory decode step (one graph: H2D, step, finalize, D2H)."""
     rng = np.random.default_rng(31)
