@@ -253,16 +253,21 @@ int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
  * D[m][n] = sum_k act[m][k] * w[n][k], exact int32, for M tokens at once --
  * each row m equals the reference's gemv_parallel of token m (kernels.py:
  * 189-268; the reference has no GEMM, a batch is M GEMV calls).  Weights in
- * the tiled layout (tb_repack; I2_S or TL1), act int8 [M][lda] with lda a
- * multiple of 16, >= cols, zero beyond cols (tb_quantize_* padding).
+ * the tiled layout (tb_repack; I2_S or TL1).  Activations are first tiled
+ * into the tensor-core operand order (tb_gemm_tile_act: int8 [M][lda], zero
+ * beyond cols, M <= 512; out = tb_gemm_act_bytes(M, cols) bytes, 16-B
+ * aligned); GEMMs over the same input share the tiled copy.
  * Outputs as tb_gemv, [M][rows] row-major per job, each may be NULL.
- * tb_gemm_batch: up to 8 GEMMs over the same M in one launch (e.g. a layer's
- * projections), M <= 512 per launch; tb_gemm_i8 loops over M.              */
+ * tb_gemm_batch: up to 8 GEMMs over the same M <= 512 in one launch (e.g. a
+ * layer's projections).  tb_gemm_i8: one matrix, any M, natural int8 input,
+ * `workspace` of tb_gemm_act_bytes(min(M, 512), cols) bytes.               */
+int64_t tb_gemm_act_bytes(int64_t M, int64_t cols);
+int tb_gemm_tile_act(const int8_t *act, int64_t M, int64_t lda, int64_t cols,
+                     uint8_t *act_tiled, void *stream);
 typedef struct tb_gemm_desc {
   const uint8_t *tiled;
   int64_t rows, cols;
-  const int8_t *act;
-  int64_t lda;
+  const uint8_t *act_tiled;
   const double *a_scale;
   double w_scale;
   int32_t *acc_out;
@@ -273,8 +278,8 @@ int tb_gemm_batch(int fmt, int64_t njobs, const tb_gemm_desc *descs, int64_t M,
                   void *stream);
 int tb_gemm_i8(int fmt, const uint8_t *tiled, int64_t rows, int64_t cols,
                const int8_t *act, int64_t M, int64_t lda, const double *a_scale,
-               double w_scale, int32_t *acc_out, double *out64, float *out32,
-               void *stream);
+               double w_scale, uint8_t *workspace, int32_t *acc_out, double *out64,
+               float *out32, void *stream);
 
 /* LUT-driven TL1/TL2 GEMV for a caller-supplied LUT (gemv_tl1/gemv_tl2 with
  * an explicit LutTL1/LutTL2, kernels.py:109-157): lut int16 [groups][9|14];

@@ -63,7 +63,9 @@ _SIGS = {
     "tb_gemv_ref_int32": (_i32, [_p, _i64, _i64, _p, _p, _p]),
     "tb_gemv_f32_ref": (_i32, [_p, _i64, _i64, _f32, _p, _p, _p]),
     "tb_gemm_batch": (_i32, [_i32, _i64, _p, _i64, _p]),
-    "tb_gemm_i8": (_i32, [_i32, _p, _i64, _i64, _p, _i64, _i64, _p, _f64, _p, _p, _p, _p]),
+    "tb_gemm_i8": (_i32, [_i32, _p, _i64, _i64, _p, _i64, _i64, _p, _f64, _p, _p, _p, _p, _p]),
+    "tb_gemm_act_bytes": (_i64, [_i64, _i64]),
+    "tb_gemm_tile_act": (_i32, [_p, _i64, _i64, _i64, _p, _p]),
 }
 
 class GemvDesc(C.Structure):
@@ -85,7 +87,7 @@ class QuantDesc(C.Structure):
 class GemmDesc(C.Structure):
     """Mirror of tb_gemm_desc (include/ternary_b200.h)."""
 
-    _fields_ = [("tiled", _p), ("rows", _i64), ("cols", _i64), ("act", _p), ("lda", _i64),
+    _fields_ = [("tiled", _p), ("rows", _i64), ("cols", _i64), ("act_tiled", _p),
                 ("a_scale", _p), ("w_scale", _f64), ("acc_out", _p), ("out64", _p),
                 ("out32", _p)]
 

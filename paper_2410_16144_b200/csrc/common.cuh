@@ -88,6 +88,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 }
 
+// Pure polling (mbarrier.test_wait never suspends the thread): lowest
+// hand-off latency for the tight producer / MMA / unpack rings of the GEMM.
+__device__ __forceinline__ bool mbar_test_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
+  while (!mbar_test_wait(bar, parity)) {
+  }
+}
+
 // 1-D bulk async copy global -> shared, completion via mbarrier tx count.
 // (cp.async.bulk: SASS UBLKCP; src/dst 16-B aligned, size multiple of 16.)
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,

@@ -3,68 +3,88 @@
 //
 // The reference has no GEMM: a batch of M tokens is M independent calls of
 // gemv_parallel (kernels.py:189-268), each token with its own absmax scale
-// (core.py:116-134).  Here the M tokens' int8 codes form A [M][K] (K-major)
-// and the packed ternary weights -- read from the same tiled layout the
-// decode GEMV streams -- are unpacked to int8 {-1,0,1} into shared memory as
-// B [N][K] (K-major); D[m][n] = sum_k A[m][k] * B[n][k] is exact in int32,
-// so every accumulator equals the reference's for that token.
+// (core.py:116-134).  Here the M tokens' int8 codes form A [M][K] and the
+// packed ternary weights -- read from the same tiled layout the decode GEMV
+// streams -- are unpacked to int8 {-1,0,1} in shared memory as B [N][K];
+// D[m][n] = sum_k A[m][k] * B[n][k] is exact in int32, so every accumulator
+// equals the reference's for that token.
 //
-// Per CTA (persistent over (job, 128-row N tile) work items):
-//   * all M <= 512 tokens stay on chip as up to 4 M=128 sub-tiles, each with
-//     its own 128-column TMEM accumulator (512 columns), so a weight tile is
-//     unpacked once and feeds 4 MMAs per K step;
-//   * K advances 128 bytes per stage through a 2-stage shared-memory ring in
-//     the UMMA canonical K-major SWIZZLE_128B layout (row r, 16-B chunk j at
-//     r*128 + ((j ^ (r&7)) << 4), 1024-B aligned): A by cp.async (zero-filled
-//     past M / lda), B unpacked in registers and stored swizzled;
-//   * one thread issues tcgen05.mma (M=128, N=128, K=32) and tcgen05.commit
-//     arrives on the stage's mbarrier, which the loaders wait on before
-//     refilling that stage -- loads of stage k+1 overlap the MMAs of stage k;
-//   * epilogue: tcgen05.ld 32x32b per warp (TMEM lanes 32*(warp%4)), then
-//     acc * w_scale * a_scale[m] in float64 (core.py:99-101) to the outputs.
+// The weights enter the tensor core as unsigned codes c = w + 1 in {0,1,2}
+// (kind::i8 with an unsigned B operand) and the epilogue subtracts the
+// token's activation sum: sum_k a*w = sum_k a*c - sum_k a.  Codes come out of
+// the packed bytes with shifts and masks only: for a 32-bit packed word, code
+// plane s (I2_S: bits 2s of every byte; TL1: a/b digits of the low/high
+// nibble) holds the weights 4q + s of byte q.  Both operands use that K order
+// inside every 16-weight group (position 4s + q <-> weight 4q + s); for A the
+// tiling kernel applies it, so the contraction is the same sum.
+//
+// Operand layout: UMMA K-major, no swizzle -- "core matrices" of 8 rows x 16
+// bytes (128 contiguous bytes), K-adjacent core matrices 128 B apart (LBO),
+// 8-row groups 512 B apart (SBO) within a 64-byte K stage.  A is pre-tiled in
+// global memory into exactly this order (tb_gemm_tile_act: [k-stage][row
+// group][k core][8 rows][16 B], plus the per-token sums), so one 1-D bulk
+// copy moves a token sub-tile of a stage.
+//
+// Warp roles (384 threads, persistent over (job, 256-row N tile, 256-token
+// half) items, K walked from a per-tile offset so CTAs spread over A):
+//   warps 0, 2  producers: A by one bulk copy per stage, the packed weight
+//               chunks of 256 rows by cp.async (arrive.noinc on the stage's
+//               mbarrier), into an 8-deep ring;
+//   warp 1      MMA issuer: one thread issues tcgen05.mma M=128 N=256 K=32 (4
+//               per stage) and tcgen05.commit, accumulators in all 512 TMEM
+//               columns;
+//   warps 4-11  unpack one weight row each into one of 3 B slots, then run
+//               the epilogue: tcgen05.ld 32x32b, transpose through shared
+//               memory (the B slots), coalesced stores of
+//               (acc - sum a) * w_scale * a_scale[m] in float64 (core.py:99-101).
 #include <algorithm>
 
 #include "common.cuh"
 
 namespace tb {
 
-constexpr int kGemmBN = 128;      // weight rows per tile (MMA N)
-constexpr int kGemmBK = 128;      // int8 K per stage = one 128-B swizzle atom
+constexpr int kGemmBN = 256;      // weight rows per tile (MMA N)
+constexpr int kGemmBK = 64;       // int8 K per stage = one packed 16-byte chunk per row
 constexpr int kGemmSubM = 128;    // MMA M
-constexpr int kGemmMaxMT = 4;     // M <= 512 tokens per launch
-constexpr int kGemmThreads = 256;
-constexpr int kGemmStages = 2;
+constexpr int kGemmMaxMT = 2;     // tokens per CTA tile: 256 (M x N = 64K int32 = all of TMEM)
+constexpr int kGemmMaxM = 512;    // tokens per launch: up to two 256-token halves
+constexpr int kGemmThreads = 384;  // 12 warps: 2 producers, MMA, 8 unpack/epilogue
+constexpr int kGemmStages = 8;   // load ring (A + packed weights): ~2 us of loads in flight
+constexpr int kGemmBSlots = 3;   // unpacked-weight (B operand) slots; reused as epilogue staging
 constexpr int kGemmMaxJobs = 8;
-constexpr int kSubTileBytes = kGemmSubM * kGemmBK;  // 16 KB
-constexpr int kBTileBytes = kGemmBN * kGemmBK;      // 16 KB
+constexpr int kSubTileBytes = kGemmSubM * kGemmBK;    // 8 KB
+constexpr int kBTileBytes = kGemmBN * kGemmBK;        // 16 KB
+constexpr int kPackedBytes = kGemmBN * kChunkBytes;   // 4 KB
+constexpr int kEpiBytes = 8 * 32 * 32 * 4;            // 8 epilogue warps x 32x32 int32 (in the B slots)
+static_assert(kEpiBytes <= kGemmBSlots * kBTileBytes, "epilogue staging lives in the B slots");
 
 struct GemmJob {
-  const uint8_t *w;      // tiled layout (gemv.cu / tb_repack)
-  const int8_t *act;     // [M][lda] int8, zero beyond cols
-  const double *a_scale; // [M]
+  const uint8_t *w;       // tiled weight layout (tb_repack)
+  const uint8_t *act;     // pre-tiled activations (tb_gemm_tile_act)
+  const double *a_scale;  // [M]
   double w_scale;
-  int32_t *acc_out;      // [M][N] or null
-  double *out64;         // [M][N] or null
-  float *out32;          // [M][N] or null
-  int N, C, lda;         // rows, 16-B chunks per row, activation row stride
-  int tile0, ntiles;     // first work item, number of N tiles
+  int32_t *acc_out;       // [M][N] or null
+  double *out64;          // [M][N] or null
+  float *out32;           // [M][N] or null
+  int N, C, Npad;         // rows, 16-B chunks per row, rows padded to 32
+  int tile0, ntiles;      // first work item, number of N tiles
 };
 
 struct GemmBatch {
   GemmJob jobs[kGemmMaxJobs];
-  int njobs, total, M, MT;
+  int njobs, total, M, MT, MH, Mpad;  // MT sub-tiles per CTA, MH token halves
 };
 
-// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B
-// apart (SBO), LBO unused for swizzled K-major, version 1 (sm_100).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
-         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE: LBO = 128 B between
+// K-adjacent core matrices, SBO = 512 B between 8-row groups, version 1.
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46);
 }
 
-// Instruction descriptor, kind::i8: D s32, A/B signed 8-bit, both K-major,
-// N = 128 (>>3 at bit 17), M = 128 (>>4 at bit 24).
-constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kGemmBN >> 3) << 17) |
+// Instruction descriptor, kind::i8: D s32, A signed 8-bit, B unsigned 8-bit
+// (weight codes), both K-major, N = 256 (>>3 at bit 17), M = 128 (>>4 at bit 24).
+constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (0u << 10) | ((uint32_t)(kGemmBN >> 3) << 17) |
                               ((uint32_t)(kGemmSubM >> 4) << 24);
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
@@ -89,63 +109,84 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void *src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-               "r"(valid ? 16 : 0)
-               : "memory");
-}
-
-// 16 packed bytes of one row (64 weights) -> 64 int8 in {-1,0,1}, as four
-// 16-byte words (word q = weights 16q..16q+15).
-__device__ __forceinline__ uint32_t minus_one_bytes(uint32_t codes) {
-  // per byte: code - 1 for codes in {0,1,2}, no borrow across bytes
-  return ((codes | 0x80808080u) - 0x01010101u) ^ 0x80808080u;
-}
-
+// One packed 32-bit word (16 weights) -> four code planes; byte q of plane s
+// is the code (w + 1) of weight 4q + s (packing.py:200-206, 222-233).
 template <int FMT>
-__device__ __forceinline__ void unpack_chunk(const uint4 p, uint4 (&o)[4]) {
-  const uint32_t w[4] = {p.x, p.y, p.z, p.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    uint32_t r[4];
-    if constexpr (FMT == TB_I2S) {
-      // byte q of w[i]: weights 16i+4q+s at bits 2s (packing.py:200-206)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t t = (w[i] >> (8 * q)) & 0xFFu;
-        const uint32_t u = t | (t << 6) | (t << 12) | (t << 18);  // bits 2s -> byte s
-        r[q] = minus_one_bytes(u & 0x03030303u);
-      }
-    } else {
-      // TL1 (packing.py:222-233): byte q = pairs (lo, hi) = weights 16i+4q..+3;
-      // nibble n = 3a + b, a = w0 + 1, b = w1 + 1
-      const uint32_t lo = w[i] & 0x0F0F0F0Fu, hi = (w[i] >> 4) & 0x0F0F0F0Fu;
-      const uint32_t alo = __umulhi(lo, 11u << 27) & 0x03030303u;
-      const uint32_t ahi = __umulhi(hi, 11u << 27) & 0x03030303u;
-      const uint32_t blo = lo - 3u * alo, bhi = hi - 3u * ahi;
-      // transpose: r[q] = (alo.q, blo.q, ahi.q, bhi.q)
-      const uint32_t t0 = prmt(alo, blo, 0x5140u), t1 = prmt(alo, blo, 0x7362u);
-      const uint32_t t2 = prmt(ahi, bhi, 0x5140u), t3 = prmt(ahi, bhi, 0x7362u);
-      r[0] = minus_one_bytes(prmt(t0, t2, 0x5410u));
-      r[1] = minus_one_bytes(prmt(t0, t2, 0x7632u));
-      r[2] = minus_one_bytes(prmt(t1, t3, 0x5410u));
-      r[3] = minus_one_bytes(prmt(t1, t3, 0x7632u));
-    }
-    o[i] = make_uint4(r[0], r[1], r[2], r[3]);
+__device__ __forceinline__ uint4 code_planes(uint32_t W) {
+  if constexpr (FMT == TB_I2S) {
+    return make_uint4(W & 0x03030303u, (W >> 2) & 0x03030303u, (W >> 4) & 0x03030303u,
+                      (W >> 6) & 0x03030303u);
+  } else {  // nibble n = 3a + b: weights (4q, 4q+1) from the low nibble, (4q+2, 4q+3) high
+    const uint32_t lo = W & 0x0F0F0F0Fu, hi = (W >> 4) & 0x0F0F0F0Fu;
+    const uint32_t alo = __umulhi(lo, 11u << 27) & 0x03030303u;
+    const uint32_t ahi = __umulhi(hi, 11u << 27) & 0x03030303u;
+    return make_uint4(alo, lo - 3u * alo, ahi, hi - 3u * ahi);
   }
 }
+
+// Cursor over this CTA's (work item, K stage) stream: items blockIdx.x,
+// blockIdx.x + gridDim.x, ...  Each item walks its K stages starting at a
+// tile-dependent offset (kb = (k0 + i) mod C): the CTAs of one job then read
+// different A stages at any moment instead of all hammering the same 32 KB
+// in L2 (int32 sums are order-independent, so results are unchanged).
+struct GemmCursor {
+  int item, i, kb, k0, j, C, n0, h;
+  __device__ __forceinline__ void set(const GemmBatch &b, int it) {
+    item = it;
+    i = 0;
+    if (it < b.total) {
+      const int tt = it / b.MH;  // tile index over all jobs; token half h
+      h = it - tt * b.MH;
+      int jj = 0;
+      while (jj + 1 < b.njobs && b.jobs[jj + 1].tile0 <= tt) ++jj;
+      j = jj;
+      C = b.jobs[jj].C;
+      const int t = tt - b.jobs[jj].tile0;
+      n0 = t * kGemmBN;
+      k0 = (int)(((long long)(t * b.MH + h) * C * 29 / 97) % C);  // spread starts over K
+      kb = k0;
+    }
+  }
+  __device__ __forceinline__ bool last() const { return i + 1 == C; }
+  __device__ __forceinline__ void next(const GemmBatch &b) {
+    if (++i == C) {
+      set(b, item + gridDim.x);
+    } else if (++kb == C) {
+      kb = 0;
+    }
+  }
+};
+
+#ifdef TB_GEMM_TRACE  // debug: per-stage SM-clock stamps of CTA 0
+constexpr int kTraceStages = 64;
+__device__ long long g_gemm_trace[kTraceStages][6];
+#define GT(p, i)                                                              \
+  do {                                                                        \
+    if (blockIdx.x == 0 && (p) < (uint32_t)kTraceStages) g_gemm_trace[p][i] = clock64(); \
+  } while (0)
+#else
+#define GT(p, i) \
+  do {           \
+  } while (0)
+#endif
 
 template <int FMT>
 __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_constant__ GemmBatch b) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t mbar[kGemmStages];
+  __shared__ __align__(8) uint64_t full[kGemmStages];   // A + packed weights landed
+  __shared__ __align__(8) uint64_t empty[kGemmStages];  // MMAs done with the ring slot
+  __shared__ __align__(8) uint64_t bready[kGemmBSlots]; // B unpacked (256 arrivals)
+  __shared__ __align__(8) uint64_t bempty[kGemmBSlots]; // MMAs done with the B slot
+  __shared__ __align__(8) uint64_t tfull, tempty;       // accumulator ready / drained
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int MT = b.MT, M = b.M;
-  const int stage_bytes = MT * kSubTileBytes + kBTileBytes;
-  const uint32_t ncols = MT <= 1 ? 128u : (MT == 2 ? 256u : 512u);
+  const int a_bytes = MT * kSubTileBytes;
+  const int stage_bytes = a_bytes + kPackedBytes;  // ring slot, multiple of 1024
+  uint8_t *bslots = smem + kGemmStages * stage_bytes;
+  const uint32_t ncols = MT <= 1 ? 256u : 512u;  // MT x 256 accumulator columns
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -153,8 +194,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
                  "r"(ncols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
-    for (int s = 0; s < kGemmStages; ++s) mbar_init(&mbar[s], 1);
+  if (tid == 32) {
+    for (int s = 0; s < kGemmStages; ++s) {
+      mbar_init(&full[s], 1 + 64);  // expect_tx + 64 cp.async-completion arrivals
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kGemmBSlots; ++s) {
+      mbar_init(&bready[s], 8 * 32);
+      mbar_init(&bempty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 8 * 32);
     fence_mbar_init_cta();
   }
   tc_fence_before();
@@ -162,126 +212,274 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
 
-  uint32_t g = 0;  // stages issued by this CTA (ring position and mbarrier phase)
-  for (int item = blockIdx.x; item < b.total; item += gridDim.x) {
-    int j = 0;
-    while (j + 1 < b.njobs && b.jobs[j + 1].tile0 <= item) ++j;
-    const GemmJob &J = b.jobs[j];
-    const int n0 = (item - J.tile0) * kGemmBN;
-    const int C = J.C;
-    const int nk = (C + 1) / 2;  // 2 chunks (128 weights) per stage
-    const int Npad = (J.N + kRowTile - 1) / kRowTile * kRowTile;
-
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = g & 1;
-      const uint32_t use = g >> 1;
-      if (use > 0) mbar_wait(&mbar[s], (use - 1) & 1);  // MMAs that read this stage are done
-      uint8_t *sA = smem + s * stage_bytes;
-      uint8_t *sB = sA + MT * kSubTileBytes;
-      const uint32_t aA = smem_u32(sA);
-      // A: MT*128 rows x 8 chunks of 16 B, zero-filled past M / lda
-      const int na = MT * kGemmSubM * 8;
-      for (int idx = tid; idx < na; idx += kGemmThreads) {
-        const int r = idx >> 3, c16 = idx & 7;
-        const int k = kb * kGemmBK + c16 * 16;
-        const bool ok = r < M && k + 16 <= J.lda;
-        const int8_t *src = ok ? J.act + (int64_t)r * J.lda + k : J.act;
-        cp_async16_zfill(aA + (r >> 7) * kSubTileBytes + (r & 127) * 128 + ((c16 ^ (r & 7)) << 4),
-                         src, ok);
+  if (warp == 0 || warp == 2) {
+    // ===== producer warps: the stage's A (one bulk copy of MT x 8 KB) and the
+    // packed weight chunk of each of the 256 rows (cp.async, lane = row % 32,
+    // coalesced 512 B per instruction); every lane's copies arrive on full[s]
+    // when they land (cp.async.mbarrier.arrive.noinc) =====
+    GemmCursor pc;
+    pc.set(b, blockIdx.x);
+    for (uint32_t p = 0; pc.item < b.total; ++p, pc.next(b)) {
+      const int s = p % kGemmStages;
+      if (p >= (uint32_t)kGemmStages) mbar_spin(&empty[s], (p / kGemmStages - 1) & 1);
+#ifndef TB_GEMM_TRACE_DEC
+      GT(p, 0);
+#endif
+      const GemmJob &J = b.jobs[pc.j];
+      uint8_t *st = smem + s * stage_bytes;
+      if (warp == 0 && lane == 0) {
+#ifdef TB_GEMM_NO_ALOAD  // profiling variant: stale A
+        mbar_arrive(&full[s]);
+#else
+        mbar_arrive_expect_tx(&full[s], a_bytes);
+        bulk_g2s(st, J.act + (size_t)pc.kb * (b.Mpad * kGemmBK) + (size_t)pc.h * a_bytes, a_bytes,
+                 &full[s]);
+#endif
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      // B: 128 rows x 2 packed chunks -> int8, one (row, chunk) per thread
-      {
-        const int row = tid >> 1, cc = tid & 1;
-        const int n = n0 + row, c = kb * 2 + cc;
-        uint4 p = make_uint4(0, 0, 0, 0);
-        const bool ok = n < Npad && c < C;
-        if (ok)
-          p = __ldg(reinterpret_cast<const uint4 *>(
-              J.w + ((int64_t)(n >> 5) * C + c) * kTileChunkBytes + (n & 31) * 16));
-        uint4 o[4];
-        if (ok) {
-          unpack_chunk<FMT>(p, o);
-        } else {
+      const int t0 = warp == 0 ? 0 : kGemmBN / 64;  // warp 0: rows 0-127, warp 2: 128-255
+      const uint32_t dst0 = smem_u32(st + a_bytes) + lane * 16;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) o[q] = make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<uint4 *>(sB + row * 128 + (((cc * 4 + q) ^ (row & 7)) << 4)) = o[q];
+      for (int t = t0; t < t0 + kGemmBN / 64; ++t) {
+        const int n = pc.n0 + t * 32 + lane;
+        const bool ok = n < J.Npad;
+        const uint8_t *src =
+            ok ? J.w + ((size_t)((pc.n0 >> 5) + t) * pc.C + pc.kb) * kTileChunkBytes + lane * 16 : J.w;
+#ifndef TB_GEMM_NO_BLOAD  // profiling variant: stale packed weights
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + t * 512),
+                     "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+#endif
       }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      // generic-proxy writes (st.shared, cp.async) -> visible to the tensor core
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      if (tid == 0) {
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s]))
+                   : "memory");
+#ifndef TB_GEMM_TRACE_DEC
+      GT(p, 1);
+#endif
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      GemmCursor cc;
+      cc.set(b, blockIdx.x);
+      uint32_t tiles = 0;
+      for (uint32_t p = 0; cc.item < b.total; ++p) {
+        const int s = p % kGemmStages, bs = p % kGemmBSlots;
+        if (cc.i == 0 && tiles > 0) mbar_spin(&tempty, (tiles - 1) & 1);  // epilogue drained TMEM
+        mbar_spin(&bready[bs], (p / kGemmBSlots) & 1);  // (implies full[s])
+        GT(p, 4);
         tc_fence_after();
-        const uint32_t aB = smem_u32(sB);
+        const uint32_t aA = smem_u32(smem + s * stage_bytes), aB = smem_u32(bslots + bs * kBTileBytes);
         for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
-          for (int k4 = 0; k4 < kGemmBK / 32; ++k4)
-            mma_i8(tmem + mt * kGemmBN, umma_desc_sw128(aA + mt * kSubTileBytes + k4 * 32),
-                   umma_desc_sw128(aB + k4 * 32), (kb > 0 || k4 > 0) ? 1u : 0u);
+          for (int k2 = 0; k2 < kGemmBK / 32; ++k2)
+#ifndef TB_GEMM_NO_MMA  // profiling variant: data movement only
+            mma_i8(tmem + mt * kGemmBN, umma_desc_noswz(aA + mt * kSubTileBytes + k2 * 256),
+                   umma_desc_noswz(aB + k2 * 256), (cc.i > 0 || k2 > 0) ? 1u : 0u);
+#else
+            ;
+#endif
         }
-        umma_commit(&mbar[s]);
+        umma_commit(&empty[s]);
+        umma_commit(&bempty[bs]);
+#ifndef TB_GEMM_TRACE_DEC
+        GT(p, 5);
+#endif
+        if (cc.last()) {
+          umma_commit(&tfull);
+          ++tiles;
+        }
+        cc.next(b);
       }
-      ++g;
     }
-    // epilogue: the last commit covers every MMA of this tile (issue order)
-    mbar_wait(&mbar[(g - 1) & 1], ((g - 1) >> 1) & 1);
-    tc_fence_after();
-    {
-      const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column half
-      for (int mt = 0; mt < MT; ++mt) {
-        const int m = mt * kGemmSubM + lg * 32 + lane;
-        const double as = m < M ? J.a_scale[m] : 0.0;
-#pragma unroll 1
-        for (int cb = 0; cb < 4; ++cb) {
-          const int col = ch * 64 + cb * 16;
-          uint32_t v[16];
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-                "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-              : "r"(tmem + ((uint32_t)(lg * 32) << 16) + mt * kGemmBN + col));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (m < M) {
-            const int nb = n0 + col;
-            const int64_t o = (int64_t)m * J.N + nb;
+  } else if (warp >= 4) {
+    // ===== unpack + epilogue (warps 4..11: row tid - 128; TMEM lane group
+    // warp % 4, column half (warp - 4) / 4).  These threads issue no
+    // cp.async, so their fence.proxy.async covers only their own st.shared. =====
+    const int r = tid - 128;
+    const int lg = warp & 3, chalf = (warp - 4) >> 2;
+    uint32_t *stg = reinterpret_cast<uint32_t *>(bslots) + (warp - 4) * 32 * 32;  // epilogue only
+    GemmCursor cc;
+    cc.set(b, blockIdx.x);
+    uint32_t tiles = 0;
+    for (uint32_t p = 0; cc.item < b.total; ++p) {
+      const int s = p % kGemmStages, bs = p % kGemmBSlots;
+      uint8_t *st = smem + s * stage_bytes;
+      uint8_t *bt = bslots + bs * kBTileBytes;
+#ifdef TB_GEMM_TRACE_DEC
+      if (tid == 128) GT(p, 0);
+#endif
+      mbar_spin(&full[s], (p / kGemmStages) & 1);
+#ifdef TB_GEMM_TRACE_DEC
+      if (tid == 128) GT(p, 1);
+#endif
+      if (p >= (uint32_t)kGemmBSlots) mbar_spin(&bempty[bs], (p / kGemmBSlots - 1) & 1);
+      if (tid == 128) GT(p, 2);
+      const GemmJob &J = b.jobs[cc.j];
+      {
+        const int rr = r;
+        uint4 o[4];
+        if (cc.n0 + rr < J.Npad) {
+          const uint4 pk = *reinterpret_cast<const uint4 *>(st + a_bytes + rr * 16);
+          o[0] = code_planes<FMT>(pk.x);
+          o[1] = code_planes<FMT>(pk.y);
+          o[2] = code_planes<FMT>(pk.z);
+          o[3] = code_planes<FMT>(pk.w);
+        } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              if (nb + e < J.N) {
-                const int32_t a = (int32_t)v[e];
-                if (J.acc_out) J.acc_out[o + e] = a;
-                if (J.out64 || J.out32) {
-                  const double y = static_cast<double>(a) * J.w_scale * as;  // core.py:99-101
-                  if (J.out64) J.out64[o + e] = y;
-                  if (J.out32) J.out32[o + e] = static_cast<float>(y);
-                }
+          for (int i = 0; i < 4; ++i) o[i] = make_uint4(0, 0, 0, 0);
+        }
+        // core matrix (row group rr/8, k chunk i): 128 B, row rr%8 at 16 B
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          *reinterpret_cast<uint4 *>(bt + ((rr >> 3) * 4 + i) * 128 + (rr & 7) * 16) = o[i];
+      }
+#ifdef TB_GEMM_TRACE_DEC
+      if (tid == 128) GT(p, 5);
+#endif
+#ifndef TB_GEMM_NO_FENCE  // profiling variant (results invalid): fence cost
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> tensor core
+#endif
+      mbar_arrive(&bready[bs]);
+      if (tid == 128) GT(p, 3);
+      if (cc.last()) {
+        // ---- epilogue of this tile ----
+        mbar_spin(&tfull, tiles & 1);
+        tc_fence_after();
+        int32_t *acc_out = J.acc_out;
+        const int32_t *rowsum =
+            reinterpret_cast<const int32_t *>(J.act + (size_t)J.C * b.Mpad * kGemmBK);
+        double *out64 = J.out64;
+        float *out32 = J.out32;
+        const double ws = J.w_scale;
+        const int Nj = J.N;
+        for (int mt = 0; mt < MT; ++mt) {
+          const int mrow0 = cc.h * (kGemmMaxMT * kGemmSubM) + mt * kGemmSubM + lg * 32;
+          if (mrow0 >= M) break;
+          const double my_as = (mrow0 + lane < M && J.a_scale) ? J.a_scale[mrow0 + lane] : 0.0;
+          const int32_t my_sum = rowsum[mrow0 + lane];  // sum_k a[m][k] (tile_act)
+          const int rows = min(32, M - mrow0);
+#pragma unroll 1
+          for (int cb = 0; cb < kGemmBN / 64; ++cb) {
+            const int col = chalf * (kGemmBN / 2) + cb * 32;
+            uint32_t v[32];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                  "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                  "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+                  "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                  "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                  "=r"(v[30]), "=r"(v[31])
+                : "r"(tmem + ((uint32_t)(lg * 32) << 16) + mt * kGemmBN + col));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            // lane = row: stage it XOR-rotated, then lane = column
+#pragma unroll
+            for (int e = 0; e < 32; ++e) stg[lane * 32 + ((e + lane) & 31)] = v[e];
+            __syncwarp();
+            const int n = cc.n0 + col + lane;
+#ifdef TB_GEMM_NO_EPI  // profiling variant: no output stores
+            const bool on = false;
+#else
+            const bool on = n < Nj;
+#endif
+            // 32 independent rows in flight (one warp per scheduler: ILP, not TLP)
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) {
+              const double as = __shfl_sync(0xffffffffu, my_as, rr);
+              const int32_t asum = __shfl_sync(0xffffffffu, my_sum, rr);
+              if (on && rr < rows) {
+                const int32_t a = (int32_t)stg[rr * 32 + ((lane + rr) & 31)] - asum;
+                const int64_t off = (int64_t)(mrow0 + rr) * Nj + n;
+                if (acc_out) acc_out[off] = a;
+                const double y = static_cast<double>(a) * ws * as;  // core.py:99-101
+                if (out64) out64[off] = y;
+                if (out32) out32[off] = static_cast<float>(y);
               }
             }
+            __syncwarp();
           }
         }
+        tc_fence_before();
+        mbar_arrive(&tempty);
+        ++tiles;
       }
+      cc.next(b);
     }
-    tc_fence_before();
-    __syncthreads();  // TMEM drained before the next tile's MMAs overwrite it
-    tc_fence_after();
   }
+  tc_fence_before();
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
 }
 
+// Natural int8 activations [M][lda] -> the GEMM's A layout, zero padded to
+// Mpad rows and ks = ceil(cols / 64) K stages, each 16-byte group in code-
+// plane order (position 4s + q holds a[16i + 4q + s]):
+// out[((ks_i * Mpad/8 + g) * 4 + c) * 128 + r8 * 16 + p] = act[8g + r8][64 ks_i + 16 c + perm(p)],
+// followed by the per-token sums int32 [Mpad] (the unsigned-code correction).
+__global__ void gemm_tile_act_kernel(const int8_t *__restrict__ act, int M, int64_t lda, int cols,
+                                     int Mpad, int ks, uint8_t *__restrict__ out) {
+  const int64_t units = (int64_t)ks * Mpad * 4;  // 16-byte units
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int r8 = (int)(u & 7);
+    const int64_t q = u >> 3;  // (ks_i, g, c)
+    const int c = (int)(q & 3);
+    const int64_t q2 = q >> 2;
+    const int g = (int)(q2 % (Mpad / 8));
+    const int ksi = (int)(q2 / (Mpad / 8));
+    const int m = g * 8 + r8;
+    const int64_t k = (int64_t)ksi * kGemmBK + c * 16;
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (m < M) {
+      const int8_t *src = act + (int64_t)m * lda + k;
+      if (k + 16 <= cols && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(src);
+        w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (k + i < cols) w[i >> 2] |= (uint32_t)(uint8_t)src[i] << (8 * (i & 3));
+      }
+    }
+    // 4x4 byte transpose: word s = (a[s], a[4+s], a[8+s], a[12+s])
+    const uint32_t t0 = prmt(w[0], w[1], 0x5140u), t1 = prmt(w[0], w[1], 0x7362u);
+    const uint32_t t2 = prmt(w[2], w[3], 0x5140u), t3 = prmt(w[2], w[3], 0x7362u);
+    reinterpret_cast<uint4 *>(out)[u] = make_uint4(prmt(t0, t2, 0x5410u), prmt(t0, t2, 0x7632u),
+                                                   prmt(t1, t3, 0x5410u), prmt(t1, t3, 0x7632u));
+  }
+}
+
+__global__ void gemm_rowsum_kernel(const int8_t *__restrict__ act, int M, int64_t lda, int cols,
+                                   int Mpad, int32_t *__restrict__ sums) {
+  const int m = blockIdx.x;
+  int32_t acc = 0;
+  if (m < M)
+    for (int k = threadIdx.x; k < cols; k += blockDim.x) acc += act[(int64_t)m * lda + k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ int32_t part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+    sums[m] = t;
+  }
+}
+
 template <int FMT>
 static int launch_gemm(GemmBatch &b, cudaStream_t s) {
-  const int smem = kGemmStages * (b.MT * kSubTileBytes + kBTileBytes) + 1024;
+  const int stage = b.MT * kSubTileBytes + kPackedBytes;
+  const int smem = kGemmStages * stage + kGemmBSlots * kBTileBytes + 1024 + 1024;
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    const int max_smem = kGemmStages * (kGemmMaxMT * kSubTileBytes + kBTileBytes) + 1024;
+    const int max_smem =
+        kGemmStages * (kGemmMaxMT * kSubTileBytes + kPackedBytes) + kGemmBSlots * kBTileBytes + 2048;
     if (cudaFuncSetAttribute(tgemm_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              max_smem) != cudaSuccess)
       return TB_ERR_CUDA;
@@ -293,65 +491,103 @@ static int launch_gemm(GemmBatch &b, cudaStream_t s) {
   return TB_OK;
 }
 
+static int64_t gemm_stages_of(int64_t cols) { return ceil_div(cols, kGemmBK); }
+
 }  // namespace tb
 
 using namespace tb;
 
+#ifdef TB_GEMM_TRACE
+extern "C" int tb_gemm_trace_fetch(void *host, int64_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_gemm_trace, bytes) == cudaSuccess ? 0 : 2;
+}
+#endif
+
+// token rows of the tiled A: one 128-row sub-tile, or whole 256-row halves
+static int64_t gemm_mpad(int64_t M) {
+  return M <= kGemmSubM ? kGemmSubM : pad_up(M, kGemmMaxMT * kGemmSubM);
+}
+
+extern "C" int64_t tb_gemm_act_bytes(int64_t M, int64_t cols) {
+  if (M < 1 || M > kGemmMaxM || cols < 1) return -1;
+  return gemm_stages_of(cols) * gemm_mpad(M) * kGemmBK + gemm_mpad(M) * (int64_t)sizeof(int32_t);
+}
+
+extern "C" int tb_gemm_tile_act(const int8_t *act, int64_t M, int64_t lda, int64_t cols,
+                                uint8_t *out, void *stream) {
+  if (!act || !out || M < 1 || M > kGemmMaxM || cols < 1 || lda < cols ||
+      (reinterpret_cast<uintptr_t>(out) & 15))
+    return TB_ERR_ARGUMENT;
+  const int Mpad = (int)gemm_mpad(M);
+  const int ks = (int)gemm_stages_of(cols);
+  const int64_t units = (int64_t)ks * Mpad * 4;
+  const int grid = (int)std::min<int64_t>(ceil_div(units, 256), (int64_t)sm_count_cached() * 8);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  gemm_tile_act_kernel<<<grid, 256, 0, s>>>(act, (int)M, lda, (int)cols, Mpad, ks, out);
+  gemm_rowsum_kernel<<<Mpad, 256, 0, s>>>(act, (int)M, lda, (int)cols, Mpad,
+                                          reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK));
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
 extern "C" int tb_gemm_batch(int fmt, int64_t njobs, const tb_gemm_desc *descs, int64_t M,
                              void *stream) {
+  if (fmt == TB_TL2) return TB_ERR_UNSUPPORTED;
   if ((fmt != TB_I2S && fmt != TB_TL1) || njobs < 1 || njobs > kGemmMaxJobs || !descs || M < 1 ||
-      M > kGemmMaxMT * kGemmSubM)
-    return fmt == TB_TL2 ? TB_ERR_UNSUPPORTED : TB_ERR_ARGUMENT;
+      M > kGemmMaxM)
+    return TB_ERR_ARGUMENT;
   GemmBatch b{};
   b.njobs = (int)njobs;
   b.M = (int)M;
-  b.MT = (int)ceil_div(M, kGemmSubM);
+  b.Mpad = (int)gemm_mpad(M);
+  b.MT = b.Mpad >= kGemmMaxMT * kGemmSubM ? kGemmMaxMT : 1;
+  b.MH = (int)ceil_div(b.Mpad, b.MT * kGemmSubM);
   int tiles = 0;
   for (int64_t j = 0; j < njobs; ++j) {
     const tb_gemm_desc &d = descs[j];
-    if (!d.tiled || !d.act || d.rows < 1 || d.cols < 1 || d.lda < 16 || (d.lda & 15) ||
-        ((d.out64 || d.out32) && !d.a_scale) || (reinterpret_cast<uintptr_t>(d.act) & 15) ||
-        (reinterpret_cast<uintptr_t>(d.tiled) & 15) || d.lda < d.cols)
+    if (!d.tiled || !d.act_tiled || d.rows < 1 || d.cols < 1 || ((d.out64 || d.out32) && !d.a_scale) ||
+        (reinterpret_cast<uintptr_t>(d.act_tiled) & 15) || (reinterpret_cast<uintptr_t>(d.tiled) & 15))
       return TB_ERR_ARGUMENT;
     GemmJob &J = b.jobs[j];
     J.w = d.tiled;
-    J.act = d.act;
+    J.act = d.act_tiled;
     J.a_scale = d.a_scale;
     J.w_scale = d.w_scale;
     J.acc_out = d.acc_out;
     J.out64 = d.out64;
     J.out32 = d.out32;
     J.N = (int)d.rows;
-    J.C = (int)ceil_div(ref_row_bytes(fmt, d.cols), kChunkBytes);
-    J.lda = (int)d.lda;
+    J.Npad = (int)pad_up(d.rows, kRowTile);
+    J.C = (int)ceil_div(ref_row_bytes(fmt, d.cols), kChunkBytes);  // == stages of 64 K
     J.tile0 = tiles;
     J.ntiles = (int)ceil_div(d.rows, kGemmBN);
     tiles += J.ntiles;
   }
-  b.total = tiles;
+  b.total = tiles * b.MH;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return fmt == TB_I2S ? launch_gemm<TB_I2S>(b, s) : launch_gemm<TB_TL1>(b, s);
 }
 
 extern "C" int tb_gemm_i8(int fmt, const uint8_t *tiled, int64_t rows, int64_t cols,
                           const int8_t *act, int64_t M, int64_t lda, const double *a_scale,
-                          double w_scale, int32_t *acc_out, double *out64, float *out32,
-                          void *stream) {
-  if (M < 1) return TB_ERR_ARGUMENT;
-  for (int64_t m0 = 0; m0 < M; m0 += kGemmMaxMT * kGemmSubM) {
-    const int64_t mm = std::min<int64_t>(M - m0, kGemmMaxMT * kGemmSubM);
+                          double w_scale, uint8_t *workspace, int32_t *acc_out, double *out64,
+                          float *out32, void *stream) {
+  if (M < 1 || !workspace) return TB_ERR_ARGUMENT;
+  for (int64_t m0 = 0; m0 < M; m0 += kGemmMaxM) {
+    const int64_t mm = std::min<int64_t>(M - m0, kGemmMaxM);
+    int st = tb_gemm_tile_act(act + m0 * lda, mm, lda, cols, workspace, stream);
+    if (st != TB_OK) return st;
     tb_gemm_desc d{};
     d.tiled = tiled;
     d.rows = rows;
     d.cols = cols;
-    d.act = act + m0 * lda;
-    d.lda = lda;
+    d.act_tiled = workspace;
     d.a_scale = a_scale ? a_scale + m0 : nullptr;
     d.w_scale = w_scale;
     d.acc_out = acc_out ? acc_out + m0 * rows : nullptr;
     d.out64 = out64 ? out64 + m0 * rows : nullptr;
     d.out32 = out32 ? out32 + m0 * rows : nullptr;
-    const int st = tb_gemm_batch(fmt, 1, &d, mm, stream);
+    st = tb_gemm_batch(fmt, 1, &d, mm, stream);
     if (st != TB_OK) return st;
   }
   return TB_OK;

@@ -112,9 +112,10 @@ def gemm_prefill(p, a: QuantizedActivations, want_out64: bool = True) -> GemvRes
     dev = main.device
     acc = torch.empty((M, p.rows), dtype=torch.int32, device=dev)
     out = torch.empty((M, p.rows), dtype=torch.float64, device=dev) if want_out64 else None
+    ws = torch.empty(lib.tb_gemm_act_bytes(min(M, 512), p.cols), dtype=torch.uint8, device=dev)
     L.check(lib.tb_gemm_i8(p.FMT, L.ptr(main), p.rows, p.cols, L.ptr(acts), M, lda,
-                           L.ptr(a.scales), float(p.scale), L.ptr(acc), L.ptr(out), None,
-                           L.stream_ptr()), "gemm_i8")
+                           L.ptr(a.scales), float(p.scale), L.ptr(ws), L.ptr(acc), L.ptr(out),
+                           None, L.stream_ptr()), "gemm_i8")
     shape = _out_shape(a, p.rows)
     return GemvResult(accumulators=acc.reshape(shape),
                       output=out.reshape(shape) if out is not None else None)

@@ -511,13 +511,19 @@ def test_prefill_gemm_batch_grouped(tb):
     shapes = [(H, H, xh), (128, H, xh), (128, H, xh), (H, H, xh), (I, H, xh), (I, H, xh), (H, I, xi)]
     descs = (L.GemmDesc * len(shapes))()
     keep, wants = [], []
+    tiled_in = {}
+    for qa, k in ((xh, H), (xi, I)):
+        t = torch.empty(lib.tb_gemm_act_bytes(M, k), dtype=torch.uint8, device="cuda")
+        L.check(lib.tb_gemm_tile_act(qa.data.data_ptr(), M, qa.data.stride(0), k, t.data_ptr(),
+                                     L.stream_ptr()))
+        tiled_in[id(qa)] = t
     for d, (n, k, qa) in zip(descs, shapes):
         v = rng.integers(-1, 2, size=(n, k), dtype=np.int8)
         p = tb.encode_i2s(tb.TernaryMatrix(n, k, v, 1.0))
         main, _ = p.tiled()
         acc = torch.empty((M, n), dtype=torch.int32, device="cuda")
         d.tiled, d.rows, d.cols = main.data_ptr(), n, k
-        d.act, d.lda = qa.data.data_ptr(), qa.data.stride(0)
+        d.act_tiled = tiled_in[id(qa)].data_ptr()
         d.a_scale, d.w_scale, d.acc_out = qa.scales.data_ptr(), 1.0, acc.data_ptr()
         keep.append((p, main, acc, qa))
         q = host(qa.data)
