@@ -37,7 +37,12 @@
 //               the epilogue: tcgen05.ld 32x32b, transpose through shared
 //               memory (the B slots), coalesced stores of
 //               (acc - sum a) * w_scale * a_scale[m] in float64 (core.py:99-101).
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -48,9 +53,10 @@ constexpr int kGemmBK = 64;       // int8 K per stage = one packed 16-byte chunk
 constexpr int kGemmSubM = 128;    // MMA M
 constexpr int kGemmMaxMT = 2;     // tokens per CTA tile: 256 (M x N = 64K int32 = all of TMEM)
 constexpr int kGemmMaxM = 512;    // tokens per launch: up to two 256-token halves
-constexpr int kGemmThreads = 384;  // 12 warps: 2 producers, MMA, 8 unpack/epilogue
+constexpr int kGemmThreads = 384;  // 12 warps: producer, MMA, (2 idle), 8 unpack/epilogue
 constexpr int kGemmStages = 8;   // load ring (A + packed weights): ~2 us of loads in flight
-constexpr int kGemmBSlots = 3;   // unpacked-weight (B operand) slots; reused as epilogue staging
+constexpr int kGemmBSlots = 3;
+constexpr int kGemmCluster = 2;  // CTA pair sharing every A stage (TMA multicast)   // unpacked-weight (B operand) slots; reused as epilogue staging
 constexpr int kGemmMaxJobs = 8;
 constexpr int kSubTileBytes = kGemmSubM * kGemmBK;    // 8 KB
 constexpr int kBTileBytes = kGemmBN * kGemmBK;        // 16 KB
@@ -58,7 +64,8 @@ constexpr int kPackedBytes = kGemmBN * kChunkBytes;   // 4 KB
 constexpr int kEpiBytes = 8 * 32 * 32 * 4;            // 8 epilogue warps x 32x32 int32 (in the B slots)
 static_assert(kEpiBytes <= kGemmBSlots * kBTileBytes, "epilogue staging lives in the B slots");
 
-struct GemmJob {
+struct alignas(64) GemmJob {
+  CUtensorMap bmap;       // the tiled weights as [T][C][512 B] (3-D, 8-byte elements)
   const uint8_t *w;       // tiled weight layout (tb_repack)
   const uint8_t *act;     // pre-tiled activations (tb_gemm_tile_act)
   const double *a_scale;  // [M]
@@ -70,9 +77,15 @@ struct GemmJob {
   int tile0, ntiles;      // first work item, number of N tiles
 };
 
+constexpr int kGemmMaxSched = 320;  // statically scheduled pair items per launch
+constexpr int kGemmMaxPairs = 80;   // >= 148 SMs / 2
+
 struct GemmBatch {
   GemmJob jobs[kGemmMaxJobs];
   int njobs, total, M, MT, MH, Mpad;  // MT sub-tiles per CTA, MH token halves
+  int scheduled;                      // 1: pair p runs sched[sched_off[p] .. sched_off[p+1])
+  uint16_t sched_off[kGemmMaxPairs + 1];
+  uint16_t sched[kGemmMaxSched];
 };
 
 // UMMA shared-memory descriptor, K-major, SWIZZLE_NONE: LBO = 128 B between
@@ -129,20 +142,32 @@ __device__ __forceinline__ uint4 code_planes(uint32_t W) {
 // tile-dependent offset (kb = (k0 + i) mod C): the CTAs of one job then read
 // different A stages at any moment instead of all hammering the same 32 KB
 // in L2 (int32 sums are order-independent, so results are unchanged).
+// A work item is (job, pair of N tiles, token half) for one CTA pair; this
+// CTA takes tile 2 * pair + rank.
 struct GemmCursor {
   int item, i, kb, k0, j, C, n0, h;
+  int q;  // position in this pair's schedule (scheduled mode)
+  __device__ __forceinline__ void start(const GemmBatch &b) {
+    const int pair = blockIdx.x / kGemmCluster;
+    if (b.scheduled) {
+      q = b.sched_off[pair];
+      set(b, q < b.sched_off[pair + 1] ? b.sched[q] : b.total);
+    } else {
+      set(b, pair);
+    }
+  }
   __device__ __forceinline__ void set(const GemmBatch &b, int it) {
     item = it;
     i = 0;
     if (it < b.total) {
-      const int tt = it / b.MH;  // tile index over all jobs; token half h
+      const int tt = it / b.MH;  // tile pair over all jobs; token half h
       h = it - tt * b.MH;
       int jj = 0;
       while (jj + 1 < b.njobs && b.jobs[jj + 1].tile0 <= tt) ++jj;
       j = jj;
       C = b.jobs[jj].C;
       const int t = tt - b.jobs[jj].tile0;
-      n0 = t * kGemmBN;
+      n0 = (t * kGemmCluster + (int)(blockIdx.x % kGemmCluster)) * kGemmBN;
       k0 = (int)(((long long)(t * b.MH + h) * C * 29 / 97) % C);  // spread starts over K
       kb = k0;
     }
@@ -150,12 +175,21 @@ struct GemmCursor {
   __device__ __forceinline__ bool last() const { return i + 1 == C; }
   __device__ __forceinline__ void next(const GemmBatch &b) {
     if (++i == C) {
-      set(b, item + gridDim.x);
+      if (b.scheduled) {
+        ++q;
+        set(b, q < b.sched_off[blockIdx.x / kGemmCluster + 1] ? b.sched[q] : b.total);
+      } else {
+        set(b, item + gridDim.x / kGemmCluster);
+      }
     } else if (++kb == C) {
       kb = 0;
     }
   }
 };
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 #ifdef TB_GEMM_TRACE  // debug: per-stage SM-clock stamps of CTA 0
 constexpr int kTraceStages = 64;
@@ -196,8 +230,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
   }
   if (tid == 32) {
     for (int s = 0; s < kGemmStages; ++s) {
-      mbar_init(&full[s], 1 + 64);  // expect_tx + 64 cp.async-completion arrivals
-      mbar_init(&empty[s], 1);
+      mbar_init(&full[s], 1);  // expect_tx (A halves from both CTAs + the weights)
+      mbar_init(&empty[s], kGemmCluster);  // both CTAs' MMAs done with the slot
     }
     for (int s = 0; s < kGemmBSlots; ++s) {
       mbar_init(&bready[s], 8 * 32);
@@ -205,63 +239,51 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
     }
     mbar_init(&tfull, 1);
     mbar_init(&tempty, 8 * 32);
-    fence_mbar_init_cta();
+    fence_mbar_init();  // release.cluster: the peer multicasts onto these barriers
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  const uint32_t crank = blockIdx.x % kGemmCluster;
 
-  if (warp == 0 || warp == 2) {
-    // ===== producer warps: the stage's A (one bulk copy of MT x 8 KB) and the
-    // packed weight chunk of each of the 256 rows (cp.async, lane = row % 32,
-    // coalesced 512 B per instruction); every lane's copies arrive on full[s]
-    // when they land (cp.async.mbarrier.arrive.noinc) =====
-    GemmCursor pc;
-    pc.set(b, blockIdx.x);
-    for (uint32_t p = 0; pc.item < b.total; ++p, pc.next(b)) {
-      const int s = p % kGemmStages;
-      if (p >= (uint32_t)kGemmStages) mbar_spin(&empty[s], (p / kGemmStages - 1) & 1);
-#ifndef TB_GEMM_TRACE_DEC
-      GT(p, 0);
-#endif
-      const GemmJob &J = b.jobs[pc.j];
-      uint8_t *st = smem + s * stage_bytes;
-      if (warp == 0 && lane == 0) {
-#ifdef TB_GEMM_NO_ALOAD  // profiling variant: stale A
-        mbar_arrive(&full[s]);
-#else
-        mbar_arrive_expect_tx(&full[s], a_bytes);
-        bulk_g2s(st, J.act + (size_t)pc.kb * (b.Mpad * kGemmBK) + (size_t)pc.h * a_bytes, a_bytes,
-                 &full[s]);
-#endif
-      }
-      const int t0 = warp == 0 ? 0 : kGemmBN / 64;  // warp 0: rows 0-127, warp 2: 128-255
-      const uint32_t dst0 = smem_u32(st + a_bytes) + lane * 16;
-#pragma unroll
-      for (int t = t0; t < t0 + kGemmBN / 64; ++t) {
-        const int n = pc.n0 + t * 32 + lane;
-        const bool ok = n < J.Npad;
+  if (warp == 0) {
+    // ===== producer: per stage one multicast bulk copy of this CTA's half of
+    // A (lands in both CTAs of the pair) and one 3-D tensor copy of the
+    // stage's packed weights (8 row-tiles x 512 B, zero-filled past the end) =====
+    if (lane == 0) {
+      GemmCursor pc;
+      pc.start(b);
+      for (uint32_t p = 0; pc.item < b.total; ++p, pc.next(b)) {
+        const int s = p % kGemmStages;
+        if (p >= (uint32_t)kGemmStages) mbar_spin(&empty[s], (p / kGemmStages - 1) & 1);
+        GT(p, 0);
+        const GemmJob &J = b.jobs[pc.j];
+        uint8_t *st = smem + s * stage_bytes;
+        mbar_arrive_expect_tx(&full[s], a_bytes + kPackedBytes);
+        const uint32_t half = a_bytes / kGemmCluster;
         const uint8_t *src =
-            ok ? J.w + ((size_t)((pc.n0 >> 5) + t) * pc.C + pc.kb) * kTileChunkBytes + lane * 16 : J.w;
-#ifndef TB_GEMM_NO_BLOAD  // profiling variant: stale packed weights
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + t * 512),
-                     "l"(src), "r"(ok ? 16 : 0)
-                     : "memory");
-#endif
+            J.act + (size_t)pc.kb * (b.Mpad * kGemmBK) + (size_t)pc.h * a_bytes + crank * half;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+            " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(st) + crank * half),
+            "l"(src), "r"(half), "r"(smem_u32(&full[s])), "h"((uint16_t)((1u << kGemmCluster) - 1))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(st + a_bytes)),
+            "l"(reinterpret_cast<uint64_t>(&J.bmap)), "r"(0), "r"(pc.kb), "r"(pc.n0 >> 5),
+            "r"(smem_u32(&full[s]))
+            : "memory");
+        GT(p, 1);
       }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s]))
-                   : "memory");
-#ifndef TB_GEMM_TRACE_DEC
-      GT(p, 1);
-#endif
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == 1) {
     // ===== MMA issuer =====
     if (lane == 0) {
       GemmCursor cc;
-      cc.set(b, blockIdx.x);
+      cc.start(b);
       uint32_t tiles = 0;
       for (uint32_t p = 0; cc.item < b.total; ++p) {
         const int s = p % kGemmStages, bs = p % kGemmBSlots;
@@ -280,7 +302,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
             ;
 #endif
         }
-        umma_commit(&empty[s]);
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+            " [%0], %1;" ::"r"(smem_u32(&empty[s])), "h"((uint16_t)((1u << kGemmCluster) - 1))
+            : "memory");
         umma_commit(&bempty[bs]);
 #ifndef TB_GEMM_TRACE_DEC
         GT(p, 5);
@@ -300,7 +325,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
     const int lg = warp & 3, chalf = (warp - 4) >> 2;
     uint32_t *stg = reinterpret_cast<uint32_t *>(bslots) + (warp - 4) * 32 * 32;  // epilogue only
     GemmCursor cc;
-    cc.set(b, blockIdx.x);
+    cc.start(b);
     uint32_t tiles = 0;
     for (uint32_t p = 0; cc.item < b.total; ++p) {
       const int s = p % kGemmStages, bs = p % kGemmBSlots;
@@ -410,6 +435,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // the peer no longer writes our shared memory / barriers
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
 }
@@ -470,6 +496,33 @@ __global__ void gemm_rowsum_kernel(const int8_t *__restrict__ act, int M, int64_
   }
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Tiled weights [T][C][32 rows x 16 B] as a 3-D tensor of 8-byte elements
+// {64, C, T}; a box {64, 1, 8} is one K stage of 256 rows.
+static bool encode_weight_map(CUtensorMap *map, const uint8_t *w, int C, int T) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {kTileChunkBytes / 8, (cuuint64_t)C, (cuuint64_t)T};
+  const cuuint64_t strides[2] = {kTileChunkBytes, (cuuint64_t)C * kTileChunkBytes};
+  const cuuint32_t box[3] = {kTileChunkBytes / 8, 1, kGemmBN / kRowTile};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint8_t *>(w), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int FMT>
 static int launch_gemm(GemmBatch &b, cudaStream_t s) {
   const int stage = b.MT * kSubTileBytes + kPackedBytes;
@@ -485,9 +538,51 @@ static int launch_gemm(GemmBatch &b, cudaStream_t s) {
       return TB_ERR_CUDA;
     configured_dev = dev;
   }
-  const int grid = std::max(1, std::min(b.total, sm_count_cached()));
-  tgemm_kernel<FMT><<<grid, kGemmThreads, smem, s>>>(b);
-  TB_CHECK_LAUNCH();
+  const int pairs = std::max(1, std::min(b.total, sm_count_cached() / kGemmCluster));
+  // Longest-processing-time-first static schedule: items (cost = K stages)
+  // go to the least-loaded pair, largest first -- a 224-stage down-projection
+  // tile no longer lands on a pair that already has two 64-stage tiles.
+  b.scheduled = 0;
+  if (b.total <= kGemmMaxSched && pairs <= kGemmMaxPairs) {
+    std::vector<std::pair<int, int>> items;  // (cost, item)
+    for (int it = 0; it < b.total; ++it) {
+      const int tt = it / b.MH;
+      int jj = 0;
+      while (jj + 1 < b.njobs && b.jobs[jj + 1].tile0 <= tt) ++jj;
+      items.push_back({b.jobs[jj].C, it});
+    }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const std::pair<int, int> &x, const std::pair<int, int> &y) { return x.first > y.first; });
+    std::vector<long long> load(pairs, 0);
+    std::vector<std::vector<int>> lists(pairs);
+    for (const auto &ci : items) {
+      int best = 0;
+      for (int q = 1; q < pairs; ++q)
+        if (load[q] < load[best]) best = q;
+      load[best] += ci.first + 8;  // + a per-tile epilogue allowance
+      lists[best].push_back(ci.second);
+    }
+    int off = 0;
+    for (int q = 0; q < pairs; ++q) {
+      b.sched_off[q] = (uint16_t)off;
+      for (int it : lists[q]) b.sched[off++] = (uint16_t)it;
+    }
+    b.sched_off[pairs] = (uint16_t)off;
+    b.scheduled = 1;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pairs * kGemmCluster);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kGemmCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, tgemm_kernel<FMT>, b) != cudaSuccess) return TB_ERR_CUDA;
   return TB_OK;
 }
 
@@ -559,11 +654,13 @@ extern "C" int tb_gemm_batch(int fmt, int64_t njobs, const tb_gemm_desc *descs, 
     J.N = (int)d.rows;
     J.Npad = (int)pad_up(d.rows, kRowTile);
     J.C = (int)ceil_div(ref_row_bytes(fmt, d.cols), kChunkBytes);  // == stages of 64 K
-    J.tile0 = tiles;
+    if (!encode_weight_map(&J.bmap, d.tiled, J.C, (int)ceil_div(d.rows, kRowTile)))
+      return TB_ERR_CUDA;
+    J.tile0 = tiles;  // in tile pairs
     J.ntiles = (int)ceil_div(d.rows, kGemmBN);
-    tiles += J.ntiles;
+    tiles += (int)ceil_div(J.ntiles, kGemmCluster);
   }
-  b.total = tiles * b.MH;
+  b.total = tiles * b.MH;  // pair items
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return fmt == TB_I2S ? launch_gemm<TB_I2S>(b, s) : launch_gemm<TB_TL1>(b, s);
 }
