@@ -448,10 +448,79 @@ def run_gpu(args, rank, world):
             "path": "tb.quantize_activations + tb.gemv_parallel(TL1) x3 (reference call "
                     "pattern, bench.py:138-153), float64 outputs to host"}
 
+    if rank == 0 and tp == 1 and not args.no_prefill:
+        result["prefill"] = run_prefill(torch, tb)
+
     if rank == 0 and not args.no_cpu_baseline and tp == 1:
         result["cpu_baseline"] = cpu_baseline(host_copy["gate"], host_copy["up"],
                                               host_copy["down"], budget_s=args.cpu_budget)
     return result
+
+
+def run_prefill(torch, tb, copies=2, reps=10):
+    """BASELINE configs[3]: one Llama-3-8B-shaped layer of prefill GEMMs at
+    M=512 (I2_S), q/k/v/o/gate/up on x_h and down on x_i, in ONE grouped
+    tcgen05 launch (tb_gemm_batch); int8 TOPS = 2*M*sum(N*K) / time, against
+    the cuBLASLt int8 throughput measured here (torch._int_mm, 8192^3)."""
+    import ctypes as C
+
+    from paper_2410_16144_b200 import _lib as L
+    lib = L.load()
+    M, KV = 512, 1024
+    g = torch.Generator(device="cuda").manual_seed(5)
+    xh = tb.quantize_activations(torch.randn(M, H, generator=g, device="cuda"))
+    xi = tb.quantize_activations(torch.randn(M, I, generator=g, device="cuda"))
+    tiled = {}
+    for qa, k in ((xh, H), (xi, I)):
+        t = torch.empty(lib.tb_gemm_act_bytes(M, k), dtype=torch.uint8, device="cuda")
+        L.check(lib.tb_gemm_tile_act(qa.data.data_ptr(), M, qa.data.stride(0), k, t.data_ptr(),
+                                     L.stream_ptr()), "gemm_tile_act")
+        tiled[k] = (qa, t)
+    shapes = [(H, H), (KV, H), (KV, H), (H, H), (I, H), (I, H), (H, I)]
+    ops = 2 * M * sum(n * k for n, k in shapes)
+    layers = []
+    for _ in range(copies):
+        descs = (L.GemmDesc * len(shapes))()
+        keep = []
+        for d, (n, k) in zip(descs, shapes):
+            w = torch.randn(n, k, generator=g, device="cuda") * 0.02
+            p = tb.encode_i2s(tb.ternarize_weights(w, n, k))
+            del w
+            main, _ = p.tiled()
+            out = torch.empty((M, n), dtype=torch.float32, device="cuda")
+            qa, t = tiled[k]
+            d.tiled, d.rows, d.cols, d.act_tiled = main.data_ptr(), n, k, t.data_ptr()
+            d.a_scale, d.w_scale, d.out32 = qa.scales.data_ptr(), float(p.scale), out.data_ptr()
+            keep.append((p, main, out))
+        layers.append((descs, keep))
+    s = L.stream_ptr()
+
+    def run(i):
+        L.check(lib.tb_gemm_batch(L.I2S, len(shapes), C.cast(layers[i % copies][0], C.c_void_p),
+                                  M, s), "gemm_batch")
+
+    def timed(fn, n):
+        fn(0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(n):
+            fn(i)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n
+
+    ms = timed(run, reps)
+    a = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda")
+    bt = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda").t()
+    peak_ms = timed(lambda i: torch._int_mm(a, bt), 5)
+    peak = 2 * 8192 ** 3 / (peak_ms * 1e-3) / 1e12
+    tops = ops / (ms * 1e-3) / 1e12
+    return {"workload": "cfg3: one Llama-3-8B-shaped layer (q,k,v,o,gate,up,down), M=512, I2_S, "
+                        "one grouped tcgen05 kind::i8 launch",
+            "tops": round(tops, 1), "us_per_layer": round(ms * 1e3, 1), "gop": round(ops / 1e9, 1),
+            "peak_tops": round(peak, 1), "peak_kind": "cuBLASLt int8 torch._int_mm 8192^3, measured",
+            "frac": round(tops / peak, 4)}
 
 
 def run_reference(args):
@@ -499,6 +568,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     if args.warmup < 3:
