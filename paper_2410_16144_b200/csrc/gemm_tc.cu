@@ -662,7 +662,7 @@ extern "C" int tb_gemm_batch(int fmt, int64_t njobs, const tb_gemm_desc *descs, 
   }
   b.total = tiles * b.MH;  // pair items
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return fmt == TB_I2S ? launch_gemm<TB_I2S>(b, s) : launch_gemm<TB_TL1>(b, s);
+  return launch_gemm<TB_I2S>(b, s);  // TL1 tiles hold I2_S codes (pack.cu repack)
 }
 
 extern "C" int tb_gemm_i8(int fmt, const uint8_t *tiled, int64_t rows, int64_t cols,

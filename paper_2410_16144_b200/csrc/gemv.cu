@@ -771,14 +771,14 @@ static int make_job(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign, in
 
 static int launch_batch(int fmt, GemvBatch &b, int maxM, cudaStream_t s) {
   if (fmt == TB_I2S) return dispatch_m<TB_I2S>(b, maxM, s);
-  if (fmt == TB_TL1) return dispatch_m<TB_TL1>(b, maxM, s);
+  if (fmt == TB_TL1) return dispatch_m<TB_I2S>(b, maxM, s);  // same tiled codes (pack.cu)
   if (fmt == TB_TL2) return dispatch_m<TB_TL2>(b, maxM, s);
   return TB_ERR_ARGUMENT;
 }
 
 static int launch_step(int fmt, GemvBatch &b, int rec_tab_bytes, cudaStream_t s) {
   if (fmt == TB_I2S) return launch_tgemv<TB_I2S, 1, true>(b, s, rec_tab_bytes);
-  if (fmt == TB_TL1) return launch_tgemv<TB_TL1, 1, true>(b, s, rec_tab_bytes);
+  if (fmt == TB_TL1) return launch_tgemv<TB_I2S, 1, true>(b, s, rec_tab_bytes);
   if (fmt == TB_TL2) return launch_tgemv<TB_TL2, 1, true>(b, s, rec_tab_bytes);
   return TB_ERR_ARGUMENT;
 }
@@ -806,7 +806,7 @@ extern "C" int tb_prep_activations(int fmt, const int8_t *act, int64_t M, int64_
   if (fmt == TB_I2S)
     act_prep_kernel<TB_I2S><<<grid, 256, 0, s>>>(act, (int)M, ld_act, act_len, (int)C, rec);
   else if (fmt == TB_TL1)
-    act_prep_kernel<TB_TL1><<<grid, 256, 0, s>>>(act, (int)M, ld_act, act_len, (int)C, rec);
+    act_prep_kernel<TB_I2S><<<grid, 256, 0, s>>>(act, (int)M, ld_act, act_len, (int)C, rec);
   else
     act_prep_kernel<TB_TL2><<<grid, 256, 0, s>>>(act, (int)M, ld_act, act_len, (int)C, rec);
   TB_CHECK_LAUNCH();
@@ -846,7 +846,7 @@ static int qrec_impl(int fmt, const T *x, int64_t M, int64_t K, int64_t ldx, int
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (fmt == TB_I2S) e = launch_qrec<TB_I2S>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
-  else if (fmt == TB_TL1) e = launch_qrec<TB_TL1>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
+  else if (fmt == TB_TL1) e = launch_qrec<TB_I2S>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
   else e = launch_qrec<TB_TL2>(x, M, K, ldx, q, ldq, scale, C, rec, flag, s);
   return e == cudaSuccess ? TB_OK : TB_ERR_CUDA;
 }

@@ -33,7 +33,9 @@ __global__ void gemv_lut_kernel(const uint8_t *__restrict__ tiled,
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t g = (int64_t)c * 32 + 2 * b + h;  // pair / triple index
-        const uint32_t idx = h ? (byte >> 4) : (byte & 15);
+        // TL1 tiles hold 2-bit codes (pack.cu repack): pair h = codes 2h, 2h+1
+        const uint32_t idx = FMT == TB_TL1 ? 3u * ((byte >> (4 * h)) & 3u) + ((byte >> (4 * h + 2)) & 3u)
+                                           : (h ? (byte >> 4) : (byte & 15));
         if (g >= groups) continue;
         if (FMT == TB_TL1) {
           if (idx <= 8) acc += lut[g * 9 + idx];

@@ -469,8 +469,10 @@ struct RegQuant {
 // ---------------------------------------------------------------------------
 // decode GEMV
 // ---------------------------------------------------------------------------
+// TL1 runs as I2_S: its tiles hold the same 2-bit codes (pack.cu repack).
 template <int FMT, int MT>
 struct Acc {
+  static_assert(FMT != TB_TL1, "TL1 tiles are decoded by the I2_S path");
   static constexpr int kSlots = Fmt<FMT>::kSlots;
   int32_t v[MT][kSlots];
   int32_t csum[MT];
@@ -486,9 +488,6 @@ struct Acc {
     if constexpr (FMT == TB_I2S) {
       // slot s accumulated codes * 4^s (masks without shifts): exact divisions
       return v[m][0] + (v[m][1] >> 2) + (v[m][2] >> 4) + (v[m][3] >> 6) - csum[m];
-    } else if constexpr (FMT == TB_TL1) {
-      // n*x1 (lo) + a*x0 - 3*a*x1 (lo) + 16*n*x1 / 16 (hi) + a*x0 - 3*a*x1 (hi)
-      return v[m][0] + v[m][1] - 3 * v[m][2] + (v[m][3] >> 4) + v[m][4] - 3 * v[m][5] - csum[m];
     } else {
       int32_t s = -csum[m];
 #pragma unroll
@@ -525,26 +524,6 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
           acc.v[m][1] = dp4a_us(x1, A.y, acc.v[m][1]);
           acc.v[m][2] = dp4a_us(x2, A.z, acc.v[m][2]);
           acc.v[m][3] = dp4a_us(x3, A.w, acc.v[m][3]);
-        }
-      }
-    } else if constexpr (FMT == TB_TL1) {
-      // nibble n = 3a + b (packing.py:56-60), codes a = w0+1, b = w1+1:
-      //   a*x0 + b*x1 = n*x1 + a*x0 - 3*a*x1,   a = n/3 = (11n) >> 5 for n <= 8.
-      // The high nibbles are used in place (16n): the same umulhi trick with
-      // a 16x smaller constant, and a 16x-scaled accumulator for n*x1.
-      const uint32_t lo = W & 0x0F0F0F0Fu, hi16 = W & 0xF0F0F0F0u;
-      const uint32_t alo = __umulhi(lo, 11u << 27) & 0x03030303u;
-      const uint32_t ahi = __umulhi(hi16, 11u << 23) & 0x03030303u;
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        if (m == 0 || m < M) {  // token 0 always exists: no branch for MT == 1
-          const uint4 A = *reinterpret_cast<const uint4 *>(rec0 + m * kTokStride + 16 * i);
-          acc.v[m][0] = dp4a_us(lo, A.y, acc.v[m][0]);
-          acc.v[m][1] = dp4a_us(alo, A.x, acc.v[m][1]);
-          acc.v[m][2] = dp4a_us(alo, A.y, acc.v[m][2]);
-          acc.v[m][3] = dp4a_us(hi16, A.w, acc.v[m][3]);
-          acc.v[m][4] = dp4a_us(ahi, A.z, acc.v[m][4]);
-          acc.v[m][5] = dp4a_us(ahi, A.w, acc.v[m][5]);
         }
       }
     } else {

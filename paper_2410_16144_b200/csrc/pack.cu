@@ -178,6 +178,23 @@ __global__ void validate_kernel(int fmt, const uint8_t *data, const uint8_t *sig
 }
 
 // ---- tile repack: reference rows -> [tile][chunk][row][16 B] -------------
+// TL1 bytes are re-encoded on the way: a pair index n = 3a + b (packing.py:
+// 56-60; a = w0 + 1, b = w1 + 1) becomes the two 2-bit codes (a, b), so a TL1
+// byte (pairs 2j, 2j+1 = weights 4j..4j+3) turns into the I2_S byte of the
+// same four weights.  Same 4 bits per pair, lossless for valid indices (the
+// only kind that reaches a kernel: validate() runs first), and the decode
+// GEMV / GEMM run one inner loop for both formats.  tb_unrepack inverts it.
+
+__device__ __forceinline__ uint8_t tl1_to_codes(uint32_t byte) {
+  const uint32_t lo = byte & 15u, hi = byte >> 4;
+  const uint32_t alo = (lo * 11u) >> 5, ahi = (hi * 11u) >> 5;  // n / 3 for n <= 8
+  return (uint8_t)(alo | ((lo - 3u * alo) << 2) | (ahi << 4) | ((hi - 3u * ahi) << 6));
+}
+
+__device__ __forceinline__ uint8_t codes_to_tl1(uint32_t c) {
+  const uint32_t lo = 3u * (c & 3u) + ((c >> 2) & 3u), hi = 3u * ((c >> 4) & 3u) + ((c >> 6) & 3u);
+  return (uint8_t)(lo | (hi << 4));
+}
 
 __global__ void repack_kernel(int fmt, const uint8_t *ref, const uint8_t *ref_sign, int64_t rows,
                               int64_t cols, uint8_t *tiled, uint8_t *tiled_sign, int64_t C,
@@ -197,6 +214,7 @@ __global__ void repack_kernel(int fmt, const uint8_t *ref, const uint8_t *ref_si
     for (int b = 0; b < 16; ++b) {
       int64_t j = 16 * c + b;
       buf[b] = (r < rows && j < rb) ? ref[r * rb + j] : zb;
+      if (fmt == TB_TL1) buf[b] = tl1_to_codes(buf[b]);
     }
     uint4 v;
     memcpy(&v, buf, 16);
@@ -226,7 +244,8 @@ __global__ void unrepack_kernel(int fmt, const uint8_t *tiled, const uint8_t *ti
     if (i < rows * rb) {
       int64_t r = i / rb, j = i % rb;
       int64_t t = r / kRowTile, rin = r % kRowTile, c = j / 16, b = j % 16;
-      ref[i] = tiled[((t * C + c) * kRowTile + rin) * 16 + b];
+      const uint8_t v = tiled[((t * C + c) * kRowTile + rin) * 16 + b];
+      ref[i] = fmt == TB_TL1 ? codes_to_tl1(v) : v;
     } else {
       int64_t k = i - rows * rb;
       int64_t r = k / sbpr, j = k % sbpr;
