@@ -450,6 +450,11 @@ def run_gpu(args, rank, world):
 
     if rank == 0 and tp == 1 and not args.no_prefill:
         result["prefill"] = run_prefill(torch, tb)
+    if rank == 0 and tp == 1 and args.stacks:
+        result["stacks"] = {}
+        for spec in args.stacks.split(","):
+            name, fmt, m = spec.split(":")
+            result["stacks"][spec] = run_stack(torch, tb, name, fmt, int(m))
 
     if rank == 0 and not args.no_cpu_baseline and tp == 1:
         result["cpu_baseline"] = cpu_baseline(host_copy["gate"], host_copy["up"],
@@ -523,6 +528,55 @@ def run_prefill(torch, tb, copies=2, reps=10):
             "frac": round(tops / peak, 4)}
 
 
+def run_stack(torch, tb, name, fmt, tokens=1, steps=10):
+    """BASELINE configs 2 / 4: M-token decode through the whole layer stack,
+    one launch per layer (M=1) or glue + grouped GEMV per layer (M > 1)."""
+    from paper_2410_16144_b200.stack import STACKS, LayerStack
+    cfg = STACKS[name]
+    t0 = time.perf_counter()
+    st = LayerStack(cfg, fmt=fmt, seed=11, tokens=tokens)
+    build_s = time.perf_counter() - t0
+    g = torch.Generator(device="cuda").manual_seed(99)
+    L = st.nlayers
+    if tokens == 1:
+        XH = torch.randn(L, cfg["hidden"], generator=g, device="cuda")
+        XI = torch.randn(L, cfg["inter"], generator=g, device="cuda")
+        xh, xi = list(XH), list(XI)
+        glues = None
+    else:
+        XH = torch.randn(L, tokens, cfg["hidden"], generator=g, device="cuda")
+        XI = torch.randn(L, tokens, cfg["inter"], generator=g, device="cuda")
+        xh = xi = None
+        glues = st.make_glues(XH, XI)
+    st.token_pass(xh, xi, glues)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            for _ in range(steps):
+                st.token_pass(xh, xi, glues)
+    graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    peak, _ = measured_peak()
+    gbs = st.algo_bytes / (ms * 1e-3) / 1e9
+    out = {"workload": f"{name}: {L} layers, hidden {cfg['hidden']}, {fmt.upper()}, M={tokens}",
+           "tokens_per_s": round(tokens * 1000.0 / ms, 1), "ms_per_token_pass": round(ms, 4),
+           "algo_bytes_per_pass": int(st.algo_bytes), "hbm_gbs": round(gbs, 1),
+           "frac": round(gbs / peak, 4), "launches_per_pass": L + 1 if tokens == 1 else 2 * L + 1,
+           "build_s": round(build_s, 1)}
+    del graph, st
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args):
     """--impl reference: the C port of the reference CPU kernels, all host threads."""
     import torch  # noqa: F401  (weights are generated with the same packer)
@@ -569,6 +623,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--stacks", default="cfg2:i2s:1,cfg2:tl2:1",
+                    help="layer-stack decode lines, name:fmt:M comma list ('' = none); "
+                         "e.g. cfg4:i2s:1,cfg4:i2s:8")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     if args.warmup < 3:
