@@ -631,3 +631,111 @@ def test_large_cfg3(tb):
 
 def test_large_cfg4(tb):
     _run_large(tb, "cfg4", formats=("i2s",))
+
+
+# ----------------------------------------------- toy decoder
+
+def test_toy_decoder_lossless_golden(tb):
+    """runtime.ToyDecoder / decode_tokens on the GPU kernels reproduce the
+    reference's token sequences (tests/golden, runtime.lossless_report
+    protocol, seed 13) -- and, with the corrupted LUT, the reference's
+    fault-injected sequences token for token."""
+    from paper_2410_16144_b200 import runtime as R
+    K = tb.KernelKind
+    for i in range(3):
+        d = R.ToyDecoder.build(seed=int(SMALL["d_seed"][i]))
+        prompt = int(SMALL["d_prompt"][i])
+        want = SMALL["d_tokens"][i].tolist()
+        for k in (K.REF_INT32, K.I2_S, K.TL1, K.TL2):
+            assert R.decode_tokens(d, k, prompt, 24) == want, k
+        assert R.decode_tokens(d, K.TL1, prompt, 24, _lut_hook=R._corrupting_hook) == \
+            SMALL["d_fault_tl1"][i].tolist()
+        assert R.decode_tokens(d, K.TL2, prompt, 24, _lut_hook=R._corrupting_hook) == \
+            SMALL["d_fault_tl2"][i].tolist()
+    with pytest.raises(ValueError, match="steps must be >= 1"):
+        R.decode_tokens(d, K.I2_S, 0, 0)
+    with pytest.raises(ValueError, match="prompt token out of range"):
+        R.decode_tokens(d, K.I2_S, 999, 1)
+
+
+def test_lossless_report(tb):
+    from paper_2410_16144_b200 import runtime as R
+    acc = R.lossless_report(trials=2, max_steps=6, seed=3)
+    assert all(v == 1.0 for v in acc.values())
+    table = R.format_lossless_table(acc)
+    assert "I2_S" in table and "100.0%" in table
+    with pytest.raises(ValueError, match="trials must be >= 1"):
+        R.lossless_report(trials=0, max_steps=1)
+
+
+# ----------------------------------------------------- TPK1 (SURVEY 8(f) 2)
+
+def test_tpk_load_to_device_and_write(tb, tmp_path):
+    """Reference-written TPK1 files load straight into validated, tiled device
+    matrices whose GEMV equals the oracle, and write back byte-identically."""
+    from paper_2410_16144_b200 import container as Ct
+    gold = json.loads((GOLD / "tpk_golden.json").read_text())
+    rng = np.random.default_rng(4)
+    for fmt, blob in gold["files"].items():
+        path = tmp_path / f"m_{fmt}.tpk"
+        path.write_bytes(bytes.fromhex(blob))
+        got_fmt, mats = Ct.load_model(path)
+        assert got_fmt == fmt
+        for (name, p), m in zip(mats, gold["matrices"]):
+            v = np.array(m["values"], dtype=np.int8).reshape(m["rows"], m["cols"])
+            x = rng.standard_normal(m["cols"]).astype(np.float32)
+            q, s, _ = O.quantize(x, 1)
+            kind = {"i2s": tb.KernelKind.I2_S, "tl1": tb.KernelKind.TL1,
+                    "tl2": tb.KernelKind.TL2}[fmt]
+            pad = {"i2s": 4, "tl1": 2, "tl2": 3}[fmt]
+            r = tb.gemv_parallel(kind, p, tb.quantize_activations(x, pad_to=pad))
+            assert np.array_equal(host(r.accumulators), O.gemv_ref_int32(v, q)), (fmt, name)
+        out = tmp_path / f"w_{fmt}.tpk"
+        Ct.write_model(out, mats)
+        assert out.read_bytes() == bytes.fromhex(blob)
+    # content validation happens on the device with the reference's message
+    bad = bytearray(bytes.fromhex(gold["files"]["i2s"]))
+    bad[-1] = 0xFF  # last payload byte of the last matrix: code 0b11
+    path = tmp_path / "bad.tpk"
+    path.write_bytes(bytes(bad))
+    with pytest.raises(ValueError, match=r"invalid I2_S code at row 6"):
+        Ct.load_model(path)
+
+
+def test_layer_stack_small(tb):
+    """Stack runner on a small config: every layer's projections equal the
+    oracle for that layer's inputs (M=1 fused steps and the M=3 glue path)."""
+    from paper_2410_16144_b200.stack import LayerStack
+    cfg = {"hidden": 192, "kv": 64, "inter": 320, "layers": 3}
+    for fmt, tokens in (("i2s", 1), ("tl2", 1), ("i2s", 3)):
+        st = LayerStack(cfg, fmt=fmt, seed=2, tokens=tokens)
+        g = torch.Generator(device="cuda").manual_seed(8)
+        if tokens == 1:
+            XH = torch.randn(3, 192, generator=g, device="cuda")
+            XI = torch.randn(3, 320, generator=g, device="cuda")
+            # run layer by layer so every layer's outputs can be checked
+            for li, step in enumerate(st.steps):
+                step.run([XH[li], XI[li]])
+                step.finalize()
+                torch.cuda.synchronize()
+                xs = [host(XH[li]), host(XI[li])]
+                for plan, (_, rows, cols, src) in zip(st.layers[li], st.shapes):
+                    v = host(tb.decode_i2s(plan.p).values) if fmt == "i2s" else \
+                        host(tb.decode_tl2(plan.p).values)
+                    q, s, _ = O.quantize(xs[src], 1)
+                    want = O.gemv_ref_int32(v, q).astype(np.float64) * plan.p.scale * s
+                    np.testing.assert_array_equal(host(plan.out32[0]), want.astype(np.float32))
+        else:
+            XH = torch.randn(3, tokens, 192, generator=g, device="cuda")
+            XI = torch.randn(3, tokens, 320, generator=g, device="cuda")
+            glues = st.make_glues(XH, XI)
+            st.token_pass(None, None, glues)
+            torch.cuda.synchronize()
+            li = 2  # outputs of the last layer are finalised at the end of the pass
+            for plan, (_, rows, cols, src) in zip(st.layers[li], st.shapes):
+                v = host(tb.decode_i2s(plan.p).values)
+                x = host(XH[li] if src == 0 else XI[li])
+                for m in range(tokens):
+                    q, s, _ = O.quantize(x[m], 1)
+                    want = O.gemv_ref_int32(v, q).astype(np.float64) * plan.p.scale * s
+                    np.testing.assert_array_equal(host(plan.out32[m]), want.astype(np.float32))
