@@ -739,3 +739,38 @@ def test_layer_stack_small(tb):
                     q, s, _ = O.quantize(x[m], 1)
                     want = O.gemv_ref_int32(v, q).astype(np.float64) * plan.p.scale * s
                     np.testing.assert_array_equal(host(plan.out32[m]), want.astype(np.float32))
+
+
+# ----------------------------------------- verify / bench / CLI (8(f) 3-4)
+
+def test_cli_gpu_commands(tb, tmp_path, capsys):
+    from paper_2410_16144_b200 import cli
+    rng = np.random.default_rng(0)
+    raw = tmp_path / "w.bin"
+    raw.write_bytes(rng.standard_normal(24 * 40).astype("<f4").tobytes())
+    for fmt in ("i2s", "tl1", "tl2"):
+        out = tmp_path / f"{fmt}.tpk"
+        assert cli.main(["pack", str(raw), str(out), "--rows", "24", "--cols", "40",
+                         "--format", fmt]) == 0
+        assert cli.main(["verify", str(out), "--vectors", "3", "--decoder-trials", "1",
+                         "--steps", "4"]) == 0
+        assert "100% exact (3/3 GEMVs)" in capsys.readouterr().out
+    gold = json.loads((GOLD / "tpk_golden.json").read_text())
+    bad = bytearray(bytes.fromhex(gold["files"]["i2s"]))
+    bad[-1] = 0xFF
+    (tmp_path / "bad.tpk").write_bytes(bytes(bad))
+    assert cli.main(["verify", str(tmp_path / "bad.tpk"), "--decoder-trials", "1"]) == 1
+    assert "invalid I2_S code at matrix 2 row 6" in capsys.readouterr().err
+    assert cli.main(["verify", "--random", "24", "--decoder-trials", "1", "--steps", "3"]) == 0
+    assert "cross-kernel exactness (24 instances): I2S 100% TL1 100% TL2 100%" in \
+        capsys.readouterr().out
+    assert cli.main(["verify", "--random", "8", "--decoder-trials", "4", "--steps", "8",
+                     "--fault-inject"]) == 1  # the harness detects the corrupted LUT
+    jl = tmp_path / "b.jsonl"
+    assert cli.main(["bench", "--config", "125M", "--tokens", "2", "--reps", "1",
+                     "--out", str(jl)]) == 0
+    out = capsys.readouterr().out
+    assert "GEMV-only token proxy" in out and "i2s" in out and "(" in out
+    recs = [json.loads(l) for l in jl.read_text().splitlines()]
+    assert {r["kernel"] for r in recs} == {"ref_f32", "i2s", "tl1", "tl2"}
+    assert all(r["tokens_per_sec"] > 0 for r in recs)
