@@ -220,9 +220,10 @@ int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
  * descs[j].cols == input_k[src[j]], descs[j].a_scale = the scale pointer
  * input src[j] will be given at launch.  x_after_wait != 0: the inputs are
  * produced by the preceding kernel (read after griddepcontrol.wait).
- * table_host (optional): the prepared host table -- small batches then ride
- * in the kernel parameters and each CTA quantises only the inputs its jobs
- * read.                                                                      */
+ * table_host / prev_table_host (optional): the prepared host tables -- small
+ * batches then ride in the kernel parameters (each CTA quantises only the
+ * inputs its jobs read; the previous step is finalised without descriptor
+ * loads).                                                                    */
 typedef struct tb_step_input {
   const float *x;          /* [K] float32 (device; 16-B alignment preferred)  */
   int64_t K;
@@ -238,7 +239,8 @@ int tb_gemv_step_launch(int fmt, const void *table_device, int64_t njobs,
                         int64_t total_chunks, int64_t ninputs,
                         const tb_step_input *inputs, int32_t x_after_wait,
                         const void *prev_table_device, int64_t prev_njobs,
-                        const void *table_host, void *stream);
+                        const void *table_host, const void *prev_table_host,
+                        void *stream);
 /* Finalise a batch's accumulators (scales -> outputs, workspace reset).    */
 int tb_gemv_batch_finalize(const void *table_device, int64_t njobs,
                            int64_t max_entries, void *stream);

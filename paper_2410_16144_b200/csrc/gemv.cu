@@ -66,22 +66,37 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 #define TL_LMARK(i) TL_MARK(i)
 #endif
 
-template <int FMT, int MT, bool kFused = false>
+// FU: 0 = records path; 1 = fused step, 8 warps, two CTAs per SM; 2 = fused
+// step, 16 warps, one CTA per SM (record tables too large for two CTAs)
+template <int FMT, int MT, int FU = 0>
 struct Cfg {
+  static constexpr bool kFused = FU != 0;
 #ifndef TB_MT1_WARPS
 #define TB_MT1_WARPS 16
 #endif
-  static constexpr int kWarps = MT == 1 ? TB_MT1_WARPS : (MT <= 4 ? 16 : 8);
+#ifndef TB_FUSED_WARPS
+#define TB_FUSED_WARPS 8
+#endif
+  // fused step: 8 warps and <= ~110 KB so two CTAs fit on an SM -- the next
+  // step's CTAs (programmatic dependent launch) quantise and prefetch while
+  // this step's CTAs stream
+  static constexpr int kWarps = FU == 1 ? TB_FUSED_WARPS
+                                       : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
+  static constexpr int kMinBlocks = (FU == 1 && TB_FUSED_WARPS <= 8) ? 2 : 1;
 #ifndef TB_MT1_RING
 #define TB_MT1_RING (TB_MT1_WARPS > 16 ? 3 : 4)
 #endif
-  static constexpr int kRing = MT == 1 ? TB_MT1_RING : (MT == 2 ? 3 : 2);
+  // M > 1: the deepest ring (<= 4 stages) that fits next to nothing else
+  static constexpr int kStageBytesAll =
+      kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + MT * Fmt<FMT>::kRecBytes);
+  static constexpr int kFit = (225 * 1024) / (kWarps * kStageBytesAll);
+  static constexpr int kRing = MT == 1 ? TB_MT1_RING : (kFit >= 4 ? 4 : (kFit >= 2 ? kFit : 2));
   static constexpr int kThreads = 32 * kWarps;
   // fused step: records live in a CTA-wide table after the ring, not per stage
   static constexpr int kStageBytes =
       kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + (kFused ? 0 : MT) * Fmt<FMT>::kRecBytes);
   static constexpr int kRingBytes = kWarps * kRing * kStageBytes;
-  static constexpr int kRecTabBytes = kFused ? 64 * 1024 : 0;  // max records of all inputs
+  static constexpr int kRecTabBytes = kFused ? (kMinBlocks == 2 ? 40 : 64) * 1024 : 0;  // records of all inputs
   static constexpr int kSmem = kRingBytes + kRecTabBytes;
   static_assert(kSmem <= 227 * 1024 - 512, "ring does not fit in shared memory");
 };
@@ -109,6 +124,19 @@ struct GemvJob {
 // completed by then (griddepcontrol.wait) -- so a decode step is one launch.
 constexpr int kMaxStepInputs = 4;
 constexpr int kMaxNeedCtas = 160;  // per-CTA input masks (>= the 148 SMs of a B200)
+constexpr int kMaxInlineFin = 8;   // previous-step jobs finalised from kernel parameters
+
+// What the finalize needs of a job, carried in the next step's parameters so
+// the tail of every CTA does no dependent descriptor loads.
+struct FinJob {
+  int32_t *ws_acc;
+  int32_t *acc_out;
+  double *out64;
+  float *out32;
+  const double *a_scale;
+  double w_scale;
+  int N, Npad, M;
+};
 struct StepInputs {
   const float *x[kMaxStepInputs];
   double *scale[kMaxStepInputs];   // per-token scale out (read by the finalize)
@@ -118,6 +146,8 @@ struct StepInputs {
   int x_after_wait;      // inputs produced by the preceding grid: read them after the wait
   const GemvJob *prev;   // device job table finalised after this launch's own work
   int prev_njobs;
+  int prev_inline;       // 1: prev jobs are in fin[] below
+  FinJob fin[kMaxInlineFin];
   int16_t writer[kMaxStepInputs];  // CTA that publishes input v's scale / flag
   uint8_t need[kMaxNeedCtas];      // inputs (bit v) the CTA's jobs contract
 };
@@ -181,6 +211,37 @@ __device__ __forceinline__ void finalize_one(const GemvJob &J, int part, int npa
     const int m = (int)(i / J.Npad), row = (int)(i - (int64_t)m * J.Npad);
     const int32_t v = J.ws_acc[i];
     J.ws_acc[i] = 0;
+    if (row < J.N) {
+      const int64_t o = (int64_t)m * J.N + row;
+      if (J.acc_out) J.acc_out[o] = v;
+      if (J.out64 || J.out32) {
+        const double y = static_cast<double>(v) * J.w_scale * J.a_scale[m];
+        if (J.out64) J.out64[o] = y;
+        if (J.out32) J.out32[o] = static_cast<float>(y);
+      }
+    }
+  }
+}
+
+// All inline previous-step jobs as ONE flat index space (a thread usually
+// gets a single entry): every load is issued in the first round instead of one
+// latency round per job.
+__device__ __forceinline__ void finalize_fin_all(const FinJob *fin, int njobs, int part,
+                                                 int nparts) {
+  int64_t total = 0;
+  for (int j = 0; j < njobs; ++j) total += (int64_t)fin[j].M * fin[j].Npad;
+  for (int64_t i = part * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)nparts * blockDim.x) {
+    int j = 0;
+    int64_t k = i;
+    while (k >= (int64_t)fin[j].M * fin[j].Npad) {
+      k -= (int64_t)fin[j].M * fin[j].Npad;
+      ++j;
+    }
+    const FinJob &J = fin[j];
+    const int m = (int)(k / J.Npad), row = (int)(k - (int64_t)m * J.Npad);
+    const int32_t v = J.ws_acc[k];
+    J.ws_acc[k] = 0;
     if (row < J.N) {
       const int64_t o = (int64_t)m * J.N + row;
       if (J.acc_out) J.acc_out[o] = v;
@@ -414,11 +475,12 @@ struct IssueState {
   }
 };
 
-template <int FMT, int MT, bool kFused>
-__global__ void __launch_bounds__(Cfg<FMT, MT, kFused>::kThreads, 1)
+template <int FMT, int MT, int FU>
+__global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::kMinBlocks)
     tgemv_kernel(const __grid_constant__ GemvBatch b) {
   using F = Fmt<FMT>;
-  using CF = Cfg<FMT, MT, kFused>;
+  using CF = Cfg<FMT, MT, FU>;
+  constexpr bool kFused = CF::kFused;
   static_assert(!kFused || MT == 1, "the fused step is a one-token decode step");
   constexpr int kRing = CF::kRing;
   constexpr int kIssueMain = kFused ? kIssueWeights : kIssueAll;
@@ -459,7 +521,8 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, kFused>::kThreads, 1)
   // stages' weights are requested before griddepcontrol.wait (this kernel is
   // a programmatic dependent of whatever produced the activation records);
   // the records follow once the producer has completed.
-  constexpr int kMaxG = FMT == TB_TL2 ? 2 : 3;
+  // record groups held in registers per thread (the rest take the looped path)
+  constexpr int kMaxG = CF::kThreads >= 512 ? (FMT == TB_TL2 ? 2 : 3) : (FMT == TB_TL2 ? 3 : 4);
   RegQuant<FMT, CF::kThreads, kMaxG> rq;
   if constexpr (kFused) {
     // the input loads go out first (small, L2-resident after the first CTA);
@@ -632,7 +695,11 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, kFused>::kThreads, 1)
       // plain store (this launch's verdict): the flag may live in mapped host memory
       if (b.in.flag[threadIdx.x]) *b.in.flag[threadIdx.x] = (s_badm >> threadIdx.x) & 1;
     }
-    for (int j = 0; j < b.in.prev_njobs; ++j) finalize_one(b.in.prev[j], blockIdx.x, gridDim.x);
+    if (b.in.prev_inline) {
+      finalize_fin_all(b.in.fin, b.in.prev_njobs, blockIdx.x, gridDim.x);
+    } else {
+      for (int j = 0; j < b.in.prev_njobs; ++j) finalize_one(b.in.prev[j], blockIdx.x, gridDim.x);
+    }
   }
 }
 
@@ -660,14 +727,16 @@ static int launch_finalize(const GemvBatch &b, cudaStream_t s) {
   return TB_OK;
 }
 
-template <int FMT, int MT, bool kFused = false>
+template <int FMT, int MT, int FU = 0>
 static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
-  using CF = Cfg<FMT, MT, kFused>;
+  using CF = Cfg<FMT, MT, FU>;
+  constexpr bool kFused = CF::kFused;
+  if (kFused && rec_tab_bytes > CF::kRecTabBytes) return TB_ERR_UNSUPPORTED;
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    if (cudaFuncSetAttribute(tgemv_kernel<FMT, MT, kFused>,
+    if (cudaFuncSetAttribute(tgemv_kernel<FMT, MT, FU>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, CF::kSmem) != cudaSuccess)
       return TB_ERR_CUDA;
     configured_dev = dev;
@@ -714,7 +783,7 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, tgemv_kernel<FMT, MT, kFused>, b) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, tgemv_kernel<FMT, MT, FU>, b) != cudaSuccess)
     return TB_ERR_CUDA;
   return (kFused || b.defer_finalize) ? TB_OK : launch_finalize(b, s);
 }
@@ -777,9 +846,14 @@ static int launch_batch(int fmt, GemvBatch &b, int maxM, cudaStream_t s) {
 }
 
 static int launch_step(int fmt, GemvBatch &b, int rec_tab_bytes, cudaStream_t s) {
-  if (fmt == TB_I2S) return launch_tgemv<TB_I2S, 1, true>(b, s, rec_tab_bytes);
-  if (fmt == TB_TL1) return launch_tgemv<TB_I2S, 1, true>(b, s, rec_tab_bytes);
-  if (fmt == TB_TL2) return launch_tgemv<TB_TL2, 1, true>(b, s, rec_tab_bytes);
+  // two CTAs per SM when the record tables allow it, else one
+  const bool small = rec_tab_bytes <= Cfg<TB_I2S, 1, 1>::kRecTabBytes;
+  if (fmt == TB_I2S || fmt == TB_TL1)  // TL1 tiles hold I2_S codes
+    return small ? launch_tgemv<TB_I2S, 1, 1>(b, s, rec_tab_bytes)
+                 : launch_tgemv<TB_I2S, 1, 2>(b, s, rec_tab_bytes);
+  if (fmt == TB_TL2)
+    return small ? launch_tgemv<TB_TL2, 1, 1>(b, s, rec_tab_bytes)
+                 : launch_tgemv<TB_TL2, 1, 2>(b, s, rec_tab_bytes);
   return TB_ERR_ARGUMENT;
 }
 
@@ -955,7 +1029,8 @@ extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t nj
                                    int64_t total_chunks, int64_t ninputs,
                                    const tb_step_input *inputs, int32_t x_after_wait,
                                    const void *prev_table_device, int64_t prev_njobs,
-                                   const void *table_host, void *stream) {
+                                   const void *table_host, const void *prev_table_host,
+                                   void *stream) {
   if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !table_device || total_chunks < 1 ||
       total_chunks >= ((int64_t)1 << 31) || ninputs < 1 || ninputs > kMaxStepInputs ||
       !inputs || prev_njobs < 0 || (prev_njobs > 0 && !prev_table_device) ||
@@ -979,11 +1054,28 @@ extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t nj
     b.in.off[v] = (int)off;
     off += C * rec;
   }
-  if (off > 64 * 1024) return TB_ERR_UNSUPPORTED;  // record tables must fit in shared memory
+  if (off > 64 * 1024) return TB_ERR_UNSUPPORTED;  // (and <= the kernel's table, checked at launch)
   b.in.n = (int)ninputs;
   b.in.x_after_wait = x_after_wait ? 1 : 0;
   b.in.prev = static_cast<const GemvJob *>(prev_table_device);
   b.in.prev_njobs = (int)prev_njobs;
+  b.in.prev_inline = 0;
+  if (prev_table_host && prev_njobs > 0 && prev_njobs <= kMaxInlineFin) {
+    const GemvJob *h = static_cast<const GemvJob *>(prev_table_host);
+    for (int j = 0; j < prev_njobs; ++j) {
+      FinJob &F = b.in.fin[j];
+      F.ws_acc = h[j].ws_acc;
+      F.acc_out = h[j].acc_out;
+      F.out64 = h[j].out64;
+      F.out32 = h[j].out32;
+      F.a_scale = h[j].a_scale;
+      F.w_scale = h[j].w_scale;
+      F.N = h[j].N;
+      F.Npad = h[j].Npad;
+      F.M = h[j].M;
+    }
+    b.in.prev_inline = 1;
+  }
   if (table_host && njobs <= kMaxInlineJobs) {  // jobs inline in the kernel parameters
     const GemvJob *h = static_cast<const GemvJob *>(table_host);
     for (int j = 0; j < njobs; ++j) b.jobs[j] = h[j];

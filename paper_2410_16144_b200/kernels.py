@@ -324,6 +324,8 @@ class GemvBatch:
                                           C.byref(maxm), C.byref(maxe)), "gemv_batch_prepare")
         dev = pairs[0][0].main.device
         self.table = torch.from_numpy(host).to(dev)
+        self._host = host  # host copy of the job table (inline finalize by a later step)
+        self._host_ptr = host.ctypes.data
         self.njobs, self.total, self.max_m = len(pairs), total.value, maxm.value
         self.max_entries = maxe.value
         self.pairs = pairs  # keep every buffer alive
@@ -474,6 +476,7 @@ class GemvStep:
             self._inputs_ptr, 1 if self.x_after_wait else 0,
             prev.table.data_ptr() if prev is not None else None,
             prev.njobs if prev is not None else 0, self._host_ptr,
+            getattr(prev, "_host_ptr", None) if prev is not None else None,
             stream_ptr if stream_ptr is not None else L.stream_ptr())
         if st:
             L.check(st, "gemv_step_launch")
