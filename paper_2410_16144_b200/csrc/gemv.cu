@@ -696,7 +696,9 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       if (b.in.flag[threadIdx.x]) *b.in.flag[threadIdx.x] = (s_badm >> threadIdx.x) & 1;
     }
     if (b.in.prev_inline) {
+#ifndef TB_NO_PREVFIN  // profiling variant: skip the previous step's finalize
       finalize_fin_all(b.in.fin, b.in.prev_njobs, blockIdx.x, gridDim.x);
+#endif
     } else {
       for (int j = 0; j < b.in.prev_njobs; ++j) finalize_one(b.in.prev[j], blockIdx.x, gridDim.x);
     }
