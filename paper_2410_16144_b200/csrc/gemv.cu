@@ -254,6 +254,32 @@ __device__ __forceinline__ void finalize_fin_all(const FinJob *fin, int njobs, i
   }
 }
 
+// Flat entries first, first + stride, ... (the tail beyond one per thread).
+__device__ __forceinline__ void finalize_fin_range(const FinJob *fin, int njobs, int64_t first,
+                                                   int64_t stride) {
+  int64_t total = 0;
+  for (int j = 0; j < njobs; ++j) total += (int64_t)fin[j].M * fin[j].Npad;
+  for (int64_t i = first; i < total; i += stride) {
+    int j = 0;
+    int64_t k = i;
+    while (k >= (int64_t)fin[j].M * fin[j].Npad) {
+      k -= (int64_t)fin[j].M * fin[j].Npad;
+      ++j;
+    }
+    const FinJob &J = fin[j];
+    const int m = (int)(k / J.Npad), row = (int)(k - (int64_t)m * J.Npad);
+    const int32_t v = J.ws_acc[k];
+    J.ws_acc[k] = 0;
+    if (row < J.N) {
+      const int64_t o = (int64_t)m * J.N + row;
+      if (J.acc_out) J.acc_out[o] = v;
+      const double y = static_cast<double>(v) * J.w_scale * J.a_scale[m];
+      if (J.out64) J.out64[o] = y;
+      if (J.out32) J.out32[o] = static_cast<float>(y);
+    }
+  }
+}
+
 __device__ __forceinline__ void finalize_job(const GemvBatch &b, int j, int part, int nparts) {
   finalize_one(job_at(b, j), part, nparts);
 }
@@ -597,11 +623,39 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // The fused step publishes partial sums only once the previous step's grid
   // has completed: it finalises (reads and zeroes) a workspace that a later
   // launch of the same batch would otherwise accumulate into.
+  // The previous step's outputs: right after that wait each thread LOADS its
+  // entry of the flat (job, row) space (one per thread when the grid covers
+  // it) -- the loads complete while the warp keeps streaming -- and the
+  // stores happen at the end, so no load latency sits in the CTA's tail.
+  int fin_j = -1;
+  int64_t fin_k = 0;
+  int32_t fin_v = 0;
+  double fin_as = 0.0;
+  auto fin_load = [&]() {
+    if constexpr (kFused) {
+      if (!b.in.prev_inline) return;
+      int64_t k = (int64_t)gw * 32 + lane;
+      for (int j = 0; j < b.in.prev_njobs; ++j) {
+        const FinJob &J = b.in.fin[j];
+        const int64_t n = (int64_t)J.M * J.Npad;
+        if (k < n) {
+          fin_j = j;
+          fin_k = k;
+          fin_v = __ldcg(J.ws_acc + k);
+          const int m = (int)(k / J.Npad);
+          fin_as = J.a_scale ? __ldcg(J.a_scale + m) : 0.0;
+          return;
+        }
+        k -= n;
+      }
+    }
+  };
   auto flush = [&](const Acc<FMT, MT> &acc, int M) {
     if constexpr (kFused) {
       if (!waited) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
         waited = true;
+        fin_load();
       }
     }
     flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
@@ -687,7 +741,10 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   }
   TL_MARK(4);
   if constexpr (kFused) {
-    if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      fin_load();
+    }
     // this step's scales (read by whoever finalises this batch), then the
     // previous step's outputs: its grid has completed, its sums are visible
     if (threadIdx.x < b.in.n && b.in.writer[threadIdx.x] == (int)blockIdx.x) {
@@ -697,7 +754,26 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     }
     if (b.in.prev_inline) {
 #ifndef TB_NO_PREVFIN  // profiling variant: skip the previous step's finalize
-      finalize_fin_all(b.in.fin, b.in.prev_njobs, blockIdx.x, gridDim.x);
+      if (fin_j >= 0) {  // the entry loaded at the wait: stores only
+        const FinJob &J = b.in.fin[fin_j];
+        J.ws_acc[fin_k] = 0;
+        const int m = (int)(fin_k / J.Npad), row = (int)(fin_k - (int64_t)m * J.Npad);
+        if (row < J.N) {
+          const int64_t o = (int64_t)m * J.N + row;
+          if (J.acc_out) J.acc_out[o] = fin_v;
+          const double y = static_cast<double>(fin_v) * J.w_scale * fin_as;  // core.py:99-101
+          if (J.out64) J.out64[o] = y;
+          if (J.out32) J.out32[o] = static_cast<float>(y);
+        }
+      }
+      // entries beyond one per thread of the grid (large previous steps)
+      const int64_t nthreads = (int64_t)gridDim.x * CF::kThreads;
+      int64_t total = 0;
+      for (int j = 0; j < b.in.prev_njobs; ++j) total += (int64_t)b.in.fin[j].M * b.in.fin[j].Npad;
+      if (total > nthreads) {
+        finalize_fin_range(b.in.fin, b.in.prev_njobs, nthreads + (int64_t)gw * 32 + lane,
+                           nthreads);
+      }
 #endif
     } else {
       for (int j = 0; j < b.in.prev_njobs; ++j) finalize_one(b.in.prev[j], blockIdx.x, gridDim.x);
