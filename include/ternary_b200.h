@@ -224,6 +224,10 @@ int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
  * batches then ride in the kernel parameters (each CTA quantises only the
  * inputs its jobs read; the previous step is finalised without descriptor
  * loads).                                                                    */
+/* tb_gemv_step_launch `flags`: */
+#define TB_STEP_X_AFTER_WAIT 1 /* inputs written by the preceding kernel          */
+#define TB_STEP_ISOLATED 2     /* one launch at a time (no chained step to overlap):
+                                  one 16-warp CTA per SM instead of two 8-warp ones */
 typedef struct tb_step_input {
   const float *x;          /* [K] float32 (device; 16-B alignment preferred)  */
   int64_t K;
@@ -237,7 +241,7 @@ int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
                          int64_t *max_entries);
 int tb_gemv_step_launch(int fmt, const void *table_device, int64_t njobs,
                         int64_t total_chunks, int64_t ninputs,
-                        const tb_step_input *inputs, int32_t x_after_wait,
+                        const tb_step_input *inputs, int32_t flags,
                         const void *prev_table_device, int64_t prev_njobs,
                         const void *table_host, const void *prev_table_host,
                         void *stream);

@@ -923,9 +923,10 @@ static int launch_batch(int fmt, GemvBatch &b, int maxM, cudaStream_t s) {
   return TB_ERR_ARGUMENT;
 }
 
-static int launch_step(int fmt, GemvBatch &b, int rec_tab_bytes, cudaStream_t s) {
-  // two CTAs per SM when the record tables allow it, else one
-  const bool small = rec_tab_bytes <= Cfg<TB_I2S, 1, 1>::kRecTabBytes;
+static int launch_step(int fmt, GemvBatch &b, int rec_tab_bytes, bool isolated, cudaStream_t s) {
+  // two 8-warp CTAs per SM (chained steps overlap) when the record tables
+  // allow it; one 16-warp CTA per SM for big tables or an isolated launch
+  const bool small = !isolated && rec_tab_bytes <= Cfg<TB_I2S, 1, 1>::kRecTabBytes;
   if (fmt == TB_I2S || fmt == TB_TL1)  // TL1 tiles hold I2_S codes
     return small ? launch_tgemv<TB_I2S, 1, 1>(b, s, rec_tab_bytes)
                  : launch_tgemv<TB_I2S, 1, 2>(b, s, rec_tab_bytes);
@@ -1105,7 +1106,7 @@ extern "C" int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *
 
 extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t njobs,
                                    int64_t total_chunks, int64_t ninputs,
-                                   const tb_step_input *inputs, int32_t x_after_wait,
+                                   const tb_step_input *inputs, int32_t x_after_wait,  /* TB_STEP_* flags */
                                    const void *prev_table_device, int64_t prev_njobs,
                                    const void *table_host, const void *prev_table_host,
                                    void *stream) {
@@ -1134,7 +1135,8 @@ extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t nj
   }
   if (off > 64 * 1024) return TB_ERR_UNSUPPORTED;  // (and <= the kernel's table, checked at launch)
   b.in.n = (int)ninputs;
-  b.in.x_after_wait = x_after_wait ? 1 : 0;
+  b.in.x_after_wait = (x_after_wait & TB_STEP_X_AFTER_WAIT) ? 1 : 0;
+  const bool isolated = (x_after_wait & TB_STEP_ISOLATED) != 0;
   b.in.prev = static_cast<const GemvJob *>(prev_table_device);
   b.in.prev_njobs = (int)prev_njobs;
   b.in.prev_inline = 0;
@@ -1159,7 +1161,7 @@ extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t nj
     for (int j = 0; j < njobs; ++j) b.jobs[j] = h[j];
     b.table = nullptr;
   }
-  return launch_step(fmt, b, (int)off, static_cast<cudaStream_t>(stream));
+  return launch_step(fmt, b, (int)off, isolated, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int tb_gemv_batch_finalize(const void *table_device, int64_t njobs,

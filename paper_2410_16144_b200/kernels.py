@@ -396,7 +396,8 @@ class GemvStep:
     ``x_after_wait``: the inputs are written by the preceding kernel.
     """
 
-    def __init__(self, pairs, input_k, x_after_wait: bool = False, flags=None):
+    def __init__(self, pairs, input_k, x_after_wait: bool = False, flags=None,
+                 isolated: bool = False):
         import ctypes as C
         import numpy as np
 
@@ -444,6 +445,8 @@ class GemvStep:
         self._host_ptr = host.ctypes.data
         self.njobs, self.total, self.max_entries = len(pairs), total.value, maxe.value
         self.x_after_wait = bool(x_after_wait)
+        # isolated: launched one at a time (e.g. HostStep), not as a chain
+        self._launch_flags = (1 if x_after_wait else 0) | (2 if isolated else 0)
         self.inputs = (L.StepInput * len(input_k))()
         for i, k in enumerate(self.input_k):
             self.inputs[i].K = k
@@ -473,7 +476,7 @@ class GemvStep:
             raise ValueError("a step cannot finalise its own previous launch")
         st = self._lib.tb_gemv_step_launch(
             self.fmt, self.table.data_ptr(), self.njobs, self.total, len(self.input_k),
-            self._inputs_ptr, 1 if self.x_after_wait else 0,
+            self._inputs_ptr, self._launch_flags,
             prev.table.data_ptr() if prev is not None else None,
             prev.njobs if prev is not None else 0, self._host_ptr,
             getattr(prev, "_host_ptr", None) if prev is not None else None,
@@ -528,7 +531,7 @@ class HostStep:
                 out64=o if out_dtype == torch.float64 else None), v))
         self.flags_host = torch.zeros(len(input_k), dtype=torch.int32).pin_memory()
         self._flags_np = self.flags_host.numpy()  # shares the pinned buffer
-        self.step = GemvStep(host_pairs, input_k, flags=self.flags_host)
+        self.step = GemvStep(host_pairs, input_k, flags=self.flags_host, isolated=True)
         self._record = self._capture()
         self._stream = torch.cuda.current_stream()
 
