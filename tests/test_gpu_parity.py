@@ -522,16 +522,20 @@ def test_prefill_gemm_batch_grouped(tb):
         p = tb.encode_i2s(tb.TernaryMatrix(n, k, v, 1.0))
         main, _ = p.tiled()
         acc = torch.empty((M, n), dtype=torch.int32, device="cuda")
+        o32 = torch.empty((M, n), dtype=torch.float32, device="cuda")
+        d.out32 = o32.data_ptr()  # fp32 outputs: within 1e-5 relative (north star)
         d.tiled, d.rows, d.cols = main.data_ptr(), n, k
         d.act_tiled = tiled_in[id(qa)].data_ptr()
         d.a_scale, d.w_scale, d.acc_out = qa.scales.data_ptr(), 1.0, acc.data_ptr()
-        keep.append((p, main, acc, qa))
+        keep.append((p, main, acc, qa, o32))
         q = host(qa.data)
         wants.append(np.stack([O.gemv_ref_int32(v, q[m]) for m in range(M)]))
     L.check(lib.tb_gemm_batch(1, len(shapes), C.cast(descs, C.c_void_p), M, L.stream_ptr()))
     torch.cuda.synchronize()
-    for (p, main, acc, qa), want in zip(keep, wants):
+    for (p, main, acc, qa, o32), want in zip(keep, wants):
         assert np.array_equal(host(acc), want)
+        ref = want.astype(np.float64) * 1.0 * host(qa.scales)[:, None]
+        np.testing.assert_allclose(host(o32), ref, rtol=1e-5, atol=0)
 
 
 def test_host_step(tb):

@@ -96,6 +96,18 @@ def main():
                                   C.cast(descs, C.c_void_p), M, s))
 
     us = events_us(run, 12)
+    if os.environ.get("TRACE_EPI"):
+        import numpy as np
+        lib.tb_gemm_epi_trace_fetch.argtypes = [C.c_void_p, C.c_int64]
+        run()
+        torch.cuda.synchronize()
+        buf = np.zeros((16, 3), dtype=np.int64)
+        lib.tb_gemm_epi_trace_fetch(buf.ctypes.data_as(C.c_void_p), buf.nbytes)
+        t0 = buf[0, 0]
+        print("tile: decoders_done  tfull_ok  epilogue_done (clk since tile0 decode end)")
+        for t in range(16):
+            if buf[t, 0]:
+                print(t, *(int(v - t0) for v in buf[t]))
     if os.environ.get("TRACE"):
         import numpy as np
         lib.tb_gemm_trace_fetch.argtypes = [C.c_void_p, C.c_int64]
