@@ -61,7 +61,7 @@ constexpr int kGemmMaxJobs = 8;
 constexpr int kSubTileBytes = kGemmSubM * kGemmBK;    // 8 KB
 constexpr int kBTileBytes = kGemmBN * kGemmBK;        // 16 KB
 constexpr int kPackedBytes = kGemmBN * kChunkBytes;   // 4 KB
-constexpr int kEpiBytes = 8 * 32 * 32 * 4;            // 8 epilogue warps x 32x32 int32 (in the B slots)
+constexpr int kEpiBytes = 8 * 32 * 36 * 4;            // 8 epilogue warps x 32x32 int32 (in the B slots)
 static_assert(kEpiBytes <= kGemmBSlots * kBTileBytes, "epilogue staging lives in the B slots");
 
 struct alignas(64) GemmJob {
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
     // cp.async, so their fence.proxy.async covers only their own st.shared. =====
     const int r = tid - 128;
     const int lg = warp & 3, chalf = (warp - 4) >> 2;
-    uint32_t *stg = reinterpret_cast<uint32_t *>(bslots) + (warp - 4) * 32 * 32;  // epilogue only
+    uint32_t *stg = reinterpret_cast<uint32_t *>(bslots) + (warp - 4) * 32 * 36;  // epilogue only
     GemmCursor cc;
     cc.start(b);
     uint32_t tiles = 0;
@@ -409,7 +409,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
                   "=r"(v[30]), "=r"(v[31])
                 : "r"(tmem + ((uint32_t)(lg * 32) << 16) + mt * kGemmBN + col));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            // lane = row: stage it XOR-rotated, then lane = column
+            // fp32-only outputs of a full 32-column block: 128-bit stores, four
+            // rows per warp instruction (the output write is what limits the
+            // epilogue); rows staged with a 36-word pitch (16-B aligned)
+            if (out32 && !out64 && !acc_out && (Nj & 3) == 0 && cc.n0 + col + 32 <= Nj) {
+#pragma unroll
+              for (int e = 0; e < 32; e += 4)
+                *reinterpret_cast<uint4 *>(stg + lane * 36 + e) =
+                    make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+              __syncwarp();
+              const int q = lane >> 3, c4 = (lane & 7) * 4;
+#pragma unroll
+              for (int it = 0; it < 8; ++it) {
+                const int r = it * 4 + q;
+                const int32_t asum = __shfl_sync(0xffffffffu, my_sum, r);
+                const float fs = __shfl_sync(0xffffffffu, my_fs, r);
+                if (r < rows) {
+                  const uint4 w = *reinterpret_cast<const uint4 *>(stg + r * 36 + c4);
+                  float4 o;
+                  o.x = static_cast<float>((int32_t)w.x - asum) * fs;
+                  o.y = static_cast<float>((int32_t)w.y - asum) * fs;
+                  o.z = static_cast<float>((int32_t)w.z - asum) * fs;
+                  o.w = static_cast<float>((int32_t)w.w - asum) * fs;
+                  *reinterpret_cast<float4 *>(out32 + (int64_t)(mrow0 + r) * Nj + cc.n0 + col + c4) = o;
+                }
+              }
+              __syncwarp();
+              continue;
+            }
+            // general path -- lane = row: stage it XOR-rotated, then lane = column
 #pragma unroll
             for (int e = 0; e < 32; ++e) stg[lane * 32 + ((e + lane) & 31)] = v[e];
             __syncwarp();
