@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
         if (k < n) {
           fin_j = j;
           fin_k = k;
-          fin_v = __ldcg(J.ws_acc + k);
+          fin_v = atomicExch(J.ws_acc + k, 0);  // read and reset in one L2 operation
           const int m = (int)(k / J.Npad);
           fin_as = J.a_scale ? __ldcg(J.a_scale + m) : 0.0;
           return;
@@ -754,9 +754,8 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     }
     if (b.in.prev_inline) {
 #ifndef TB_NO_PREVFIN  // profiling variant: skip the previous step's finalize
-      if (fin_j >= 0) {  // the entry loaded at the wait: stores only
+      if (fin_j >= 0) {  // the entry read (and reset) at the wait: output store only
         const FinJob &J = b.in.fin[fin_j];
-        J.ws_acc[fin_k] = 0;
         const int m = (int)(fin_k / J.Npad), row = (int)(fin_k - (int64_t)m * J.Npad);
         if (row < J.N) {
           const int64_t o = (int64_t)m * J.N + row;
