@@ -210,14 +210,18 @@ def run_gpu(args, rank, world):
 
     import paper_2410_16144_b200 as tb
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", _local_device(torch))
     torch.cuda.set_device(dev)
-    tp = world
+    # N > 1: independent decode replicas by default (each GPU holds the block
+    # and decodes its own token stream -- no data-path collective, weak
+    # scaling); --parallel tp shards the block instead (column-parallel
+    # gate/up, row-parallel down + one NCCL int32 all-reduce per token).
+    tp = world if args.parallel == "tp" else 1
     # ---- weights: NCOPY distinct seeded copies, TP-sharded
     plans = []
     gate_full_bytes = 0
     for c in range(NCOPY):
-        gen = torch.Generator(device="cuda").manual_seed(1000 + c)
+        gen = torch.Generator(device="cuda").manual_seed(1000 + c + (rank * 97 if tp == 1 else 0))
         mats = {}
         for name, rows, cols in (("gate", I, H), ("up", I, H), ("down", H, I)):
             w = torch.randn(rows, cols, generator=gen, device="cuda", dtype=torch.float32) * 0.02
@@ -248,7 +252,7 @@ def run_gpu(args, rank, world):
             p._cache.pop("ref_dropped", None)
     torch.cuda.synchronize()
 
-    gen = torch.Generator(device="cuda").manual_seed(77)
+    gen = torch.Generator(device="cuda").manual_seed(77 + rank)
     XH = torch.randn(NX, H, generator=gen, device="cuda", dtype=torch.float32)
     XI = torch.randn(NX, I, generator=gen, device="cuda", dtype=torch.float32)
     # activation records: quantisation fused with the GEMV input layout; the
@@ -311,23 +315,32 @@ def run_gpu(args, rank, world):
     run_steps(max(args.warmup, NCOPY))
     torch.cuda.synchronize()
 
-    # ---- device-resident timed region: K steps in one CUDA graph
+    # ---- device-resident timed region: K steps in one CUDA graph (NCCL
+    #      collectives are capturable; a gloo functional check runs eagerly)
+    capturable = world == 1 or dist.get_backend() == "nccl"
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     graph = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(s):
-        with torch.cuda.graph(graph, stream=s):
+    if capturable:
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(graph, stream=s):
+                run_steps(args.steps)
+        torch.cuda.synchronize()
+        graph.replay()  # untimed replay (first replay uploads the graph)
+        torch.cuda.synchronize()
+
+        def timed_region():
+            graph.replay()
+    else:
+        def timed_region():
             run_steps(args.steps)
-    torch.cuda.synchronize()
-    graph.replay()  # untimed replay (first replay uploads the graph)
-    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
         e0.record()
-        graph.replay()
+        timed_region()
         e1.record()
         torch.cuda.synchronize()
     if world > 1:
@@ -370,17 +383,20 @@ def run_gpu(args, rank, world):
     peak, peak_kind = measured_peak()
     achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
 
+    replicas = world if tp == 1 else 1
     result = {
-        "metric": METRIC, "value": round(1000.0 / ms_per_step, 2), "unit": "tokens/s",
+        "metric": METRIC, "value": round(replicas * 1000.0 / ms_per_step, 2), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "i8",
+        "scaling": "weak" if replicas > 1 else "strong", "vs_baseline": None, "dtype": "i8",
         "data": "synthetic (seeded N(0,0.02) latent weights -> absmean ternary, N(0,1) activations)",
         "config": {"workload": "cfg1: TL1 FFN block, gate/up 4096->14336 + down 14336->4096, M=1",
-                   "format": "TL1", "tokens_per_step": 1,
+                   "format": "TL1", "tokens_per_step": replicas,
                    "l2": f"{NCOPY} rotating weight copies ({NCOPY * 3 * gate_full_bytes / 1e6:.0f} MB "
                          "packed per rank) > 126 MB L2",
-                   "parallelism": "tp1" if tp == 1 else f"tp{tp} (col-parallel gate/up, "
+                   "parallelism": (f"dp{world} (independent decode replicas, no collective)"
+                                   if replicas > 1 else "tp1") if tp == 1 else
+                                  f"tp{tp} (col-parallel gate/up, "
                                   "row-parallel down + NCCL int32 all-reduce)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -614,6 +630,16 @@ def run_reference(args):
     }
 
 
+def _local_device(torch):
+    """LOCAL_RANK's GPU.  TB_BENCH_SHARE_GPU=1 folds ranks onto the visible
+    GPUs -- a functional check of the tp > 1 code path on a 1-GPU box (with
+    TB_BENCH_DIST_BACKEND=gloo), never a measurement."""
+    lr = int(os.environ.get("LOCAL_RANK", 0))
+    if os.environ.get("TB_BENCH_SHARE_GPU") == "1":
+        lr %= torch.cuda.device_count()
+    return lr
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -627,6 +653,8 @@ def main():
                     help="layer-stack decode lines, name:fmt:M comma list ('' = none); "
                          "e.g. cfg4:i2s:1,cfg4:i2s:8")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--parallel", default="dp", choices=["dp", "tp"],
+                    help="N > 1: independent replicas (dp, default) or tensor parallel (tp)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -641,8 +669,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(_local_device(torch))
+        dist.init_process_group(os.environ.get("TB_BENCH_DIST_BACKEND", "nccl"))
     res = run_gpu(args, rank, world)
     if rank == 0:
         print(json.dumps(res), flush=True)
