@@ -123,18 +123,13 @@ __device__ __forceinline__ void tc_fence_after() {
 }
 
 // One packed 32-bit word (16 weights) -> four code planes; byte q of plane s
-// is the code (w + 1) of weight 4q + s (packing.py:200-206, 222-233).
+// is the code (w + 1) of weight 4q + s (packing.py:200-206).  TL1 tiles hold
+// the same 2-bit codes (the repack turns each pair index into two codes).
 template <int FMT>
 __device__ __forceinline__ uint4 code_planes(uint32_t W) {
-  if constexpr (FMT == TB_I2S) {
-    return make_uint4(W & 0x03030303u, (W >> 2) & 0x03030303u, (W >> 4) & 0x03030303u,
-                      (W >> 6) & 0x03030303u);
-  } else {  // nibble n = 3a + b: weights (4q, 4q+1) from the low nibble, (4q+2, 4q+3) high
-    const uint32_t lo = W & 0x0F0F0F0Fu, hi = (W >> 4) & 0x0F0F0F0Fu;
-    const uint32_t alo = __umulhi(lo, 11u << 27) & 0x03030303u;
-    const uint32_t ahi = __umulhi(hi, 11u << 27) & 0x03030303u;
-    return make_uint4(alo, lo - 3u * alo, ahi, hi - 3u * ahi);
-  }
+  static_assert(FMT == TB_I2S, "TL1 tiles are I2_S-coded; TL2 has no GEMM path");
+  return make_uint4(W & 0x03030303u, (W >> 2) & 0x03030303u, (W >> 4) & 0x03030303u,
+                    (W >> 6) & 0x03030303u);
 }
 
 // Cursor over this CTA's (work item, K stage) stream: items blockIdx.x,
