@@ -469,6 +469,9 @@ def run_gpu(args, rank, world):
     if rank == 0 and tp == 1 and args.stacks:
         result["stacks"] = {}
         for spec in args.stacks.split(","):
+            if spec == "cfg0":
+                result["stacks"][spec] = run_cfg0(torch, tb)
+                continue
             name, fmt, m = spec.split(":")
             result["stacks"][spec] = run_stack(torch, tb, name, fmt, int(m))
 
@@ -593,6 +596,50 @@ def run_stack(torch, tb, name, fmt, tokens=1, steps=10):
     return out
 
 
+def run_cfg0(torch, tb, copies=32, steps=200):
+    """BASELINE configs[0]: one I2_S GEMV, M=1, 4096 x 4096 -- one fused
+    launch per token (quantise + GEMV + previous finalize), rotating over
+    32 weight copies (134 MB > L2) in a CUDA graph."""
+    n = k = 4096
+    g = torch.Generator(device="cuda").manual_seed(3)
+    steps_obj = []
+    for _ in range(copies):
+        w = torch.randn(n, k, generator=g, device="cuda") * 0.02
+        plan = tb.GemvPlan(tb.encode_i2s(tb.ternarize_weights(w, n, k)), out_dtype=torch.float32)
+        steps_obj.append(tb.GemvStep([(plan, 0)], [k]))
+        del w
+    X = torch.randn(16, k, generator=g, device="cuda")
+
+    def run(cnt):
+        for i in range(cnt):
+            steps_obj[i % copies].run([X[i % 16]], prev=steps_obj[(i - 1) % copies])
+        steps_obj[(cnt - 1) % copies].finalize()
+
+    run(copies)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            run(steps)
+    graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / steps
+    algo = n * k // 4 + k + 4 * n
+    peak, _ = measured_peak()
+    return {"workload": "cfg0: I2_S GEMV M=1, 4096x4096, one fused launch per token",
+            "tokens_per_s": round(1e6 / us, 1), "us_per_gemv": round(us, 3),
+            "algo_bytes": algo, "hbm_gbs": round(algo / (us * 1e-6) / 1e9, 1),
+            "frac": round(algo / (us * 1e-6) / 1e9 / peak, 4),
+            "note": "4.2 MB per launch: launch/latency-bound, not bandwidth-bound"}
+
+
 def run_reference(args):
     """--impl reference: the C port of the reference CPU kernels, all host threads."""
     import torch  # noqa: F401  (weights are generated with the same packer)
@@ -649,7 +696,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
-    ap.add_argument("--stacks", default="cfg2:i2s:1,cfg2:tl2:1",
+    ap.add_argument("--stacks", default="cfg0,cfg2:i2s:1,cfg2:tl2:1",
                     help="layer-stack decode lines, name:fmt:M comma list ('' = none); "
                          "e.g. cfg4:i2s:1,cfg4:i2s:8")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
