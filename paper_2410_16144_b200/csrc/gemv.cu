@@ -650,12 +650,44 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       }
     }
   };
+  // Fused step: a finished tile's partial sums (one int32 per lane) are
+  // stashed in registers instead of published, so the warp never stops its
+  // weight stream at griddepcontrol.wait; the wait, the previous step's
+  // finalize loads and the REDs all happen once the warp's range is done.
+  // A range crossing more than kStash tiles waits at the overflow instead.
+  constexpr int kStash = kFused ? 4 : 1;
+  int ns = 0;
+  int32_t st_v[kStash];
+  int st_j[kStash], st_t[kStash];
+  auto drain = [&]() {
+#pragma unroll
+    for (int s = 0; s < kStash; ++s)
+      if (s < ns) {
+#ifndef TB_NO_FLUSH
+        red_add_s32(job_at(b, st_j[s]).ws_acc + st_t[s] * kRowTile + lane, st_v[s]);
+#endif
+      }
+    ns = 0;
+  };
   auto flush = [&](const Acc<FMT, MT> &acc, int M) {
     if constexpr (kFused) {
       if (!waited) {
+        if (ns < kStash) {
+          const int32_t v = acc.total(0);
+#pragma unroll
+          for (int s = 0; s < kStash; ++s)
+            if (s == ns) {
+              st_v[s] = v;
+              st_j[s] = cur.j;
+              st_t[s] = cur.t;
+            }
+          ++ns;
+          return;
+        }
         asm volatile("griddepcontrol.wait;" ::: "memory");
         waited = true;
         fin_load();
+        drain();
       }
     }
     flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
@@ -745,6 +777,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       asm volatile("griddepcontrol.wait;" ::: "memory");
       fin_load();
     }
+    drain();
     // this step's scales (read by whoever finalises this batch), then the
     // previous step's outputs: its grid has completed, its sums are visible
     if (threadIdx.x < b.in.n && b.in.writer[threadIdx.x] == (int)blockIdx.x) {
