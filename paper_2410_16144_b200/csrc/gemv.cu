@@ -82,7 +82,13 @@ struct Cfg {
   // this step's CTAs stream
   static constexpr int kWarps = FU == 1 ? TB_FUSED_WARPS
                                        : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
-  static constexpr int kMinBlocks = (FU == 1 && TB_FUSED_WARPS <= 8) ? 2 : 1;
+#ifndef TB_FUSED_MINB
+#define TB_FUSED_MINB 2
+#endif
+#ifndef TB_FUSED_RING
+#define TB_FUSED_RING 4
+#endif
+  static constexpr int kMinBlocks = (FU == 1 && TB_FUSED_WARPS <= 16) ? TB_FUSED_MINB : 1;
 #ifndef TB_MT1_RING
 #define TB_MT1_RING (TB_MT1_WARPS > 16 ? 3 : 4)
 #endif
@@ -90,13 +96,14 @@ struct Cfg {
   static constexpr int kStageBytesAll =
       kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + MT * Fmt<FMT>::kRecBytes);
   static constexpr int kFit = (225 * 1024) / (kWarps * kStageBytesAll);
-  static constexpr int kRing = MT == 1 ? TB_MT1_RING : (kFit >= 4 ? 4 : (kFit >= 2 ? kFit : 2));
+  static constexpr int kRing = FU == 1 ? TB_FUSED_RING
+                               : (MT == 1 ? TB_MT1_RING : (kFit >= 4 ? 4 : (kFit >= 2 ? kFit : 2)));
   static constexpr int kThreads = 32 * kWarps;
   // fused step: records live in a CTA-wide table after the ring, not per stage
   static constexpr int kStageBytes =
       kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + (kFused ? 0 : MT) * Fmt<FMT>::kRecBytes);
   static constexpr int kRingBytes = kWarps * kRing * kStageBytes;
-  static constexpr int kRecTabBytes = kFused ? (kMinBlocks == 2 ? 40 : 64) * 1024 : 0;  // records of all inputs
+  static constexpr int kRecTabBytes = kFused ? (kMinBlocks >= 2 ? 40 : 64) * 1024 : 0;  // records of all inputs
   static constexpr int kSmem = kRingBytes + kRecTabBytes;
   static_assert(kSmem <= 227 * 1024 - 512, "ring does not fit in shared memory");
 };
@@ -548,7 +555,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // a programmatic dependent of whatever produced the activation records);
   // the records follow once the producer has completed.
   // record groups held in registers per thread (the rest take the looped path)
-  constexpr int kMaxG = CF::kThreads >= 512 ? (FMT == TB_TL2 ? 2 : 3) : (FMT == TB_TL2 ? 3 : 4);
+  constexpr int kMaxG = CF::kThreads >= 384 ? (FMT == TB_TL2 ? 2 : 3) : (FMT == TB_TL2 ? 3 : 4);
   RegQuant<FMT, CF::kThreads, kMaxG> rq;
   if constexpr (kFused) {
     // the input loads go out first (small, L2-resident after the first CTA);
@@ -721,7 +728,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
         const uint8_t *act = kFused ? rtab + cur.c * F::kRecBytes : slot_act;
 #pragma unroll
         for (int j = 0; j < kStageChunks; ++j) {
-          const uint4 w4 = *reinterpret_cast<const uint4 *>(slot + j * kTileChunkBytes + lane * 16);
+          const uint4 w4 = load_wchunk<FMT, MT>(slot + j * kTileChunkBytes, lane);
           uint32_t sg = 0;
           if (FMT == TB_TL2)
             sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
@@ -742,7 +749,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
               load_shape();
             }
           }
-          const uint4 w4 = *reinterpret_cast<const uint4 *>(slot + j * kTileChunkBytes + lane * 16);
+          const uint4 w4 = load_wchunk<FMT, MT>(slot + j * kTileChunkBytes, lane);
           uint32_t sg = 0;
           if (FMT == TB_TL2)
             sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);

@@ -470,7 +470,14 @@ struct RegQuant {
 // decode GEMV
 // ---------------------------------------------------------------------------
 // TL1 runs as I2_S: its tiles hold the same 2-bit codes (pack.cu repack).
-template <int FMT, int MT>
+#ifndef TB_I2S_DP4A
+template <int MT>
+constexpr bool kI2sMma = MT >= 2;  // M = 1 stays on dp4a (measured faster there)
+#else
+template <int MT>
+constexpr bool kI2sMma = false;
+#endif
+template <int FMT, int MT, bool kMma = (FMT == TB_I2S && kI2sMma<MT>)>
 struct Acc {
   static_assert(FMT != TB_TL1, "TL1 tiles are decoded by the I2_S path");
   static constexpr int kSlots = Fmt<FMT>::kSlots;
@@ -497,6 +504,106 @@ struct Acc {
   }
 };
 
+// ---------------------------------------------------------------------------
+// I2_S / TL1 on the legacy int8 tensor-core path (mma.sync m16n8k32 u8 x s8).
+// The warp's 32-row x 16-byte weight chunk is read with ldmatrix.x4, so lane
+// (g = lane/4, t = lane%4) holds word t of rows g, g+8, g+16, g+24; each
+// masked code plane of a word is a 4-byte K-slice of the MMA's A fragment.
+//  - M <= 2 ("plane columns"): planes are masked without shifts (codes x 4^s,
+//    u8) and every plane gets its own D column: P0 = planes 0|1 -> columns 0|1,
+//    P1 = planes 2|3 -> columns 2|3 (token 1: columns 4..7).  B lane g holds
+//    activation word 4t + (g&3) of token g>>2 (b0 for even g, b1 for odd), so
+//    one LDS per lane feeds both MMAs; the cross terms land in columns that
+//    are never read.  4 MMAs per chunk, 16 LOPs.
+//  - M >= 4 ("token columns"): planes are shifted down to codes 0..2 and
+//    column n = token n of an 8-token block: 4 MMAs per chunk and 8 tokens.
+// The per-row result is Sum codes*a - Sum a, exact in int32 like the dp4a
+// path (4^s scaling divided out exactly at the end).  A dp4a issue slot holds
+// 128 weight MACs, an IMMA 512 (plane columns) -- the decode loop was
+// issue-bound.
+// ---------------------------------------------------------------------------
+#ifndef TB_I2S_DP4A
+#define TB_I2S_MMA 1
+template <int MT>
+struct Acc<TB_I2S, MT, true> {
+  static constexpr bool kPlaneCols = MT <= 2;
+  static constexpr int kSets = kPlaneCols ? 2 : (MT + 7) / 8;  // P0/P1 or 8-token blocks
+  int32_t d[2][kSets][4];  // [row half h][set][fragment reg]
+  int32_t csum[MT];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int q = 0; q < kSets; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) d[h][q][r] = 0;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) csum[m] = 0;
+  }
+  // Row (lane) total of token m; every lane of the warp must call it.
+  __device__ __forceinline__ int32_t total(int m) const {
+    const int lane = threadIdx.x & 31;
+    int32_t R[4];  // this lane's rows g, g+8, g+16, g+24 (of its fragment column pair)
+    int src;
+    if constexpr (kPlaneCols) {
+      const bool odd = lane & 1;  // t odd: planes 2|3 of set P1, else planes 0|1 of P0
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int32_t *e = d[h][0], *o = d[h][1];
+        const int32_t lo = odd ? (o[0] >> 4) + (o[1] >> 6) : e[0] + (e[1] >> 2);
+        const int32_t hi = odd ? (o[2] >> 4) + (o[3] >> 6) : e[2] + (e[3] >> 2);
+        R[2 * h] = lo + __shfl_xor_sync(0xffffffffu, lo, 1);
+        R[2 * h + 1] = hi + __shfl_xor_sync(0xffffffffu, hi, 1);
+      }
+      src = 4 * (lane & 7) + 2 * m;  // lane t = 2m holds token m
+    } else {
+      const int nb = m >> 3, c = m & 7, which = c & 1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        R[2 * h] = which ? d[h][nb][1] : d[h][nb][0];
+        R[2 * h + 1] = which ? d[h][nb][3] : d[h][nb][2];
+      }
+      src = 4 * (lane & 7) + (c >> 1);
+    }
+    // lane L wants row L: rows g + 8q live in R[q] of lane 4*(L%8) + t
+    int32_t out = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int32_t v = __shfl_sync(0xffffffffu, R[q], src);
+      if ((lane >> 3) == q) out = v;
+    }
+    return out - csum[m];
+  }
+};
+
+__device__ __forceinline__ uint4 ldsm_x4(const void *p) {
+  uint4 r;
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+
+__device__ __forceinline__ void imma_u8s8(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                          uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+#endif
+
+// The warp's view of one 32-row x 16-byte chunk in shared memory: lane = row
+// (dp4a paths), or the ldmatrix fragment of the tensor-core I2_S path.
+template <int FMT, int MT>
+__device__ __forceinline__ uint4 load_wchunk(const uint8_t *chunk, int lane) {
+#ifdef TB_I2S_MMA
+  if constexpr (FMT == TB_I2S && kI2sMma<MT>) return ldsm_x4(chunk + lane * 16);
+#endif
+  return *reinterpret_cast<const uint4 *>(chunk + lane * 16);
+}
+
 // One 16-byte chunk of this lane's row against MT activation records.
 template <int FMT, int MT>
 __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn,
@@ -505,14 +612,64 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
   using F = Fmt<FMT>;
   constexpr int kTokStride = kStageChunks * F::kRecBytes;  // record stride between tokens
 #ifdef TB_NO_COMPUTE  // profiling variant: data movement only
-  acc.v[0][0] += (int32_t)(w4.x ^ w4.w);
+  acc.csum[0] += (int32_t)(w4.x ^ w4.w);
   return;
+#endif
+#ifdef TB_I2S_MMA
+  if constexpr (FMT == TB_I2S && kI2sMma<MT>) {
+    using A = Acc<TB_I2S, MT>;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    if constexpr (A::kPlaneCols) {
+      const int tok = g >> 2;
+      uint32_t v = 0;
+      if (tok == 0 || tok < M)
+        v = *reinterpret_cast<const uint32_t *>(rec0 + tok * kTokStride + 4 * (4 * t + (g & 3)));
+      const uint32_t b0 = (g & 1) ? 0u : v, b1 = (g & 1) ? v : 0u;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t ra = h ? w4.z : w4.x, rb = h ? w4.w : w4.y;
+        imma_u8s8(acc.d[h][0], ra & 0x03030303u, rb & 0x03030303u, ra & 0x0C0C0C0Cu,
+                  rb & 0x0C0C0C0Cu, b0, b1);
+        imma_u8s8(acc.d[h][1], ra & 0x30303030u, rb & 0x30303030u, ra & 0xC0C0C0C0u,
+                  rb & 0xC0C0C0C0u, b0, b1);
+      }
+    } else {
+      uint4 bq[A::kSets];
+#pragma unroll
+      for (int nb = 0; nb < A::kSets; ++nb) {
+        const int tok = 8 * nb + g;
+        bq[nb] = tok < M ? *reinterpret_cast<const uint4 *>(rec0 + tok * kTokStride + 16 * t)
+                         : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t ra = h ? w4.z : w4.x, rb = h ? w4.w : w4.y;
+        const uint32_t a0 = ra & 0x03030303u, b0c = rb & 0x03030303u;
+        const uint32_t a1 = (ra >> 2) & 0x03030303u, b1c = (rb >> 2) & 0x03030303u;
+        const uint32_t a2 = (ra >> 4) & 0x03030303u, b2c = (rb >> 4) & 0x03030303u;
+        const uint32_t a3 = (ra >> 6) & 0x03030303u, b3c = (rb >> 6) & 0x03030303u;
+#pragma unroll
+        for (int nb = 0; nb < A::kSets; ++nb) {
+          imma_u8s8(acc.d[h][nb], a0, b0c, a1, b1c, bq[nb].x, bq[nb].y);
+          imma_u8s8(acc.d[h][nb], a2, b2c, a3, b3c, bq[nb].z, bq[nb].w);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+      if (m == 0 || m < M)
+        acc.csum[m] += *reinterpret_cast<const int32_t *>(rec0 + m * kTokStride + F::kActWords * 4);
+    return;
+  }
 #endif
   const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t W = w[i];
     if constexpr (FMT == TB_I2S) {
+#ifdef TB_I2S_MMA
+      if constexpr (!kI2sMma<MT>) {
+#endif
       // byte b of (W & (3 << 2s)) = code of weight 16i + 4b + s, times 4^s
       const uint32_t x0 = W & 0x03030303u, x1 = W & 0x0C0C0C0Cu;
       const uint32_t x2 = W & 0x30303030u, x3 = W & 0xC0C0C0C0u;
@@ -526,6 +683,9 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
           acc.v[m][3] = dp4a_us(x3, A.w, acc.v[m][3]);
         }
       }
+#ifdef TB_I2S_MMA
+      }
+#endif
     } else {
       // TL2 (packing.py:63-74): d = 13 + idx (sign 0) or 13 - idx (sign 1) is
       // the base-3 number of the triple's codes (c0 c1 c2).
