@@ -164,7 +164,8 @@ struct GemvBatch {
   const GemvJob *table;  // device copy, used when njobs > kMaxInlineJobs
   int njobs;
   int total;  // flat chunks over all jobs
-  int base, rem;  // warp w gets base + (w < rem) chunks
+  int base, rem;  // warp w gets unit * (base + (w < rem)) chunks (+ tail: the last warp)
+  int unit, tail;  // unit = a ring stage, so stages rarely straddle a row tile
   int defer_finalize;  // host: the caller finalises (e.g. in the next glue kernel)
   int max_entries;     // host: max over jobs of M * Npad (sizes the finalize grid)
   int fin_parts;       // device (glue): 8-CTA groups per job in the finalize rows
@@ -526,8 +527,9 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   TL_MARK(0);
   // let our programmatic dependent (finalize kernel / next step) launch early
   asm volatile("griddepcontrol.launch_dependents;");
-  const int w0 = gw * b.base + min(gw, b.rem);
-  const int n = b.base + (gw < b.rem ? 1 : 0);
+  const int w0 = b.unit * (gw * b.base + min(gw, b.rem));
+  const int n = b.unit * (b.base + (gw < b.rem ? 1 : 0)) +
+                (gw == (int)gridDim.x * CF::kWarps - 1 ? b.tail : 0);
   bool waited = false;
   __shared__ double s_scale[kMaxStepInputs];
   int s_badm = 0;  // fused: non-finite inputs (bit v), identical in every thread
@@ -863,8 +865,12 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
   const int64_t want = ceil_div(b.total, (int64_t)CF::kWarps);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count_cached(), want));
   const int nw = grid * CF::kWarps;
-  b.base = b.total / nw;
-  b.rem = b.total % nw;
+  // whole ring stages per warp: with C % 4 == 0 (I2_S / TL1 at K % 256 == 0)
+  // no stage straddles a row tile, so the main loop stays on its fast path
+  b.unit = b.total >= (int64_t)nw * kStageChunks ? kStageChunks : 1;
+  b.base = (b.total / b.unit) / nw;
+  b.rem = (b.total / b.unit) % nw;
+  b.tail = b.total % b.unit;
   if (kFused) {
     // which inputs each CTA's chunk range touches (needs the jobs on the host)
     const int all = (1 << b.in.n) - 1;
@@ -873,8 +879,9 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
       int seen = 0;
       for (int c = 0; c < grid; ++c) {
         const int64_t w0 = (int64_t)c * CF::kWarps, w1 = w0 + CF::kWarps;
-        const int64_t lo = w0 * b.base + std::min<int64_t>(w0, b.rem);
-        const int64_t hi = w1 * b.base + std::min<int64_t>(w1, b.rem);
+        const int64_t lo = b.unit * (w0 * b.base + std::min<int64_t>(w0, b.rem));
+        const int64_t hi = b.unit * (w1 * b.base + std::min<int64_t>(w1, b.rem)) +
+                           (c == grid - 1 ? b.tail : 0);
         int m = 0;
         for (int j = 0; j < b.njobs; ++j)
           if (b.jobs[j].start < hi && b.jobs[j].end > lo) m |= 1 << b.jobs[j].src;

@@ -480,7 +480,12 @@ constexpr bool kI2sMma = false;
 template <int FMT, int MT, bool kMma = (FMT == TB_I2S && kI2sMma<MT>)>
 struct Acc {
   static_assert(FMT != TB_TL1, "TL1 tiles are decoded by the I2_S path");
-  static constexpr int kSlots = Fmt<FMT>::kSlots;
+#ifndef TB_DP4A_SPLIT
+#define TB_DP4A_SPLIT 1
+#endif
+  // M = 1 I2_S: two accumulator sets (even / odd words) halve the dp4a chains
+  static constexpr int kSets = (FMT == TB_I2S && MT == 1) ? 1 + TB_DP4A_SPLIT : 1;
+  static constexpr int kSlots = Fmt<FMT>::kSlots * kSets;
   int32_t v[MT][kSlots];
   int32_t csum[MT];
   __device__ __forceinline__ void zero() {
@@ -494,7 +499,11 @@ struct Acc {
   __device__ __forceinline__ int32_t total(int m) const {
     if constexpr (FMT == TB_I2S) {
       // slot s accumulated codes * 4^s (masks without shifts): exact divisions
-      return v[m][0] + (v[m][1] >> 2) + (v[m][2] >> 4) + (v[m][3] >> 6) - csum[m];
+      int32_t r = -csum[m];
+#pragma unroll
+      for (int q = 0; q < kSets; ++q)
+        r += v[m][4 * q] + (v[m][4 * q + 1] >> 2) + (v[m][4 * q + 2] >> 4) + (v[m][4 * q + 3] >> 6);
+      return r;
     } else {
       int32_t s = -csum[m];
 #pragma unroll
@@ -677,10 +686,12 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
       for (int m = 0; m < MT; ++m) {
         if (m == 0 || m < M) {  // token 0 always exists: no branch for MT == 1
           const uint4 A = *reinterpret_cast<const uint4 *>(rec0 + m * kTokStride + 16 * i);
-          acc.v[m][0] = dp4a_us(x0, A.x, acc.v[m][0]);
-          acc.v[m][1] = dp4a_us(x1, A.y, acc.v[m][1]);
-          acc.v[m][2] = dp4a_us(x2, A.z, acc.v[m][2]);
-          acc.v[m][3] = dp4a_us(x3, A.w, acc.v[m][3]);
+          constexpr int kS = Acc<FMT, MT>::kSets;
+          const int o = kS > 1 ? 4 * (i % kS) : 0;
+          acc.v[m][o + 0] = dp4a_us(x0, A.x, acc.v[m][o + 0]);
+          acc.v[m][o + 1] = dp4a_us(x1, A.y, acc.v[m][o + 1]);
+          acc.v[m][o + 2] = dp4a_us(x2, A.z, acc.v[m][o + 2]);
+          acc.v[m][o + 3] = dp4a_us(x3, A.w, acc.v[m][o + 3]);
         }
       }
 #ifdef TB_I2S_MMA
