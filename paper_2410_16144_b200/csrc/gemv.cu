@@ -33,6 +33,7 @@
 namespace tb {
 
 constexpr int kMaxInlineJobs = 8;
+constexpr int kMaxSegs = 4;
 
 // Optional per-warp timeline (debug builds with -DTB_TIMELINE only).
 #ifdef TB_TIMELINE
@@ -164,8 +165,15 @@ struct GemvBatch {
   const GemvJob *table;  // device copy, used when njobs > kMaxInlineJobs
   int njobs;
   int total;  // flat chunks over all jobs
-  int base, rem;  // warp w gets unit * (base + (w < rem)) chunks (+ tail: the last warp)
-  int unit, tail;  // unit = a ring stage, so stages rarely straddle a row tile
+  // Warp ranges.  The flat chunk space is cut into segments (the fused step:
+  // runs of jobs contracting the same input, so no CTA has to quantise two
+  // inputs), each owning CTAs [seg_cta[s], seg_cta[s+1]) and chunks
+  // [seg_chunk[s], seg_chunk[s+1]); segment warp w gets
+  // unit * (base + (w < rem)) chunks (+ tail: its last warp).
+  int unit;  // a ring stage, so stages rarely straddle a row tile
+  int nseg;
+  int seg_cta[kMaxSegs + 1], seg_chunk[kMaxSegs + 1];
+  int seg_base[kMaxSegs], seg_rem[kMaxSegs], seg_tail[kMaxSegs];
   int defer_finalize;  // host: the caller finalises (e.g. in the next glue kernel)
   int max_entries;     // host: max over jobs of M * Npad (sizes the finalize grid)
   int fin_parts;       // device (glue): 8-CTA groups per job in the finalize rows
@@ -527,9 +535,15 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   TL_MARK(0);
   // let our programmatic dependent (finalize kernel / next step) launch early
   asm volatile("griddepcontrol.launch_dependents;");
-  const int w0 = b.unit * (gw * b.base + min(gw, b.rem));
-  const int n = b.unit * (b.base + (gw < b.rem ? 1 : 0)) +
-                (gw == (int)gridDim.x * CF::kWarps - 1 ? b.tail : 0);
+  int seg = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxSegs; ++q)
+    if (q < b.nseg && (int)blockIdx.x >= b.seg_cta[q]) seg = q;
+  const int lw = gw - b.seg_cta[seg] * CF::kWarps;  // warp within the segment
+  const int sbase = b.seg_base[seg], srem = b.seg_rem[seg];
+  const int w0 = b.seg_chunk[seg] + b.unit * (lw * sbase + min(lw, srem));
+  const int n = b.unit * (sbase + (lw < srem ? 1 : 0)) +
+                (lw == (b.seg_cta[seg + 1] - b.seg_cta[seg]) * CF::kWarps - 1 ? b.seg_tail[seg] : 0);
   bool waited = false;
   __shared__ double s_scale[kMaxStepInputs];
   int s_badm = 0;  // fused: non-finite inputs (bit v), identical in every thread
@@ -557,7 +571,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // a programmatic dependent of whatever produced the activation records);
   // the records follow once the producer has completed.
   // record groups held in registers per thread (the rest take the looped path)
-  constexpr int kMaxG = CF::kThreads >= 384 ? (FMT == TB_TL2 ? 2 : 3) : (FMT == TB_TL2 ? 3 : 4);
+  constexpr int kMaxG = FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4;
   RegQuant<FMT, CF::kThreads, kMaxG> rq;
   if constexpr (kFused) {
     // the input loads go out first (small, L2-resident after the first CTA);
@@ -734,7 +748,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
           uint32_t sg = 0;
           if (FMT == TB_TL2)
             sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
-          process_chunk<FMT, MT>(w4, sg, act + j * F::kRecBytes, M, acc);
+          process_chunk<FMT, MT>(w4, sg, act + j * F::kRecBytes, M, acc, j);
         }
         nch += kStageChunks;
         cur.c += kStageChunks;
@@ -868,9 +882,36 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
   // whole ring stages per warp: with C % 4 == 0 (I2_S / TL1 at K % 256 == 0)
   // no stage straddles a row tile, so the main loop stays on its fast path
   b.unit = b.total >= (int64_t)nw * kStageChunks ? kStageChunks : 1;
-  b.base = (b.total / b.unit) / nw;
-  b.rem = (b.total / b.unit) % nw;
-  b.tail = b.total % b.unit;
+  // segments: one per run of same-input jobs (fused step), CTAs in
+  // proportion to their chunks; otherwise one segment
+  b.nseg = 1;
+  b.seg_chunk[0] = 0;
+  if (kFused && b.table == nullptr) {
+    int ns = 0, starts[kMaxInlineJobs + 1];
+    for (int j = 0; j < b.njobs; ++j)
+      if (j == 0 || b.jobs[j].src != b.jobs[j - 1].src) starts[ns++] = b.jobs[j].start;
+    if (ns <= kMaxSegs && ns <= grid && ns > 1) {
+      b.nseg = ns;
+      for (int q = 0; q < ns; ++q) b.seg_chunk[q] = starts[q];
+    }
+  }
+  b.seg_chunk[b.nseg] = b.total;
+  {
+    int assigned = 0;
+    for (int q = 0; q < b.nseg; ++q) {
+      const int64_t nq = b.seg_chunk[q + 1] - b.seg_chunk[q];
+      int c = q + 1 == b.nseg ? grid - assigned
+                              : (int)std::llround((double)grid * nq / (double)b.total);
+      c = std::max(1, std::min(c, grid - assigned - (b.nseg - 1 - q)));
+      b.seg_cta[q] = assigned;
+      assigned += c;
+      const int64_t sw = (int64_t)c * CF::kWarps;
+      b.seg_base[q] = (int)((nq / b.unit) / sw);
+      b.seg_rem[q] = (int)((nq / b.unit) % sw);
+      b.seg_tail[q] = (int)(nq % b.unit);
+    }
+    b.seg_cta[b.nseg] = grid;
+  }
   if (kFused) {
     // which inputs each CTA's chunk range touches (needs the jobs on the host)
     const int all = (1 << b.in.n) - 1;
@@ -878,10 +919,12 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
     if (b.table == nullptr && grid <= kMaxNeedCtas) {
       int seen = 0;
       for (int c = 0; c < grid; ++c) {
-        const int64_t w0 = (int64_t)c * CF::kWarps, w1 = w0 + CF::kWarps;
-        const int64_t lo = b.unit * (w0 * b.base + std::min<int64_t>(w0, b.rem));
-        const int64_t hi = b.unit * (w1 * b.base + std::min<int64_t>(w1, b.rem)) +
-                           (c == grid - 1 ? b.tail : 0);
+        int q = 0;
+        while (q + 1 < b.nseg && c >= b.seg_cta[q + 1]) ++q;
+        const int64_t w0 = (int64_t)(c - b.seg_cta[q]) * CF::kWarps, w1 = w0 + CF::kWarps;
+        const int64_t lo = b.seg_chunk[q] + b.unit * (w0 * b.seg_base[q] + std::min<int64_t>(w0, b.seg_rem[q]));
+        const int64_t hi = b.seg_chunk[q] + b.unit * (w1 * b.seg_base[q] + std::min<int64_t>(w1, b.seg_rem[q])) +
+                           (c + 1 == b.seg_cta[q + 1] ? b.seg_tail[q] : 0);
         int m = 0;
         for (int j = 0; j < b.njobs; ++j)
           if (b.jobs[j].start < hi && b.jobs[j].end > lo) m |= 1 << b.jobs[j].src;

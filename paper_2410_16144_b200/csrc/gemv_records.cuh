@@ -471,8 +471,11 @@ struct RegQuant {
 // ---------------------------------------------------------------------------
 // TL1 runs as I2_S: its tiles hold the same 2-bit codes (pack.cu repack).
 #ifndef TB_I2S_DP4A
+#ifndef TB_MMA_M1
+#define TB_MMA_M1 0
+#endif
 template <int MT>
-constexpr bool kI2sMma = MT >= 2;  // M = 1 stays on dp4a (measured faster there)
+constexpr bool kI2sMma = MT >= 2 || TB_MMA_M1;  // M = 1 stays on dp4a (measured faster there)
 #else
 template <int MT>
 constexpr bool kI2sMma = false;
@@ -536,7 +539,8 @@ struct Acc {
 template <int MT>
 struct Acc<TB_I2S, MT, true> {
   static constexpr bool kPlaneCols = MT <= 2;
-  static constexpr int kSets = kPlaneCols ? 2 : (MT + 7) / 8;  // P0/P1 or 8-token blocks
+  // P0/P1 (twice for M = 1: even / odd chunks, shorter MMA chains) or 8-token blocks
+  static constexpr int kSets = kPlaneCols ? (MT == 1 ? 4 : 2) : (MT + 7) / 8;
   int32_t d[2][kSets][4];  // [row half h][set][fragment reg]
   int32_t csum[MT];
   __device__ __forceinline__ void zero() {
@@ -558,7 +562,12 @@ struct Acc<TB_I2S, MT, true> {
       const bool odd = lane & 1;  // t odd: planes 2|3 of set P1, else planes 0|1 of P0
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int32_t *e = d[h][0], *o = d[h][1];
+        int32_t e[4], o[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          e[r] = d[h][0][r] + (kSets == 4 ? d[h][2][r] : 0);
+          o[r] = d[h][1][r] + (kSets == 4 ? d[h][3][r] : 0);
+        }
         const int32_t lo = odd ? (o[0] >> 4) + (o[1] >> 6) : e[0] + (e[1] >> 2);
         const int32_t hi = odd ? (o[2] >> 4) + (o[3] >> 6) : e[2] + (e[3] >> 2);
         R[2 * h] = lo + __shfl_xor_sync(0xffffffffu, lo, 1);
@@ -617,7 +626,7 @@ __device__ __forceinline__ uint4 load_wchunk(const uint8_t *chunk, int lane) {
 template <int FMT, int MT>
 __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn,
                                               const uint8_t *__restrict__ rec0, int M,
-                                              Acc<FMT, MT> &acc) {
+                                              Acc<FMT, MT> &acc, int par = 0) {
   using F = Fmt<FMT>;
   constexpr int kTokStride = kStageChunks * F::kRecBytes;  // record stride between tokens
 #ifdef TB_NO_COMPUTE  // profiling variant: data movement only
@@ -637,9 +646,10 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint32_t ra = h ? w4.z : w4.x, rb = h ? w4.w : w4.y;
-        imma_u8s8(acc.d[h][0], ra & 0x03030303u, rb & 0x03030303u, ra & 0x0C0C0C0Cu,
+        const int q = A::kSets == 4 ? 2 * (par & 1) : 0;
+        imma_u8s8(acc.d[h][q], ra & 0x03030303u, rb & 0x03030303u, ra & 0x0C0C0C0Cu,
                   rb & 0x0C0C0C0Cu, b0, b1);
-        imma_u8s8(acc.d[h][1], ra & 0x30303030u, rb & 0x30303030u, ra & 0xC0C0C0C0u,
+        imma_u8s8(acc.d[h][q + 1], ra & 0x30303030u, rb & 0x30303030u, ra & 0xC0C0C0C0u,
                   rb & 0xC0C0C0C0u, b0, b1);
       }
     } else {

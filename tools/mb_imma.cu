@@ -18,6 +18,10 @@ __global__ void k(int iters, uint32_t seed, int *out) {
                      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
       } else if (OP == 1) {
         asm volatile("dp4a.u32.s32 %0, %1, %2, %0;" : "+r"(c[j][0]) : "r"(a0 + j), "r"(b0));
+      } else if (OP == 3) {
+        asm volatile("mma.sync.aligned.m16n8k64.row.col.s32.u4.s4.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                     : "+r"(c[j][0]), "+r"(c[j][1]), "+r"(c[j][2]), "+r"(c[j][3])
+                     : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
       } else {
         asm volatile("mma.sync.aligned.m16n8k16.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
                      : "+r"(c[j][0]), "+r"(c[j][1]), "+r"(c[j][2]), "+r"(c[j][3])
@@ -58,6 +62,7 @@ int main() {
     run<0>("mma m16n8k32 u8.s8", w, out);
     run<2>("mma m16n8k16 u8.s8", w, out);
     run<1>("dp4a", w, out);
+    run<3>("mma m16n8k64 u4.s4", w, out);
   }
   return 0;
 }
