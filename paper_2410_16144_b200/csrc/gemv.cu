@@ -603,9 +603,13 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     if (rq.fits()) {
 #ifndef TB_FUSED_NOQ
       TL_PMARK(1);
+#ifndef TB_FUSED_NORED
       s_badm = rq.reduce(b.in.n, s_scale, red, redb);
+#endif
       TL_PMARK(2);
+#ifndef TB_FUSED_NOREC
       rq.records(b.in.off, rtab_base);
+#endif
       TL_PMARK(3);
 #endif
     } else {

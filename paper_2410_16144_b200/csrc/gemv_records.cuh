@@ -353,54 +353,48 @@ struct RegQuant {
   float amx[4], invf[4];  // per-input absmax and 127 / absmax (after reduce)
 
   // Every thread of the CTA.  Writes s_scale[v] (thread v) and returns the
-  // non-finite mask (bit v) in every thread.
+  // non-finite mask (bit v) in every thread.  The absmax is an integer max of
+  // the |x| bit patterns: for finite floats it orders like the values, and
+  // any Inf / NaN lands at or above 0x7F800000 (the non-finite verdict).
   __device__ __forceinline__ int reduce(int n, double *s_scale,
                                         float *red /* [kThreads/32][4] */,
-                                        int *redb /* [kThreads/32] */) {
+                                        int * /* unused */) {
     constexpr int kW = kThreads / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float am[4] = {0.f, 0.f, 0.f, 0.f};
-    int badm = 0;
+    uint32_t am[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int r = 0; r < kMaxG; ++r) {
       const int g = threadIdx.x + r * kThreads;
       const int v = g < G ? vid(slot_of(g)) : 0;
-      float m = 0.f;
-      bool nf = false;
+      uint32_t m = 0u;
 #pragma unroll
       for (int u = 0; u < F::kGroup; ++u) {
         const float4 t = xr[r][u];
-        nf |= !(isfinite(t.x) && isfinite(t.y) && isfinite(t.z) && isfinite(t.w));
-        m = fmaxf(m, fmaxf(fmaxf(fabsf(t.x), fabsf(t.y)), fmaxf(fabsf(t.z), fabsf(t.w))));
+        m = max(m, max(max(__float_as_uint(t.x) & 0x7FFFFFFFu, __float_as_uint(t.y) & 0x7FFFFFFFu),
+                       max(__float_as_uint(t.z) & 0x7FFFFFFFu, __float_as_uint(t.w) & 0x7FFFFFFFu)));
       }
 #pragma unroll
       for (int vv = 0; vv < 4; ++vv)
-        if (vv == v) am[vv] = fmaxf(am[vv], m);
-      if (nf) badm |= 1 << v;
+        if (vv == v) am[vv] = max(am[vv], m);
     }
+    uint32_t *ured = reinterpret_cast<uint32_t *>(red);
 #pragma unroll
-    for (int vv = 0; vv < 4; ++vv)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) am[vv] = fmaxf(am[vv], __shfl_xor_sync(0xffffffffu, am[vv], o));
-    badm = __reduce_or_sync(0xffffffffu, badm);
-    if (lane == 0) {
-#pragma unroll
-      for (int vv = 0; vv < 4; ++vv) red[warp * 4 + vv] = am[vv];
-      redb[warp] = badm;
+    for (int vv = 0; vv < 4; ++vv) {
+      const uint32_t w = __reduce_max_sync(0xffffffffu, am[vv]);
+      if (lane == 0) ured[warp * 4 + vv] = w;
     }
     __syncthreads();
     int badmask = 0;
-#pragma unroll
-    for (int w = 0; w < kW; ++w) badmask |= redb[w];
     // per-input absmax; the scale itself (float64, core.py:128-130) is only
     // needed by thread v (output) and on the rare near-tie path
 #pragma unroll
     for (int vv = 0; vv < 4; ++vv) {
-      float a = 0.f;
+      uint32_t a = 0u;
 #pragma unroll
-      for (int w = 0; w < kW; ++w) a = fmaxf(a, red[w * 4 + vv]);
-      amx[vv] = a;
-      invf[vv] = a > 0.f ? 127.0f / a : 1.0f;  // within 2^-24 of 1/s: quantize_fast's bound
+      for (int w = 0; w < kW; ++w) a = max(a, ured[w * 4 + vv]);
+      if (a >= 0x7F800000u) badmask |= 1 << vv;
+      amx[vv] = __uint_as_float(a);
+      invf[vv] = a > 0u ? 127.0f / amx[vv] : 1.0f;  // within 2^-24 of 1/s: quantize_fast's bound
     }
 #pragma unroll
     for (int vv = 0; vv < 4; ++vv)
@@ -410,8 +404,13 @@ struct RegQuant {
   }
 
   // Records of this thread's groups from the registers (after reduce()).
+  // q = x * (127 / amax) is rounded by ONE fma with 1.5 * 2^23 (its low
+  // mantissa byte is rint(q) in two's complement, |q| <= 127); a second fma
+  // gives the exact rounding residue, and elements within 4e-5 of a .5 tie
+  // are redone in float64 (core.py:24-27, 128-130).
   __device__ __forceinline__ void records(const int *offs, uint8_t *rtab) {
     const int lane = threadIdx.x & 31;
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
 #pragma unroll
     for (int r = 0; r < kMaxG; ++r) {
       const int gw = (threadIdx.x - lane) + r * kThreads;  // warp-uniform
@@ -431,15 +430,15 @@ struct RegQuant {
         for (int u = 0; u < F::kGroup; ++u) {
           const float4 t = xr[r][u];
           const float e[4] = {t.x, t.y, t.z, t.w};
-          uint32_t wd = 0;
+          uint32_t tb[4];
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
-            const float q = e[b] * inv;
-            const float rq = rintf(q);
-            if (!(fabsf(q - rq) < 0.49996f)) tie |= 1u << (4 * u + b);
-            wd |= ((uint32_t)static_cast<int>(rq) & 0xFFu) << (8 * b);
+            const float m = __fmaf_rn(e[b], inv, kMagic);
+            const float d = __fmaf_rn(e[b], inv, -(m - kMagic));  // q - rint(q)
+            if (!(fabsf(d) < 0.49996f)) tie |= 1u << (4 * u + b);
+            tb[b] = __float_as_uint(m);
           }
-          words[u] = wd;
+          words[u] = prmt(prmt(tb[0], tb[1], 0x0040u), prmt(tb[2], tb[3], 0x0040u), 0x5410u);
         }
         if (tie) {  // rare: redo the flagged elements in float64 (exact at ties)
           const double s = am > 0.f ? static_cast<double>(am) / 127.0 : 1.0;
