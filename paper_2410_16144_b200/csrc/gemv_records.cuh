@@ -425,7 +425,7 @@ struct RegQuant {
         for (int vv = 1; vv < 4; ++vv)
           if (vv == v) inv = invf[vv], am = amx[vv];
         uint32_t words[F::kGroup];
-        uint32_t tie = 0;  // bit 4u+b: element within 4e-5 of a rounding tie
+        bool near = false;  // some element within 4e-5 of a rounding tie
 #pragma unroll
         for (int u = 0; u < F::kGroup; ++u) {
           const float4 t = xr[r][u];
@@ -434,11 +434,24 @@ struct RegQuant {
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const float m = __fmaf_rn(e[b], inv, kMagic);
-            const float d = __fmaf_rn(e[b], inv, -(m - kMagic));  // q - rint(q)
-            if (!(fabsf(d) < 0.49996f)) tie |= 1u << (4 * u + b);
+            const float d = __fmaf_rn(e[b], inv, kMagic - m);  // q - rint(q)
+            near |= !(fabsf(d) < 0.49996f);
             tb[b] = __float_as_uint(m);
           }
           words[u] = prmt(prmt(tb[0], tb[1], 0x0040u), prmt(tb[2], tb[3], 0x0040u), 0x5410u);
+        }
+        uint32_t tie = 0;  // bit 4u+b: element within 4e-5 of a rounding tie
+        if (near) {
+#pragma unroll
+          for (int u = 0; u < F::kGroup; ++u) {
+            const float4 t = xr[r][u];
+            const float e[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const float m = __fmaf_rn(e[b], inv, kMagic);
+              if (!(fabsf(__fmaf_rn(e[b], inv, kMagic - m)) < 0.49996f)) tie |= 1u << (4 * u + b);
+            }
+          }
         }
         if (tie) {  // rare: redo the flagged elements in float64 (exact at ties)
           const double s = am > 0.f ? static_cast<double>(am) / 127.0 : 1.0;
