@@ -34,6 +34,11 @@ namespace tb {
 
 constexpr int kMaxInlineJobs = 8;
 constexpr int kMaxSegs = 4;
+constexpr int kMaxStepCluster = 4;  // fused step: CTAs sharing one quantisation
+#ifndef TB_STEP_CLUSTER
+#define TB_STEP_CLUSTER 2
+#endif
+constexpr int kStepCQ = TB_STEP_CLUSTER;
 
 // Optional per-warp timeline (debug builds with -DTB_TIMELINE only).
 #ifdef TB_TIMELINE
@@ -517,7 +522,7 @@ struct IssueState {
   }
 };
 
-template <int FMT, int MT, int FU>
+template <int FMT, int MT, int FU, int CQ = 1>  // CQ: cluster size of the fused step
 __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::kMinBlocks)
     tgemv_kernel(const __grid_constant__ GemvBatch b) {
   using F = Fmt<FMT>;
@@ -571,14 +576,19 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // a programmatic dependent of whatever produced the activation records);
   // the records follow once the producer has completed.
   // record groups held in registers per thread (the rest take the looped path)
-  constexpr int kMaxG = FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4;
+  constexpr int kMaxG = CQ >= 2 ? 2 : (FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4);
   RegQuant<FMT, CF::kThreads, kMaxG> rq;
   if constexpr (kFused) {
     // the input loads go out first (small, L2-resident after the first CTA);
     // then the weight prefetch; the loaded values are consumed after both
     const int need = blockIdx.x < kMaxNeedCtas ? b.in.need[blockIdx.x] : 0xF;
+    // thread-block cluster (launch attribute): its Q CTAs quantise disjoint
+    // slices of the inputs (same `need`) and share records through DSMEM
+    constexpr int cq = CQ;
+    const int crank = CQ > 1 ? (int)cluster_rank() : 0;
+    if (cq > 1) cluster_arrive_relaxed();
 #ifndef TB_FUSED_NOLOAD  // profiling variants: TB_FUSED_NOLOAD / TB_FUSED_NOQ
-    if (!b.in.x_after_wait) rq.load(b.in.x, b.in.K, b.in.C, b.in.n, need);
+    if (!b.in.x_after_wait) rq.load(b.in.x, b.in.K, b.in.C, b.in.n, need, crank, cq);
 #else
     rq.G = 0;
 #endif
@@ -595,24 +605,30 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     if (b.in.x_after_wait) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       waited = true;
-      rq.load(b.in.x, b.in.K, b.in.C, b.in.n, need);
+      rq.load(b.in.x, b.in.K, b.in.C, b.in.n, need, crank, cq);
     }
     // quantise every input vector into this CTA's record tables
     __shared__ float red[CF::kWarps * 4];
-    __shared__ int redb[CF::kWarps];
+    __shared__ uint32_t cl_amax[kMaxStepCluster * 4];
     if (rq.fits()) {
 #ifndef TB_FUSED_NOQ
       TL_PMARK(1);
 #ifndef TB_FUSED_NORED
-      s_badm = rq.reduce(b.in.n, s_scale, red, redb);
+      s_badm = rq.reduce(b.in.n, s_scale, red, cl_amax, crank, cq);
 #endif
       TL_PMARK(2);
 #ifndef TB_FUSED_NOREC
-      rq.records(b.in.off, rtab_base);
+      rq.records(b.in.off, rtab_base, cq);
 #endif
       TL_PMARK(3);
 #endif
+      if (cq > 1) cluster_sync();  // every rank's records are in every table
     } else {
+      if (cq > 1) {  // each rank quantises everything itself; keep the barrier count
+        cluster_wait();
+        cluster_sync();
+        cluster_sync();
+      }
       s_badm = 0;
       for (int v = 0; v < b.in.n; ++v) {  // large inputs: one loop per vector
         bool bad;
@@ -876,6 +892,10 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
     if (cudaFuncSetAttribute(tgemv_kernel<FMT, MT, FU>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, CF::kSmem) != cudaSuccess)
       return TB_ERR_CUDA;
+    if (kFused && cudaFuncSetAttribute(tgemv_kernel<FMT, MT, FU, kStepCQ>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       CF::kSmem) != cudaSuccess)
+      return TB_ERR_CUDA;
     configured_dev = dev;
   }
   // spread over every SM (latency-bound sizes want the parallelism), one CTA
@@ -900,13 +920,16 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
     }
   }
   b.seg_chunk[b.nseg] = b.total;
+  // fused step: clusters of Q CTAs share the quantisation (segments in whole clusters)
+  int Q = 1;
+  if (kFused && kStepCQ > 1 && grid % kStepCQ == 0 && grid >= kStepCQ * b.nseg) Q = kStepCQ;
   {
     int assigned = 0;
     for (int q = 0; q < b.nseg; ++q) {
       const int64_t nq = b.seg_chunk[q + 1] - b.seg_chunk[q];
       int c = q + 1 == b.nseg ? grid - assigned
-                              : (int)std::llround((double)grid * nq / (double)b.total);
-      c = std::max(1, std::min(c, grid - assigned - (b.nseg - 1 - q)));
+                              : Q * (int)std::llround((double)grid * nq / (double)b.total / Q);
+      c = std::max(Q, std::min(c, grid - assigned - Q * (b.nseg - 1 - q)));
       b.seg_cta[q] = assigned;
       assigned += c;
       const int64_t sw = (int64_t)c * CF::kWarps;
@@ -938,6 +961,11 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
         seen |= m;
       }
       b.in.need[0] |= (uint8_t)(all & ~seen);  // unused inputs: CTA 0 still publishes a scale
+      for (int c0 = 0; c0 < grid; c0 += Q) {  // one quantisation per cluster: the union
+        int m = 0;
+        for (int c = c0; c < c0 + Q; ++c) m |= b.in.need[c];
+        for (int c = c0; c < c0 + Q; ++c) b.in.need[c] = (uint8_t)m;
+      }
     } else {
       for (int c = 0; c < kMaxNeedCtas; ++c) b.in.need[c] = (uint8_t)all;
     }
@@ -949,12 +977,17 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
   cfg.blockDim = dim3(CF::kThreads);
   cfg.dynamicSmemBytes = kFused ? CF::kRingBytes + rec_tab_bytes : CF::kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = Q;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, tgemv_kernel<FMT, MT, FU>, b) != cudaSuccess)
+  cfg.numAttrs = Q > 1 ? 2 : 1;
+  if (cudaLaunchKernelEx(&cfg, Q > 1 ? tgemv_kernel<FMT, MT, FU, kStepCQ> : tgemv_kernel<FMT, MT, FU>,
+                         b) != cudaSuccess)
     return TB_ERR_CUDA;
   return (kFused || b.defer_finalize) ? TB_OK : launch_finalize(b, s);
 }

@@ -24,9 +24,48 @@ struct Fmt {
 //   word kActWords = sum of the chunk's activations
 // One thread per (token, chunk, group i); the 4 group threads are adjacent lanes.
 // ---------------------------------------------------------------------------
+// Distributed shared memory (thread-block clusters): the fused step's CTAs
+// of one cluster quantise disjoint slices of the inputs and write every
+// record into all ranks' tables.
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// split barrier: every rank arrives at entry and waits before its first
+// DSMEM store, so no CTA writes into a peer that has not started yet
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
 template <int FMT>
 __device__ __forceinline__ void write_group(uint8_t *rec_chunk, int i, const uint32_t (&r)[Fmt<FMT>::kGroup],
-                                            int32_t gsum, bool on) {
+                                            int32_t gsum, bool on, int Q = 1) {
   using F = Fmt<FMT>;
   // chunk sum over the 4 adjacent group lanes (all 32 lanes shuffle)
   gsum += __shfl_xor_sync(0xffffffffu, gsum, 1);
@@ -34,6 +73,7 @@ __device__ __forceinline__ void write_group(uint8_t *rec_chunk, int i, const uin
   if (!on) return;
   uint32_t *dst = reinterpret_cast<uint32_t *>(rec_chunk) + i * F::kGroup;
   if constexpr (FMT == TB_TL2) {
+    uint32_t wv[6];
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       uint32_t word = 0;
@@ -42,7 +82,17 @@ __device__ __forceinline__ void write_group(uint8_t *rec_chunk, int i, const uin
         const int b = 6 * j + s;
         word |= ((r[b >> 2] >> (8 * (b & 3))) & 0xFFu) << (8 * j);
       }
-      dst[s] = word;
+      wv[s] = word;
+    }
+    if (Q == 1) {
+#pragma unroll
+      for (int s = 0; s < 6; ++s) dst[s] = wv[s];
+    } else {
+      for (int p = 0; p < Q; ++p) {
+        const uint32_t a = mapa_rank(smem_u32(dst), p);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) st_cluster_u32(a + 4 * s, wv[s]);
+      }
     }
   } else {  // 4x4 byte transpose
     const uint32_t t0 = prmt(r[0], r[1], 0x5140u), t1 = prmt(r[0], r[1], 0x7362u);
@@ -52,9 +102,22 @@ __device__ __forceinline__ void write_group(uint8_t *rec_chunk, int i, const uin
     o.y = prmt(t0, t2, 0x7632u);
     o.z = prmt(t1, t3, 0x5410u);
     o.w = prmt(t1, t3, 0x7632u);
-    reinterpret_cast<uint4 *>(dst)[0] = o;
+    if (Q == 1) {
+      reinterpret_cast<uint4 *>(dst)[0] = o;
+    } else {
+      for (int p = 0; p < Q; ++p) st_cluster_v4(mapa_rank(smem_u32(dst), p), o);
+    }
   }
-  if (i == 0) *reinterpret_cast<int4 *>(rec_chunk + F::kActWords * 4) = make_int4(gsum, 0, 0, 0);
+  if (i == 0) {
+    const int4 sv = make_int4(gsum, 0, 0, 0);
+    int4 *sp = reinterpret_cast<int4 *>(rec_chunk + F::kActWords * 4);
+    if (Q == 1) {
+      *sp = sv;
+    } else {
+      for (int p = 0; p < Q; ++p)
+        st_cluster_v4(mapa_rank(smem_u32(sp), p), make_uint4((uint32_t)gsum, 0u, 0u, 0u));
+    }
+  }
 }
 
 template <int FMT>
@@ -292,6 +355,7 @@ struct RegQuant {
   // they occupy compact slots 0.. in input order; vmap holds slot -> input.
   int gb1, gb2, gb3;  // first global group of slots 1..3 (INT_MAX past the last)
   int G;
+  int lo, hi, per;  // this CTA's groups [lo, hi) of the G (cluster rank r of Q: per each)
   int vmap;
   const float *const *xs_;
 
@@ -300,10 +364,11 @@ struct RegQuant {
     return c == 0 ? 0 : (c == 1 ? gb1 : (c == 2 ? gb2 : gb3));
   }
   __device__ __forceinline__ int vid(int c) const { return (vmap >> (4 * c)) & 15; }
-  __device__ __forceinline__ bool fits() const { return G <= kMaxG * kThreads; }
+  // every rank of a cluster decides alike (per is rank-independent)
+  __device__ __forceinline__ bool fits() const { return per <= kMaxG * kThreads; }
 
   __device__ __forceinline__ void load(const float *const *xs, const int *Ks, const int *Cs, int n,
-                                       int need) {
+                                       int need, int rank = 0, int Q = 1) {
     int acc = 0, gbv[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff}, ns = 0;
     vmap = 0;
 #pragma unroll
@@ -320,11 +385,15 @@ struct RegQuant {
     gb1 = gbv[1], gb2 = gbv[2], gb3 = gbv[3];
     G = acc;
     xs_ = xs;
+    // whole chunks (4 groups) per rank: a chunk's sum is a 4-lane shuffle
+    per = (((G + Q - 1) / Q) + 3) & ~3;
+    lo = min(G, rank * per);
+    hi = min(G, lo + per);
     if (!fits()) return;
 #pragma unroll
     for (int r = 0; r < kMaxG; ++r) {
-      const int g = threadIdx.x + r * kThreads;
-      const int c = g < G ? slot_of(g) : 0;
+      const int g = lo + threadIdx.x + r * kThreads;
+      const int c = g < hi ? slot_of(g) : 0;
       const int v = vid(c);
       const int local = g - base_of(c);
       const int k0 = (local >> 2) * F::kWeights + (local & 3) * 4 * F::kGroup;
@@ -335,7 +404,7 @@ struct RegQuant {
       for (int u = 0; u < F::kGroup; ++u) {
         const int kv = k0 + 4 * u;
         float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (g < G) {
+        if (g < hi) {
           if (vec && kv + 3 < K) {
             t = __ldg(reinterpret_cast<const float4 *>(x + kv));
           } else {
@@ -356,16 +425,18 @@ struct RegQuant {
   // non-finite mask (bit v) in every thread.  The absmax is an integer max of
   // the |x| bit patterns: for finite floats it orders like the values, and
   // any Inf / NaN lands at or above 0x7F800000 (the non-finite verdict).
+  // Q > 1: the CTA's partial maxima go to every rank's cl[rank][v] (DSMEM)
+  // and the cluster barrier makes the full absmax visible everywhere.
   __device__ __forceinline__ int reduce(int n, double *s_scale,
                                         float *red /* [kThreads/32][4] */,
-                                        int * /* unused */) {
+                                        uint32_t *cl /* [Q][4] */, int rank, int Q) {
     constexpr int kW = kThreads / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t am[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int r = 0; r < kMaxG; ++r) {
-      const int g = threadIdx.x + r * kThreads;
-      const int v = g < G ? vid(slot_of(g)) : 0;
+      const int g = lo + threadIdx.x + r * kThreads;
+      const int v = g < hi ? vid(slot_of(g)) : 0;
       uint32_t m = 0u;
 #pragma unroll
       for (int u = 0; u < F::kGroup; ++u) {
@@ -384,14 +455,29 @@ struct RegQuant {
       if (lane == 0) ured[warp * 4 + vv] = w;
     }
     __syncthreads();
+    if (Q > 1) {
+      cluster_wait();  // pairs with the entry arrive: every peer is running
+      if (threadIdx.x < 4) {
+        uint32_t a = 0u;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) a = max(a, ured[w * 4 + threadIdx.x]);
+        const uint32_t dst = smem_u32(cl + rank * 4 + threadIdx.x);
+        for (int p = 0; p < Q; ++p) st_cluster_u32(mapa_rank(dst, p), a);
+      }
+      cluster_sync();
+    }
     int badmask = 0;
     // per-input absmax; the scale itself (float64, core.py:128-130) is only
     // needed by thread v (output) and on the rare near-tie path
 #pragma unroll
     for (int vv = 0; vv < 4; ++vv) {
       uint32_t a = 0u;
+      if (Q > 1) {
+        for (int p = 0; p < Q; ++p) a = max(a, cl[p * 4 + vv]);
+      } else {
 #pragma unroll
-      for (int w = 0; w < kW; ++w) a = max(a, ured[w * 4 + vv]);
+        for (int w = 0; w < kW; ++w) a = max(a, ured[w * 4 + vv]);
+      }
       if (a >= 0x7F800000u) badmask |= 1 << vv;
       amx[vv] = __uint_as_float(a);
       invf[vv] = a > 0u ? 127.0f / amx[vv] : 1.0f;  // within 2^-24 of 1/s: quantize_fast's bound
@@ -408,15 +494,16 @@ struct RegQuant {
   // mantissa byte is rint(q) in two's complement, |q| <= 127); a second fma
   // gives the exact rounding residue, and elements within 4e-5 of a .5 tie
   // are redone in float64 (core.py:24-27, 128-130).
-  __device__ __forceinline__ void records(const int *offs, uint8_t *rtab) {
+  // Q > 1: every record goes to the same offset in all Q ranks' tables.
+  __device__ __forceinline__ void records(const int *offs, uint8_t *rtab, int Q = 1) {
     const int lane = threadIdx.x & 31;
     constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
 #pragma unroll
     for (int r = 0; r < kMaxG; ++r) {
-      const int gw = (threadIdx.x - lane) + r * kThreads;  // warp-uniform
-      if (gw < G) {
+      const int gw = lo + (threadIdx.x - lane) + r * kThreads;  // warp-uniform
+      if (gw < hi) {
         const int g = gw + lane;
-        const bool on = g < G;
+        const bool on = g < hi;
         const int c = on ? slot_of(g) : 0;
         const int v = vid(c);
         const int local = on ? g - base_of(c) : 0;
@@ -472,7 +559,7 @@ struct RegQuant {
         int32_t gs = 0;
 #pragma unroll
         for (int u = 0; u < F::kGroup; ++u) gs = __dp4a((int)words[u], 0x01010101, gs);
-        write_group<FMT>(rtab + offs[v] + (local >> 2) * F::kRecBytes, local & 3, words, gs, on);
+        write_group<FMT>(rtab + offs[v] + (local >> 2) * F::kRecBytes, local & 3, words, gs, on, Q);
       }
     }
   }
