@@ -81,20 +81,21 @@ struct Cfg {
 #define TB_MT1_WARPS 16
 #endif
 #ifndef TB_FUSED_WARPS
-#define TB_FUSED_WARPS 8
+#define TB_FUSED_WARPS 6
 #endif
-  // fused step: 8 warps and <= ~110 KB so two CTAs fit on an SM -- the next
-  // step's CTAs (programmatic dependent launch) quantise and prefetch while
-  // this step's CTAs stream
-  static constexpr int kWarps = FU == 1 ? TB_FUSED_WARPS
-                                       : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
 #ifndef TB_FUSED_MINB
-#define TB_FUSED_MINB 2
+#define TB_FUSED_MINB 3
 #endif
 #ifndef TB_FUSED_RING
 #define TB_FUSED_RING 4
 #endif
-  static constexpr int kMinBlocks = (FU == 1 && TB_FUSED_WARPS <= 16) ? TB_FUSED_MINB : 1;
+  // fused step: small CTAs (I2_S / TL1: 6 warps, <= ~75 KB, three per SM;
+  // TL2, whose decode needs more registers: 8 warps, two per SM) -- the next
+  // steps' CTAs (programmatic dependent launch) quantise and prefetch while
+  // this step's CTAs stream
+  static constexpr int kWarps = FU == 1 ? (FMT == TB_TL2 ? 8 : TB_FUSED_WARPS)
+                                       : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
+  static constexpr int kMinBlocks = FU == 1 ? (FMT == TB_TL2 ? 2 : TB_FUSED_MINB) : 1;
 #ifndef TB_MT1_RING
 #define TB_MT1_RING (TB_MT1_WARPS > 16 ? 3 : 4)
 #endif
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // a programmatic dependent of whatever produced the activation records);
   // the records follow once the producer has completed.
   // record groups held in registers per thread (the rest take the looped path)
-  constexpr int kMaxG = CQ >= 2 ? 2 : (FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4);
+  constexpr int kMaxG = CQ >= 2 ? (CF::kThreads <= 192 ? 3 : 2) : (FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4);
   RegQuant<FMT, CF::kThreads, kMaxG> rq;
   if constexpr (kFused) {
     // the input loads go out first (small, L2-resident after the first CTA);
@@ -1052,7 +1053,7 @@ static int launch_batch(int fmt, GemvBatch &b, int maxM, cudaStream_t s) {
 static int launch_step(int fmt, GemvBatch &b, int rec_tab_bytes, bool isolated, cudaStream_t s) {
   // two 8-warp CTAs per SM (chained steps overlap) when the record tables
   // allow it; one 16-warp CTA per SM for big tables or an isolated launch
-  const bool small = !isolated && rec_tab_bytes <= Cfg<TB_I2S, 1, 1>::kRecTabBytes;
+  const bool small = !isolated && rec_tab_bytes <= Cfg<TB_I2S, 1, 1>::kRecTabBytes;  // 40 KB
   if (fmt == TB_I2S || fmt == TB_TL1)  // TL1 tiles hold I2_S codes
     return small ? launch_tgemv<TB_I2S, 1, 1>(b, s, rec_tab_bytes)
                  : launch_tgemv<TB_I2S, 1, 2>(b, s, rec_tab_bytes);
