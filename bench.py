@@ -411,12 +411,39 @@ def run_gpu(args, rank, world):
     }
 
     # ---- e2e through the public API with host buffers: every step copies its
-    #      two pinned f32 input vectors in, runs, and reads the three fp32
-    #      output vectors back (synchronously) before the next step
+    #      two f32 input vectors in from pinned host memory, runs, and copies
+    #      its three fp32 output vectors back to pinned host memory
     if rank == 0 and not args.no_e2e and tp == 1:
         n_e2e = max(10, min(args.steps, 200))
         xh_h = torch.randn(NX, H).pin_memory()
         xi_h = torch.randn(NX, I).pin_memory()
+        # (a) the serving form: n_e2e independent steps in one HostPipeline
+        #     run (H2D / step kernels / D2H overlapped on three streams), the
+        #     weights rotating over the NCOPY copies as in `value`
+        pipe = tb.HostPipeline([[(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)]
+                                for pl in plans], [H, I], steps=n_e2e)
+        for i in range(n_e2e):
+            pipe.inputs[0][i].copy_(xh_h[i % NX])
+            pipe.inputs[1][i].copy_(xi_h[i % NX])
+        for _ in range(3):
+            pipe.run()
+        reps = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            pipe.run()
+            reps.append(time.perf_counter() - t0)
+        e2e_s = sorted(reps)[len(reps) // 2] / n_e2e
+        result["e2e"] = {"value": round(1.0 / e2e_s, 2), "unit": "tokens/s",
+                         "h2d_bytes_per_step": (H + I) * 4,
+                         "d2h_bytes_per_step": (2 * I + H) * 4,
+                         "steps": n_e2e,
+                         "path": "tb.HostPipeline.run(): per step, pinned host f32 inputs -> H2D "
+                                 "copy -> fused step kernel (PDL chain) -> D2H copy of the fp32 "
+                                 "outputs to pinned host memory; copies and kernels on three "
+                                 "streams in one CUDA graph; wall clock incl. the final sync "
+                                 "(median of 5 runs)"}
+
+        # (b) one token at a time, synchronous (latency-bound): HostStep
         hosts = [tb.HostStep([(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)], [H, I])
                  for pl in plans]
 
@@ -428,14 +455,11 @@ def run_gpu(args, rank, world):
         t0 = time.perf_counter()
         for i in range(n_e2e):
             e2e_step(i)
-        e2e_s = (time.perf_counter() - t0) / n_e2e
-        result["e2e"] = {"value": round(1.0 / e2e_s, 2), "unit": "tokens/s",
-                         "h2d_bytes_per_step": (H + I) * 4,
-                         "d2h_bytes_per_step": (2 * I + H) * 4,
-                         "steps": n_e2e,
-                         "path": "tb.HostStep: host f32 inputs -> pinned staging -> one CUDA graph "
-                                 "(H2D, fused step kernel, finalize, D2H) -> fp32 outputs on the "
-                                 "host, stream sync per token"}
+        sync_s = (time.perf_counter() - t0) / n_e2e
+        result["e2e_sync"] = {"value": round(1.0 / sync_s, 2), "unit": "tokens/s",
+                              "us_per_token": round(sync_s * 1e6, 2), "steps": n_e2e,
+                              "path": "tb.HostStep: one token per call (H2D, fused step, "
+                                      "finalize into mapped pinned memory, stream sync)"}
 
         # the reference-shaped per-call API (quantize_activations + gemv_parallel
         # per projection, float64 GemvResult.output to host)

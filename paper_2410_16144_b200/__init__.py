@@ -25,6 +25,7 @@ from .kernels import (
     GemvPlan,
     GemvStep,
     HostStep,
+    HostPipeline,
     StepGlue,
     KernelKind,
     gemm_prefill,

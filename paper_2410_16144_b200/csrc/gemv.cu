@@ -158,6 +158,7 @@ struct StepInputs {
   int K[kMaxStepInputs], C[kMaxStepInputs], off[kMaxStepInputs];  // off: record table offset
   int n;
   int x_after_wait;      // inputs produced by the preceding grid: read them after the wait
+  int sticky_flags;      // store the non-finite flag only when set
   const GemvJob *prev;   // device job table finalised after this launch's own work
   int prev_njobs;
   int prev_inline;       // 1: prev jobs are in fin[] below
@@ -827,7 +828,8 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     if (threadIdx.x < b.in.n && b.in.writer[threadIdx.x] == (int)blockIdx.x) {
       *b.in.scale[threadIdx.x] = s_scale[threadIdx.x];
       // plain store (this launch's verdict): the flag may live in mapped host memory
-      if (b.in.flag[threadIdx.x]) *b.in.flag[threadIdx.x] = (s_badm >> threadIdx.x) & 1;
+      const int bad = (s_badm >> threadIdx.x) & 1;
+      if (b.in.flag[threadIdx.x] && (bad || !b.in.sticky_flags)) *b.in.flag[threadIdx.x] = bad;
     }
     if (b.in.prev_inline) {
 #ifndef TB_NO_PREVFIN  // profiling variant: skip the previous step's finalize
@@ -1263,6 +1265,7 @@ extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t nj
   if (off > 64 * 1024) return TB_ERR_UNSUPPORTED;  // (and <= the kernel's table, checked at launch)
   b.in.n = (int)ninputs;
   b.in.x_after_wait = (x_after_wait & TB_STEP_X_AFTER_WAIT) ? 1 : 0;
+  b.in.sticky_flags = (x_after_wait & TB_STEP_STICKY_FLAGS) ? 1 : 0;
   const bool isolated = (x_after_wait & TB_STEP_ISOLATED) != 0;
   b.in.prev = static_cast<const GemvJob *>(prev_table_device);
   b.in.prev_njobs = (int)prev_njobs;

@@ -397,7 +397,7 @@ class GemvStep:
     """
 
     def __init__(self, pairs, input_k, x_after_wait: bool = False, flags=None,
-                 isolated: bool = False):
+                 isolated: bool = False, sticky_flags: bool = False):
         import ctypes as C
         import numpy as np
 
@@ -446,7 +446,8 @@ class GemvStep:
         self.njobs, self.total, self.max_entries = len(pairs), total.value, maxe.value
         self.x_after_wait = bool(x_after_wait)
         # isolated: launched one at a time (e.g. HostStep), not as a chain
-        self._launch_flags = (1 if x_after_wait else 0) | (2 if isolated else 0)
+        self._launch_flags = ((1 if x_after_wait else 0) | (2 if isolated else 0)
+                              | (4 if sticky_flags else 0))
         self.inputs = (L.StepInput * len(input_k))()
         for i, k in enumerate(self.input_k):
             self.inputs[i].K = k
@@ -566,6 +567,135 @@ class HostStep:
         if self._flags_np.any():
             raise ValueError("activations must be finite")  # core.py:116-134
         return self.out_host
+
+
+class HostPipeline:
+    """Independent decode steps streamed between pinned HOST memory and the
+    device: ``run()`` copies every step's float32 inputs in, runs the fused
+    step chain and copies every step's outputs back.  The copies go in blocks
+    of ``block`` steps on two copy streams, so a block's host-to-device copy
+    and the previous block's device-to-host copy overlap the step kernels,
+    and the kernels stay one programmatic-dependent-launch chain (a cross-
+    stream wait only at block starts).  This is the serving form over a queue
+    of independent requests; HostStep is the one-token synchronous form.
+
+    ``slot_pairs`` holds R >= 2 lists of (GemvPlan, input index) pairs; step
+    i uses list i % R (the same plans may repeat: every slot gets its own
+    workspace, only the weights are shared).  ``steps`` steps are captured
+    into one CUDA graph.  Fill ``inputs[v]`` (pinned, [steps, K_v]) and read
+    ``outputs[j]`` (pinned, [steps, N_j]) for the j-th pair of the slot
+    lists.  Non-finite inputs raise ValueError like quantize_activations
+    (core.py:116-134).
+    """
+
+    def __init__(self, slot_pairs, input_k, steps: int, block: int = 16, _copies=(True, True)):
+        import types
+
+        self._copies = _copies  # profiling only: (host-to-device, device-to-host)
+        R = len(slot_pairs)
+        if R < 2:
+            raise ValueError("a pipeline needs at least two slots")
+        if steps < 1 or block < 1:
+            raise ValueError("steps and block must be >= 1")
+        npairs = len(slot_pairs[0])
+        rows = [plan.p.rows for plan, _ in slot_pairs[0]]
+        if any(len(sp) != npairs or [plan.p.rows for plan, _ in sp] != rows for sp in slot_pairs):
+            raise ValueError("every slot must hold the same projections")
+        dev = slot_pairs[0][0][0].main.device
+        self.input_k = [int(k) for k in input_k]
+        self.steps, self.block = steps, block
+        offs, n = [], 0
+        for k in self.input_k:
+            offs.append(n)
+            n += -(-k // 4) * 4  # 16-byte aligned vectors
+        ooffs, nout = [], 0
+        for r_ in rows:
+            ooffs.append(nout)
+            nout += -(-r_ // 4) * 4
+        self.x_host = torch.zeros((steps, n), dtype=torch.float32).pin_memory()
+        self.inputs = [self.x_host[:, o:o + k] for o, k in zip(offs, self.input_k)]
+        self._out_host = torch.empty((steps, nout), dtype=torch.float32).pin_memory()
+        self.outputs = [self._out_host[:, o:o + r_] for o, r_ in zip(ooffs, rows)]
+        self._x_dev = torch.empty((steps, n), dtype=torch.float32, device=dev)
+        self._o_dev = torch.empty((steps, nout), dtype=torch.float32, device=dev)
+        # non-finite verdicts, sticky and zero-copy in mapped pinned memory
+        self._flags = torch.zeros((R, len(self.input_k)), dtype=torch.int32).pin_memory()
+        self._flags_np = self._flags.numpy()
+        self._ws = [[torch.zeros_like(plan.ws) for plan, _ in sp] for sp in slot_pairs]
+        self._steps = []
+        for i in range(steps):
+            r = i % R
+            pairs = []
+            for (plan, v), ws, oo in zip(slot_pairs[r], self._ws[r], ooffs):
+                o = self._o_dev[i:i + 1, oo:oo + plan.p.rows]
+                pairs.append((types.SimpleNamespace(p=plan.p, main=plan.main, sign=plan.sign,
+                                                    ws=ws, acc=None, out32=o, out64=None), v))
+            st = GemvStep(pairs, self.input_k, flags=self._flags[r], sticky_flags=True)
+            st.bind([self._x_dev[i, o:o + k] for o, k in zip(offs, self.input_k)])
+            self._steps.append(st)
+        self._graph = self._capture()
+
+    def _record(self):
+        T, B = self.steps, self.block
+        comp = torch.cuda.current_stream()
+        h2d, d2h = self._h2d, self._d2h
+        blocks = [(b0, min(T, b0 + B)) for b0 in range(0, T, B)]
+        in_ev = [torch.cuda.Event() for _ in blocks]
+        done_ev = [torch.cuda.Event() for _ in blocks]
+        start = torch.cuda.Event()
+        start.record(comp)
+        h2d.wait_event(start)
+        d2h.wait_event(start)
+        with torch.cuda.stream(h2d):
+            for b, (b0, b1) in enumerate(blocks):
+                if self._copies[0]:
+                    self._x_dev[b0:b1].copy_(self.x_host[b0:b1], non_blocking=True)
+                in_ev[b].record(h2d)
+
+        def copy_out(b):  # block b is final once the next block's first kernel finalised it
+            done_ev[b].record(comp)
+            d2h.wait_event(done_ev[b])
+            b0, b1 = blocks[b]
+            with torch.cuda.stream(d2h):
+                if self._copies[1]:
+                    self._out_host[b0:b1].copy_(self._o_dev[b0:b1], non_blocking=True)
+
+        for b, (b0, b1) in enumerate(blocks):
+            comp.wait_event(in_ev[b])
+            for i in range(b0, b1):
+                self._steps[i].run(prev=self._steps[i - 1] if i else None)
+                if i == b0 and b:
+                    copy_out(b - 1)
+        self._steps[T - 1].finalize()
+        copy_out(len(blocks) - 1)
+        comp.wait_stream(h2d)
+        comp.wait_stream(d2h)
+
+    def _capture(self):
+        s = torch.cuda.Stream()
+        self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self._record()  # warm-up (kernel attributes) outside the capture
+        s.synchronize()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self._record()
+        torch.cuda.synchronize()
+        self._stream = s
+        return g
+
+    def run(self):
+        """All ``steps`` steps: inputs from ``inputs``, results in ``outputs``."""
+        self._flags_np[...] = 0
+        with torch.cuda.stream(self._stream):
+            self._graph.replay()
+        self._stream.synchronize()
+        if self._flags_np.any():
+            raise ValueError("activations must be finite")  # core.py:116-134
+        return self.outputs
 
 
 class ActRecords:

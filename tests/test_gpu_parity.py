@@ -561,6 +561,37 @@ def test_host_step(tb):
         hs([bad, x1])
 
 
+def test_host_pipeline(tb):
+    """Independent steps streamed host -> device -> host on three streams."""
+    rng = np.random.default_rng(37)
+    v0 = rng.integers(-1, 2, size=(200, 640), dtype=np.int8)
+    v1 = rng.integers(-1, 2, size=(64, 300), dtype=np.int8)
+    v2 = rng.integers(-1, 2, size=(96, 640), dtype=np.int8)
+    mats = [tb.TernaryMatrix(200, 640, v0, 0.25), tb.TernaryMatrix(64, 300, v1, 0.5),
+            tb.TernaryMatrix(96, 640, v2, 0.125)]
+    plans = [tb.GemvPlan(tb.encode_tl1(m)) for m in mats]
+    pairs = [(plans[0], 0), (plans[1], 1), (plans[2], 0)]
+    T = 7
+    pipe = tb.HostPipeline([pairs, pairs, pairs], [640, 300], steps=T)
+    for trial in range(2):
+        xs0 = rng.standard_normal((T, 640)).astype(np.float32)
+        xs1 = rng.standard_normal((T, 300)).astype(np.float32)
+        pipe.inputs[0].copy_(torch.from_numpy(xs0))
+        pipe.inputs[1].copy_(torch.from_numpy(xs1))
+        outs = pipe.run()
+        for i in range(T):
+            (q0, s0, _), (q1, s1, _) = O.quantize(xs0[i], 1), O.quantize(xs1[i], 1)
+            for j, (vals, ws, q, s_) in enumerate(((v0, 0.25, q0, s0), (v1, 0.5, q1, s1),
+                                                   (v2, 0.125, q0, s0))):
+                want = (O.gemv_ref_int32(vals, q).astype(np.float64) * ws * s_).astype(np.float32)
+                np.testing.assert_array_equal(outs[j][i].numpy(), want, err_msg=f"{trial} {i} {j}")
+    pipe.inputs[1][4, 7] = float("nan")
+    with pytest.raises(ValueError, match="activations must be finite"):
+        pipe.run()
+    pipe.inputs[1][4, 7] = 0.0
+    pipe.run()  # the verdict is per run
+
+
 def test_fused_step_nonfinite_flag(tb):
     v = np.ones((40, 64), dtype=np.int8)
     plan = tb.GemvPlan(tb.encode_tl1(tb.TernaryMatrix(40, 64, v, 1.0)), out_dtype=torch.float64)
