@@ -1,0 +1,48 @@
+"""A few token passes of a small layer stack, for one ncu capture of its kernels.
+
+    ncu --set full -k regex:tgemv_kernel --launch-skip 4 --launch-count 1 \
+        python tools/ncu_stack.py cfg4 i2s 8 2
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2410_16144_b200 import _lib as L  # noqa: E402
+
+if os.environ.get("TB_LIB"):
+    L.load(os.environ["TB_LIB"])
+
+from paper_2410_16144_b200.stack import STACKS, LayerStack  # noqa: E402
+
+
+def main():
+    name, fmt, M, layers = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
+    st = LayerStack(STACKS[name], fmt, tokens=M, layers=layers)
+    h, i = STACKS[name]["hidden"], STACKS[name]["inter"]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    if M == 1:
+        xh = [torch.randn(h, generator=g, device="cuda") for _ in range(layers)]
+        xi = [torch.randn(i, generator=g, device="cuda") for _ in range(layers)]
+        pool = None
+    else:
+        xh = [torch.randn(M, h, generator=g, device="cuda") for _ in range(layers)]
+        xi = [torch.randn(M, i, generator=g, device="cuda") for _ in range(layers)]
+        pool = st.make_glues(xh, xi)
+    for _ in range(4):
+        st.token_pass(xh, xi, pool)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        st.token_pass(xh, xi, pool)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{name} {fmt} M={M} layers={layers}: {e0.elapsed_time(e1) / 5 / layers * 1e3:.1f} us/layer "
+          f"({st.algo_bytes / layers / 1e6:.1f} MB/layer)")
+
+
+if __name__ == "__main__":
+    main()
