@@ -348,6 +348,69 @@ __device__ __forceinline__ void glue_quant(const QuantVec &Q, int m) {
                                     Q.scale, Q.C, Q.rec, Q.flag, m, blockIdx.x, gridDim.x);
 }
 
+// The glue's finalize: every job's M x Npad entries as ONE flat space in
+// units of 4 (Npad is a multiple of 32, so a unit never straddles a job or a
+// token row); int4 workspace loads, kGlueIlp units in flight per thread, and
+// only as many CTAs as that needs (a few hundred, not one per 256 entries).
+constexpr int kMaxGlueFin = 16;
+constexpr int kGlueIlp = 4;
+__device__ __forceinline__ void glue_finalize_flat(const GemvBatch &b, int part, int nparts) {
+  __shared__ FinJob fj[kMaxGlueFin];
+  __shared__ int64_t pre[kMaxGlueFin + 1];
+  if ((int)threadIdx.x < b.njobs) {
+    const GemvJob J = job_at(b, threadIdx.x);
+    fj[threadIdx.x] = FinJob{J.ws_acc, J.acc_out, J.out64, J.out32, J.a_scale, J.w_scale,
+                             J.N, J.Npad, J.M};
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    pre[0] = 0;
+    for (int j = 0; j < b.njobs; ++j) pre[j + 1] = pre[j] + (int64_t)fj[j].M * fj[j].Npad;
+  }
+  __syncthreads();
+  const int64_t units = pre[b.njobs] >> 2;
+  const int64_t stride = (int64_t)nparts * blockDim.x;
+  for (int64_t u0 = (int64_t)part * blockDim.x + threadIdx.x; u0 < units; u0 += stride * kGlueIlp) {
+    int4 v[kGlueIlp];
+    int jj[kGlueIlp];
+    int64_t kk[kGlueIlp];
+#pragma unroll
+    for (int q = 0; q < kGlueIlp; ++q) {  // all loads first
+      const int64_t u = u0 + q * stride;
+      jj[q] = -1;
+      if (u < units) {
+        const int64_t e = u << 2;
+        int j = 0;
+        while (j + 1 < b.njobs && pre[j + 1] <= e) ++j;
+        jj[q] = j;
+        kk[q] = e - pre[j];
+        int4 *ws = reinterpret_cast<int4 *>(fj[j].ws_acc + kk[q]);
+        v[q] = __ldcg(ws);
+        __stcg(ws, make_int4(0, 0, 0, 0));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kGlueIlp; ++q) {
+      if (jj[q] < 0) continue;
+      const FinJob &J = fj[jj[q]];
+      const int m = (int)(kk[q] / J.Npad), row0 = (int)(kk[q] - (int64_t)m * J.Npad);
+      const double as = (J.out64 || J.out32) ? __ldg(J.a_scale + m) : 0.0;
+      const int32_t a[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int row = row0 + e;
+        if (row < J.N) {
+          const int64_t o = (int64_t)m * J.N + row;
+          if (J.acc_out) J.acc_out[o] = a[e];
+          const double y = static_cast<double>(a[e]) * J.w_scale * as;  // core.py:99-101
+          if (J.out64) J.out64[o] = y;
+          if (J.out32) J.out32[o] = static_cast<float>(y);
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueParams g) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   // the next GEMV group may launch now: its prologue prefetches weights (no
@@ -362,6 +425,9 @@ __global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueP
     }
     if (g.q[v].fmt == TB_TL2) glue_quant<TB_TL2>(g.q[v], m);
     else glue_quant<TB_I2S>(g.q[v], m);  // I2_S and TL1 share the record layout
+  } else if (g.fin.njobs <= kMaxGlueFin) {
+    const int r = y - g.q_tokens;  // finalize rows: flat over every job's entries
+    glue_finalize_flat(g.fin, r * gridDim.x + blockIdx.x, g.fin.fin_parts * gridDim.x);
   } else {
     const int r = y - g.q_tokens;  // (job, group) of 8 CTAs: one element per thread
     const int j = r / g.fin.fin_parts, part = r - j * g.fin.fin_parts;
@@ -1340,9 +1406,19 @@ extern "C" int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
     tokens += Q.M;
   }
   g.q_tokens = tokens;
-  // finalize rows: 8 CTAs x 256 threads per group, one accumulator per thread
-  g.fin.fin_parts = fin_njobs > 0 ? (int)ceil_div(fin_max_entries, (int64_t)8 * 256) : 0;
-  const int64_t rows64 = tokens + fin_njobs * g.fin.fin_parts;
+  // finalize rows: flat over all jobs (units of 4 entries, kGlueIlp units per
+  // thread) when the table is small enough to stage; else 8-CTA groups per job
+  int64_t fin_rows = 0;
+  if (fin_njobs > kMaxGlueFin) {
+    g.fin.fin_parts = fin_njobs > 0 ? (int)ceil_div(fin_max_entries, (int64_t)8 * 256) : 0;
+    fin_rows = fin_njobs * g.fin.fin_parts;
+  } else if (fin_njobs > 0) {
+    // the caller passes the largest job's entries; bound the total by njobs x that
+    const int64_t units = fin_njobs * fin_max_entries / 4;
+    g.fin.fin_parts = (int)std::max<int64_t>(1, ceil_div(units, (int64_t)8 * 256 * kGlueIlp));
+    fin_rows = g.fin.fin_parts;
+  }
+  const int64_t rows64 = tokens + fin_rows;
   if (rows64 > 65535) return TB_ERR_ARGUMENT;
   const int rows = (int)rows64;
   if (rows == 0) return TB_OK;

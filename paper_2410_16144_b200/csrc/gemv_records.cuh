@@ -641,7 +641,11 @@ struct Acc<TB_I2S, MT, true> {
   // P0/P1 (twice for M = 1: even / odd chunks, shorter MMA chains) or 8-token blocks
   static constexpr int kSets = kPlaneCols ? (MT == 1 ? 4 : 2) : (MT + 7) / 8;
   int32_t d[2][kSets][4];  // [row half h][set][fragment reg]
-  int32_t csum[MT];
+  // Activation sums of this lane's own fragment columns only (plane columns:
+  // token t/2; token columns: tokens 8nb + 2t, 8nb + 2t + 1); total() fetches
+  // a token's sum from the lane that holds it.
+  static constexpr int kCs = kPlaneCols ? 1 : 2 * kSets;
+  int32_t csum[kCs];
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int h = 0; h < 2; ++h)
@@ -650,14 +654,16 @@ struct Acc<TB_I2S, MT, true> {
 #pragma unroll
         for (int r = 0; r < 4; ++r) d[h][q][r] = 0;
 #pragma unroll
-    for (int m = 0; m < MT; ++m) csum[m] = 0;
+    for (int m = 0; m < kCs; ++m) csum[m] = 0;
   }
   // Row (lane) total of token m; every lane of the warp must call it.
   __device__ __forceinline__ int32_t total(int m) const {
     const int lane = threadIdx.x & 31;
     int32_t R[4];  // this lane's rows g, g+8, g+16, g+24 (of its fragment column pair)
     int src;
+    int32_t cs;  // token m's activation sum, valid in lane src
     if constexpr (kPlaneCols) {
+      cs = csum[0];
       const bool odd = lane & 1;  // t odd: planes 2|3 of set P1, else planes 0|1 of P0
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -675,6 +681,10 @@ struct Acc<TB_I2S, MT, true> {
       src = 4 * (lane & 7) + 2 * m;  // lane t = 2m holds token m
     } else {
       const int nb = m >> 3, c = m & 7, which = c & 1;
+      cs = csum[0];
+#pragma unroll
+      for (int q = 1; q < kCs; ++q)
+        if (q == 2 * nb + which) cs = csum[q];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         R[2 * h] = which ? d[h][nb][1] : d[h][nb][0];
@@ -689,7 +699,7 @@ struct Acc<TB_I2S, MT, true> {
       const int32_t v = __shfl_sync(0xffffffffu, R[q], src);
       if ((lane >> 3) == q) out = v;
     }
-    return out - csum[m];
+    return out - __shfl_sync(0xffffffffu, cs, src);
   }
 };
 
@@ -773,10 +783,18 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
         }
       }
     }
+    if constexpr (A::kPlaneCols) {
+      const int tok = t >> 1;
+      if (tok == 0 || tok < M)
+        acc.csum[0] += *reinterpret_cast<const int32_t *>(rec0 + tok * kTokStride + F::kActWords * 4);
+    } else {
 #pragma unroll
-    for (int m = 0; m < MT; ++m)
-      if (m == 0 || m < M)
-        acc.csum[m] += *reinterpret_cast<const int32_t *>(rec0 + m * kTokStride + F::kActWords * 4);
+      for (int q = 0; q < A::kCs; ++q) {
+        const int tok = 8 * (q >> 1) + 2 * t + (q & 1);
+        if (tok < M)
+          acc.csum[q] += *reinterpret_cast<const int32_t *>(rec0 + tok * kTokStride + F::kActWords * 4);
+      }
+    }
     return;
   }
 #endif
