@@ -46,7 +46,11 @@ constexpr int kTimelineWarps = 148 * 32;
 __device__ unsigned long long g_timeline[kTimelineWarps][5];
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
+#ifdef TB_TL_CLOCK  // SM clock cycles (per-warp deltas only; SMs are not in sync)
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+#else
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+#endif
   return t;
 }
 #define TL_MARK(i)                                                    \
@@ -608,6 +612,24 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   TL_MARK(0);
   // let our programmatic dependent (finalize kernel / next step) launch early
   asm volatile("griddepcontrol.launch_dependents;");
+  // Fused step: the input loads go out first -- they depend on nothing but the
+  // CTA's input mask, while the warp-range and job lookups below are chains of
+  // constant-bank loads that are cold at launch (~1.4 us measured before the
+  // loads were issued when they came after them).
+  constexpr int kMaxG = CQ >= 2 ? (CF::kThreads <= 192 ? 3 : 2) : (FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4);
+  RegQuant<FMT, CF::kThreads, kMaxG> rq;
+  constexpr int cq = CQ;
+  int crank = 0, need = 0;
+  if constexpr (kFused) {
+    need = blockIdx.x < kMaxNeedCtas ? b.in.need[blockIdx.x] : 0xF;
+    crank = CQ > 1 ? (int)cluster_rank() : 0;
+    if (cq > 1) cluster_arrive_relaxed();
+#ifndef TB_FUSED_NOLOAD  // profiling variants: TB_FUSED_NOLOAD / TB_FUSED_NOQ
+    if (!b.in.x_after_wait) rq.load(b.in.x, b.in.K, b.in.C, b.in.n, need, crank, cq);
+#else
+    rq.G = 0;
+#endif
+  }
   int seg = 0;
 #pragma unroll
   for (int q = 1; q < kMaxSegs; ++q)
@@ -632,7 +654,13 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   Cursor cur{0, 0, 0};
   IssueState is;  // issue cursor + cached job pointers (identical in every lane)
   if (n > 0) {
-    while (cur.j + 1 < b.njobs && job_at(b, cur.j + 1).start <= w0) ++cur.j;
+    if (b.table) {
+      while (cur.j + 1 < b.njobs && job_at(b, cur.j + 1).start <= w0) ++cur.j;
+    } else {  // inline jobs: independent constant loads, no dependent chain
+#pragma unroll
+      for (int j = 1; j < kMaxInlineJobs; ++j)
+        if (j < b.njobs && b.jobs[j].start <= w0) cur.j = j;
+    }
     GemvJob J = job_at(b, cur.j);
     const int local = w0 - J.start;
     cur.t = local / J.C;
@@ -644,21 +672,13 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // a programmatic dependent of whatever produced the activation records);
   // the records follow once the producer has completed.
   // record groups held in registers per thread (the rest take the looped path)
-  constexpr int kMaxG = CQ >= 2 ? (CF::kThreads <= 192 ? 3 : 2) : (FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4);
-  RegQuant<FMT, CF::kThreads, kMaxG> rq;
   if constexpr (kFused) {
-    // the input loads go out first (small, L2-resident after the first CTA);
-    // then the weight prefetch; the loaded values are consumed after both
-    const int need = blockIdx.x < kMaxNeedCtas ? b.in.need[blockIdx.x] : 0xF;
-    // thread-block cluster (launch attribute): its Q CTAs quantise disjoint
-    // slices of the inputs (same `need`) and share records through DSMEM
-    constexpr int cq = CQ;
-    const int crank = CQ > 1 ? (int)cluster_rank() : 0;
-    if (cq > 1) cluster_arrive_relaxed();
-#ifndef TB_FUSED_NOLOAD  // profiling variants: TB_FUSED_NOLOAD / TB_FUSED_NOQ
-    if (!b.in.x_after_wait) rq.load(b.in.x, b.in.K, b.in.C, b.in.n, need, crank, cq);
-#else
-    rq.G = 0;
+    // (the input loads went out at entry; now the weight prefetch; the loaded
+    // values are consumed after both.)  Thread-block cluster (launch
+    // attribute): its Q CTAs quantise disjoint slices of the inputs (same
+    // `need`) and share records through DSMEM.
+#ifdef TB_TL_PM1_EARLY
+    TL_PMARK(1);
 #endif
 #ifndef TB_PRE_STAGES
 #define TB_PRE_STAGES kRing
@@ -680,7 +700,9 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     __shared__ uint32_t cl_amax[kMaxStepCluster * 4];
     if (rq.fits()) {
 #ifndef TB_FUSED_NOQ
+#ifndef TB_TL_PM1_EARLY
       TL_PMARK(1);
+#endif
 #ifndef TB_FUSED_NORED
       s_badm = rq.reduce(b.in.n, s_scale, red, cl_amax, crank, cq);
 #endif

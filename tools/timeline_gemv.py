@@ -33,9 +33,10 @@ def main():
     ap.add_argument("--rows", type=int, default=14336)
     ap.add_argument("--cols", type=int, default=4096)
     ap.add_argument("--step", action="store_true")
+    ap.add_argument("--chain", type=int, default=0, help="--step: marks of the last of N chained steps")
     a = ap.parse_args()
     if a.step:
-        return step_timeline()
+        return step_timeline(a.chain)
     enc = {"i2s": tb.encode_i2s, "tl1": tb.encode_tl1, "tl2": tb.encode_tl2}[a.fmt]
     g = torch.Generator(device="cuda").manual_seed(0)
     plans = []
@@ -70,7 +71,10 @@ def report(name):
     lib.tb_timeline_fetch(buf.ctypes.data_as(C.c_void_p), buf.nbytes)
     used = buf[:, 0] > 0
     t = buf[used].astype(np.int64)
-    rel = (t - t[:, 0].min()) / 1000.0
+    if os.environ.get("TL_CLOCK"):  # per-warp clock64 deltas since its own entry, in k-cycles
+        rel = (t - t[:, :1]) / 1000.0
+    else:
+        rel = (t - t[:, 0].min()) / 1000.0
     print(f"{name}: {used.sum()} warps; us since first entry  (min / p50 / p90 / max)")
     for k, nm in enumerate(["entry", "prologue", "first data", "compute done", "flushed"]):
         col = rel[:, k]
@@ -78,7 +82,7 @@ def report(name):
               f"{np.quantile(col, 0.9):7.2f} {col.max():7.2f}")
 
 
-def step_timeline():
+def step_timeline(chain=0):
     H, I = 4096, 14336
     g = torch.Generator(device="cuda").manual_seed(0)
     steps = []
@@ -94,6 +98,19 @@ def step_timeline():
     for i in range(8):
         steps[i % 4].run([xh, xi], prev=steps[(i - 1) % 4])
     torch.cuda.synchronize()
+    if chain:
+        for trial in range(3):
+            lib.tb_timeline_clear()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(chain):
+                steps[i % 4].run([xh, xi], prev=steps[(i - 1) % 4])
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"chain of {chain}: {e0.elapsed_time(e1) * 1e3 / chain:.2f} us/step (eager launches)")
+            report(f"last step of the chain, trial {trial}")
+        return
     for trial in range(3):
         lib.tb_timeline_clear()
         torch.cuda.synchronize()
