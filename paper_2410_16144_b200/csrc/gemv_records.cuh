@@ -369,6 +369,18 @@ struct RegQuant {
 
   __device__ __forceinline__ void load(const float *const *xs, const int *Ks, const int *Cs, int n,
                                        int need, int rank = 0, int Q = 1) {
+    // Every parameter at a fixed offset, loaded up front: kernel parameters are
+    // cold in the constant cache at each launch, so a chain of dependent
+    // (indexed) constant loads costs one L2 round trip per link (measured
+    // ~1.4 us before the first input load went out).
+    const float *xv[4];
+    int Kv[4], Cv[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      xv[v] = xs[v];
+      Kv[v] = Ks[v];
+      Cv[v] = Cs[v];
+    }
     int acc = 0, gbv[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff}, ns = 0;
     vmap = 0;
 #pragma unroll
@@ -379,7 +391,7 @@ struct RegQuant {
           if (c == ns) gbv[c] = acc;
         vmap |= v << (4 * ns);
         ++ns;
-        acc += 4 * Cs[v];
+        acc += 4 * Cv[v];
       }
     }
     gb1 = gbv[1], gb2 = gbv[2], gb3 = gbv[3];
@@ -397,8 +409,11 @@ struct RegQuant {
       const int v = vid(c);
       const int local = g - base_of(c);
       const int k0 = (local >> 2) * F::kWeights + (local & 3) * 4 * F::kGroup;
-      const float *x = xs[v];
-      const int K = Ks[v];
+      const float *x = xv[0];
+      int K = Kv[0];
+#pragma unroll
+      for (int vv = 1; vv < 4; ++vv)
+        if (v == vv) x = xv[vv], K = Kv[vv];
       const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
 #pragma unroll
       for (int u = 0; u < F::kGroup; ++u) {
