@@ -371,7 +371,12 @@ def run_gpu(args, rank, world):
     g2.replay()
     e1.record()
     torch.cuda.synchronize()
-    gemv_ms = e0.elapsed_time(e1) / R
+    chain_ms = e0.elapsed_time(e1) / R
+    # tp1: the timed region IS the step kernel chain (K step launches + one
+    # trailing finalize), so the kernel's average launch duration over the
+    # timed region is ms_per_step (conservative: the finalize is included);
+    # the 24-launch chain above is reported beside it
+    gemv_ms = ms_per_step if tp == 1 else chain_ms
     for pl in plans:  # finalise what is pending (resets the workspaces)
         if tp == 1:
             pl["step"].finalize()
@@ -405,6 +410,10 @@ def run_gpu(args, rank, world):
                                 "gate/up (14336x4096) + down (4096x14336) + previous finalize")
                                if tp == 1 else "tgemv_kernel<TL1,1> grouped gate+up+down",
                      "bytes_per_launch": gemv_bytes, "launch_us": round(gemv_ms * 1e3, 3),
+                     "launch_us_source": ("timed region / K step launches (incl. the one trailing "
+                                          "finalize)" if tp == 1 else
+                                          f"{R}-launch graph of the grouped GEMV alone"),
+                     "launch_us_chain24": round(chain_ms * 1e3, 3),
                      "peak_kind": f"{peak_kind} hbm_gbs (copy)"},
         "gpu_launches": launches_per_step * args.steps + (1 if tp == 1 else 0),
         "clocks": clk.summary(),
