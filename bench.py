@@ -429,9 +429,12 @@ def run_gpu(args, rank, world):
         # (a) the serving form: n_e2e independent steps in one HostPipeline
         #     run (H2D / step kernels / D2H overlapped on three streams), the
         #     weights rotating over the NCOPY copies as in `value`
+        # 400 steps per run: the first block's copy in and the last block's
+        # copy back (not hidden behind kernels) amortise over the run
+        n_pipe = 400
         pipe = tb.HostPipeline([[(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)]
-                                for pl in plans], [H, I], steps=n_e2e)
-        for i in range(n_e2e):
+                                for pl in plans], [H, I], steps=n_pipe)
+        for i in range(n_pipe):
             pipe.inputs[0][i].copy_(xh_h[i % NX])
             pipe.inputs[1][i].copy_(xi_h[i % NX])
         for _ in range(3):
@@ -441,11 +444,11 @@ def run_gpu(args, rank, world):
             t0 = time.perf_counter()
             pipe.run()
             reps.append(time.perf_counter() - t0)
-        e2e_s = sorted(reps)[len(reps) // 2] / n_e2e
+        e2e_s = sorted(reps)[len(reps) // 2] / n_pipe
         result["e2e"] = {"value": round(1.0 / e2e_s, 2), "unit": "tokens/s",
                          "h2d_bytes_per_step": (H + I) * 4,
                          "d2h_bytes_per_step": (2 * I + H) * 4,
-                         "steps": n_e2e,
+                         "steps": n_pipe,
                          "path": "tb.HostPipeline.run(): per step, pinned host f32 inputs -> H2D "
                                  "copy -> fused step kernel (PDL chain) -> D2H copy of the fp32 "
                                  "outputs to pinned host memory; copies and kernels on three "

@@ -24,12 +24,13 @@ def main():
             pl[name] = tb.GemvPlan(tb.encode_tl1(tb.ternarize_weights(w, rows, cols)))
         plans.append(pl)
     slots = [[(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)] for pl in plans]
-    for T, blk, copies in ((100, 8, (True, True)),
-                           (100, 4, (True, True)), (100, 16, (True, True)),
-                           (100, 25, (True, True)), (200, 8, (True, True))):
+    for T, blk, copies in ((100, 16, (True, True)), (100, 16, (False, False)),
+                           (100, 16, (True, False)), (100, 16, (False, True)),
+                           (100, 100, (True, True)), (200, 16, (True, True)), (400, 16, (True, True))):
         pipe = tb.HostPipeline(slots, [H, I], steps=T, block=blk, _copies=copies)
         pipe.inputs[0].normal_()
         pipe.inputs[1].normal_()
+        pipe._x_dev.normal_()  # copies off: the device inputs stay finite
         for _ in range(3):
             pipe.run()
         reps = []
