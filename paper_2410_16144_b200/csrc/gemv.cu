@@ -85,18 +85,18 @@ struct Cfg {
 #define TB_MT1_WARPS 16
 #endif
 #ifndef TB_FUSED_WARPS
-#define TB_FUSED_WARPS 6
+#define TB_FUSED_WARPS 5
 #endif
 #ifndef TB_FUSED_MINB
-#define TB_FUSED_MINB 3
+#define TB_FUSED_MINB 4
 #endif
 #ifndef TB_FUSED_RING
-#define TB_FUSED_RING 4
+#define TB_FUSED_RING 3
 #endif
-  // fused step: small CTAs (I2_S / TL1: 6 warps, <= ~75 KB, three per SM;
-  // TL2, whose decode needs more registers: 8 warps, two per SM) -- the next
-  // steps' CTAs (programmatic dependent launch) quantise and prefetch while
-  // this step's CTAs stream
+  // fused step: small CTAs (I2_S / TL1: 5 warps with 3-stage rings, <= ~55 KB,
+  // four per SM; TL2, whose decode needs more registers: 8 warps, two per SM)
+  // -- the next steps' CTAs (programmatic dependent launch) quantise and
+  // prefetch while this step's CTAs stream
   static constexpr int kWarps = FU == 1 ? (FMT == TB_TL2 ? 8 : TB_FUSED_WARPS)
                                        : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
   static constexpr int kMinBlocks = FU == 1 ? (FMT == TB_TL2 ? 2 : TB_FUSED_MINB) : 1;
@@ -107,7 +107,7 @@ struct Cfg {
   static constexpr int kStageBytesAll =
       kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + MT * Fmt<FMT>::kRecBytes);
   static constexpr int kFit = (225 * 1024) / (kWarps * kStageBytesAll);
-  static constexpr int kRing = FU == 1 ? TB_FUSED_RING
+  static constexpr int kRing = FU == 1 ? (FMT == TB_TL2 ? 4 : TB_FUSED_RING)
                                : (MT == 1 ? TB_MT1_RING : (kFit >= 4 ? 4 : (kFit >= 2 ? kFit : 2)));
   static constexpr int kThreads = 32 * kWarps;
   // fused step: records live in a CTA-wide table after the ring, not per stage
