@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // CTA's input mask, while the warp-range and job lookups below are chains of
   // constant-bank loads that are cold at launch (~1.4 us measured before the
   // loads were issued when they came after them).
-  constexpr int kMaxG = CQ >= 2 ? (CF::kThreads <= 192 ? 3 : 2) : (FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4);
+  constexpr int kMaxG = CQ >= 2 ? (CF::kThreads <= 128 ? 4 : CF::kThreads <= 192 ? 3 : 2) : (FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4);
   RegQuant<FMT, CF::kThreads, kMaxG> rq;
   constexpr int cq = CQ;
   int crank = 0, need = 0;
