@@ -760,26 +760,33 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // entry of the flat (job, row) space (one per thread when the grid covers
   // it) -- the loads complete while the warp keeps streaming -- and the
   // stores happen at the end, so no load latency sits in the CTA's tail.
-  int fin_j = -1;
-  int64_t fin_k = 0;
-  int32_t fin_v = 0;
-  double fin_as = 0.0;
+  // Two entries per thread (a 148 x 160-thread grid covers 23,680 of the
+  // cfg1 step's 32,768): both read-and-resets go out together at the wait.
+  constexpr int kFinPer = 2;
+  int fin_j[kFinPer] = {-1, -1};
+  int64_t fin_k[kFinPer] = {0, 0};
+  int32_t fin_v[kFinPer] = {0, 0};
+  double fin_as[kFinPer] = {0.0, 0.0};
   auto fin_load = [&]() {
     if constexpr (kFused) {
       if (!b.in.prev_inline) return;
-      int64_t k = (int64_t)gw * 32 + lane;
-      for (int j = 0; j < b.in.prev_njobs; ++j) {
-        const FinJob &J = b.in.fin[j];
-        const int64_t n = (int64_t)J.M * J.Npad;
-        if (k < n) {
-          fin_j = j;
-          fin_k = k;
-          fin_v = atomicExch(J.ws_acc + k, 0);  // read and reset in one L2 operation
-          const int m = (int)(k / J.Npad);
-          fin_as = J.a_scale ? __ldcg(J.a_scale + m) : 0.0;
-          return;
+      const int64_t nthreads = (int64_t)gridDim.x * CF::kThreads;
+#pragma unroll
+      for (int e = 0; e < kFinPer; ++e) {
+        int64_t k = (int64_t)gw * 32 + lane + e * nthreads;
+        for (int j = 0; j < b.in.prev_njobs; ++j) {
+          const FinJob &J = b.in.fin[j];
+          const int64_t n = (int64_t)J.M * J.Npad;
+          if (k < n) {
+            fin_j[e] = j;
+            fin_k[e] = k;
+            fin_v[e] = atomicExch(J.ws_acc + k, 0);  // read and reset in one L2 operation
+            const int m = (int)(k / J.Npad);
+            fin_as[e] = J.a_scale ? __ldcg(J.a_scale + m) : 0.0;
+            break;
+          }
+          k -= n;
         }
-        k -= n;
       }
     }
   };
@@ -921,23 +928,25 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     }
     if (b.in.prev_inline) {
 #ifndef TB_NO_PREVFIN  // profiling variant: skip the previous step's finalize
-      if (fin_j >= 0) {  // the entry read (and reset) at the wait: output store only
-        const FinJob &J = b.in.fin[fin_j];
-        const int m = (int)(fin_k / J.Npad), row = (int)(fin_k - (int64_t)m * J.Npad);
+#pragma unroll
+      for (int e = 0; e < kFinPer; ++e) {
+        if (fin_j[e] < 0) continue;  // the entries read (and reset) at the wait: stores only
+        const FinJob &J = b.in.fin[fin_j[e]];
+        const int m = (int)(fin_k[e] / J.Npad), row = (int)(fin_k[e] - (int64_t)m * J.Npad);
         if (row < J.N) {
           const int64_t o = (int64_t)m * J.N + row;
-          if (J.acc_out) J.acc_out[o] = fin_v;
-          const double y = static_cast<double>(fin_v) * J.w_scale * fin_as;  // core.py:99-101
+          if (J.acc_out) J.acc_out[o] = fin_v[e];
+          const double y = static_cast<double>(fin_v[e]) * J.w_scale * fin_as[e];  // core.py:99-101
           if (J.out64) J.out64[o] = y;
           if (J.out32) J.out32[o] = static_cast<float>(y);
         }
       }
-      // entries beyond one per thread of the grid (large previous steps)
+      // entries beyond kFinPer per thread of the grid (large previous steps)
       const int64_t nthreads = (int64_t)gridDim.x * CF::kThreads;
       int64_t total = 0;
       for (int j = 0; j < b.in.prev_njobs; ++j) total += (int64_t)b.in.fin[j].M * b.in.fin[j].Npad;
-      if (total > nthreads) {
-        finalize_fin_range(b.in.fin, b.in.prev_njobs, nthreads + (int64_t)gw * 32 + lane,
+      if (total > kFinPer * nthreads) {
+        finalize_fin_range(b.in.fin, b.in.prev_njobs, kFinPer * nthreads + (int64_t)gw * 32 + lane,
                            nthreads);
       }
 #endif
