@@ -109,13 +109,16 @@ __device__ __forceinline__ void write_group(uint8_t *rec_chunk, int i, const uin
     }
   }
   if (i == 0) {
-    const int4 sv = make_int4(gsum, 0, 0, 0);
+    // the sum in all four tail words: readers of different tokens pick
+    // different words (token records 320 B apart put every even token's
+    // tail in the same bank; one word each would be a 4-way conflict)
+    const int4 sv = make_int4(gsum, gsum, gsum, gsum);
     int4 *sp = reinterpret_cast<int4 *>(rec_chunk + F::kActWords * 4);
     if (Q == 1) {
       *sp = sv;
     } else {
-      for (int p = 0; p < Q; ++p)
-        st_cluster_v4(mapa_rank(smem_u32(sp), p), make_uint4((uint32_t)gsum, 0u, 0u, 0u));
+      const uint32_t u = (uint32_t)gsum;
+      for (int p = 0; p < Q; ++p) st_cluster_v4(mapa_rank(smem_u32(sp), p), make_uint4(u, u, u, u));
     }
   }
 }
@@ -807,7 +810,8 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
       for (int q = 0; q < A::kCs; ++q) {
         const int tok = 8 * (q >> 1) + 2 * t + (q & 1);
         if (tok < M)
-          acc.csum[q] += *reinterpret_cast<const int32_t *>(rec0 + tok * kTokStride + F::kActWords * 4);
+          acc.csum[q] += *reinterpret_cast<const int32_t *>(rec0 + tok * kTokStride +
+                                                          (F::kActWords + ((tok >> 1) & 3)) * 4);
       }
     }
     return;
