@@ -236,6 +236,9 @@ typedef struct tb_step_input {
   double *scale;           /* out: absmax / 127 (or 1) of this vector         */
   int32_t *nonfinite_flag; /* optional: 1 if this launch saw NaN / inf, else 0
                             (device or mapped pinned host memory)            */
+  const int32_t *ready;    /* optional: the launch waits until *ready != 0
+                            before reading x (e.g. set by the copy engine
+                            after the host-to-device copy that fills x)     */
 } tb_step_input;
 int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
                          const int32_t *src, int64_t ninputs, const int64_t *input_k,

@@ -95,7 +95,7 @@ class GemmDesc(C.Structure):
 class StepInput(C.Structure):
     """Mirror of tb_step_input (include/ternary_b200.h)."""
 
-    _fields_ = [("x", _p), ("K", _i64), ("scale", _p), ("nonfinite_flag", _p)]
+    _fields_ = [("x", _p), ("K", _i64), ("scale", _p), ("nonfinite_flag", _p), ("ready", _p)]
 
 
 _lib = None

@@ -157,6 +157,7 @@ struct FinJob {
 };
 struct StepInputs {
   const float *x[kMaxStepInputs];
+  const int32_t *ready[kMaxStepInputs];  // optional: spin until != 0 before reading x
   double *scale[kMaxStepInputs];   // per-token scale out (read by the finalize)
   int32_t *flag[kMaxStepInputs];   // optional non-finite flag
   int K[kMaxStepInputs], C[kMaxStepInputs], off[kMaxStepInputs];  // off: record table offset
@@ -196,6 +197,12 @@ struct GemvBatch {
 __device__ __forceinline__ GemvJob job_at(const GemvBatch &b, int j) {
   if (b.table) return b.table[j];
   return b.jobs[j];
+}
+
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t *p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ int atom_add_acq_rel(int *ptr, int v) {
@@ -624,6 +631,13 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     need = blockIdx.x < kMaxNeedCtas ? b.in.need[blockIdx.x] : 0xF;
     crank = CQ > 1 ? (int)cluster_rank() : 0;
     if (cq > 1) cluster_arrive_relaxed();
+    // inputs filled by a copy that signals completion (HostPipeline block
+    // starts): an in-kernel wait instead of a graph edge, which would end the
+    // programmatic-dependent-launch overlap with the previous step
+#pragma unroll
+    for (int v = 0; v < kMaxStepInputs; ++v)
+      if (v < b.in.n && b.in.ready[v] && ((need >> v) & 1))
+        while (ld_acquire_gpu(b.in.ready[v]) == 0) __nanosleep(200);
 #ifndef TB_FUSED_NOLOAD  // profiling variants: TB_FUSED_NOLOAD / TB_FUSED_NOQ
     if (!b.in.x_after_wait) rq.load(b.in.x, b.in.K, b.in.C, b.in.n, need, crank, cq);
 #else
@@ -1352,6 +1366,7 @@ extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t nj
     if (!in.x || !in.scale || in.K < 1) return TB_ERR_ARGUMENT;
     const int64_t C = ceil_div(ref_row_bytes(fmt, in.K), kChunkBytes);
     b.in.x[v] = in.x;
+    b.in.ready[v] = in.ready;
     b.in.scale[v] = in.scale;
     b.in.flag[v] = in.nonfinite_flag;
     b.in.K[v] = (int)in.K;

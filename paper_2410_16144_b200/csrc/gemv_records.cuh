@@ -273,18 +273,18 @@ __device__ __forceinline__ float cta_absmax_f32(const float *__restrict__ x, int
     const int K4 = K >> 2;
     const float4 *x4 = reinterpret_cast<const float4 *>(x);
     for (int i = threadIdx.x; i < K4; i += kThreads) {
-      const float4 v = __ldg(x4 + i);
+      const float4 v = __ldcg(x4 + i);
       nf |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
       amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
     }
     for (int k = (K4 << 2) + threadIdx.x; k < K; k += kThreads) {
-      const float v = __ldg(x + k);
+      const float v = __ldcg(x + k);
       nf |= !isfinite(v);
       amax = fmaxf(amax, fabsf(v));
     }
   } else {
     for (int k = threadIdx.x; k < K; k += kThreads) {
-      const float v = __ldg(x + k);
+      const float v = __ldcg(x + k);
       nf |= !isfinite(v);
       amax = fmaxf(amax, fabsf(v));
     }
@@ -324,11 +324,11 @@ __device__ __forceinline__ void cta_build_records(const float *__restrict__ x, i
       const int kv = k0 + 4 * v;
       float xv[4];
       if (on && vec && kv + 3 < K) {
-        const float4 t = __ldg(reinterpret_cast<const float4 *>(x + kv));
+        const float4 t = __ldcg(reinterpret_cast<const float4 *>(x + kv));
         xv[0] = t.x, xv[1] = t.y, xv[2] = t.z, xv[3] = t.w;
       } else {
 #pragma unroll
-        for (int b = 0; b < 4; ++b) xv[b] = (on && kv + b < K) ? __ldg(x + kv + b) : 0.f;
+        for (int b = 0; b < 4; ++b) xv[b] = (on && kv + b < K) ? __ldcg(x + kv + b) : 0.f;
       }
       uint32_t word = 0;
 #pragma unroll
@@ -424,12 +424,12 @@ struct RegQuant {
         float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
         if (g < hi) {
           if (vec && kv + 3 < K) {
-            t = __ldg(reinterpret_cast<const float4 *>(x + kv));
-          } else {
-            if (kv < K) t.x = __ldg(x + kv);
-            if (kv + 1 < K) t.y = __ldg(x + kv + 1);
-            if (kv + 2 < K) t.z = __ldg(x + kv + 2);
-            if (kv + 3 < K) t.w = __ldg(x + kv + 3);
+            t = __ldcg(reinterpret_cast<const float4 *>(x + kv));
+          } else {  // L2 loads: x may have been written by a copy engine (ready flags)
+            if (kv < K) t.x = __ldcg(x + kv);
+            if (kv + 1 < K) t.y = __ldcg(x + kv + 1);
+            if (kv + 2 < K) t.z = __ldcg(x + kv + 2);
+            if (kv + 3 < K) t.w = __ldcg(x + kv + 3);
           }
         }
         xr[r][u] = t;

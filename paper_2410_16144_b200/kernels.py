@@ -470,6 +470,15 @@ class GemvStep:
         self._bound = xs  # keep alive
         return self
 
+    def set_ready(self, flag):
+        """Make the launch wait (in-kernel) until the int32 device word
+        ``flag`` is nonzero before reading its inputs -- e.g. set by the copy
+        that fills them; ``None`` clears it."""
+        for i in range(len(self.input_k)):
+            self.inputs[i].ready = flag.data_ptr() if flag is not None else None
+        self._ready = flag  # keep alive
+        return self
+
     def run(self, xs=None, prev=None, stream_ptr: int | None = None):
         if xs is not None:
             self.bind(xs)
@@ -573,11 +582,13 @@ class HostPipeline:
     """Independent decode steps streamed between pinned HOST memory and the
     device: ``run()`` copies every step's float32 inputs in, runs the fused
     step chain and copies every step's outputs back.  The copies go in blocks
-    of ``block`` steps on two copy streams, so a block's host-to-device copy
-    and the previous block's device-to-host copy overlap the step kernels,
-    and the kernels stay one programmatic-dependent-launch chain (a cross-
-    stream wait only at block starts).  This is the serving form over a queue
-    of independent requests; HostStep is the one-token synchronous form.
+    (up to ``block`` steps) on two copy streams, so a block's host-to-device
+    copy and the previous block's device-to-host copy overlap the step
+    kernels; a block's steps wait for its copy through a ready flag (set by a
+    4-byte copy after it) inside the kernel, so the kernels stay one unbroken
+    programmatic-dependent-launch chain.  This is the serving form
+    over a queue of independent requests; HostStep is the one-token
+    synchronous form.
 
     ``slot_pairs`` holds R >= 2 lists of (GemvPlan, input index) pairs; step
     i uses list i % R (the same plans may repeat: every slot gets its own
@@ -633,24 +644,63 @@ class HostPipeline:
             st = GemvStep(pairs, self.input_k, flags=self._flags[r], sticky_flags=True)
             st.bind([self._x_dev[i, o:o + k] for o, k in zip(offs, self.input_k)])
             self._steps.append(st)
+        # copy blocks: sizes ramp 1, 2, 4 .. block and back down at the end, so
+        # the only copies not hidden behind step kernels (the first block's
+        # copy in, the last block's copy back) are small
+        ramp, k = [], 1
+        while k < block:
+            ramp.append(k)
+            k *= 2
+        sizes, left = [], steps
+        for k in ramp:
+            if left <= 0:
+                break
+            sizes.append(min(k, left))
+            left -= sizes[-1]
+        tail = []
+        for k in ramp:
+            if left <= 2 * block:
+                break
+            tail.append(k)
+            left -= k
+        while left > 0:
+            sizes.append(min(block, left))
+            left -= sizes[-1]
+        sizes += tail[::-1]
+        self._blocks, b0 = [], 0
+        for k in sizes:
+            self._blocks.append((b0, b0 + k))
+            b0 += k
+        nb = len(self._blocks)
+        self._ready = torch.zeros(nb, dtype=torch.int32, device=dev)
+        self._one = torch.ones(1, dtype=torch.int32).pin_memory()
+        self._zeros = torch.zeros(nb, dtype=torch.int32).pin_memory()
+        # every step of a block waits (a later step can start early under
+        # programmatic dependent launch, before the block's first step has
+        # seen its flag)
+        for b, (b0, b1) in enumerate(self._blocks):
+            for i in range(b0, b1):
+                self._steps[i].set_ready(self._ready[b:b + 1])
         self._graph = self._capture()
 
     def _record(self):
         T, B = self.steps, self.block
         comp = torch.cuda.current_stream()
         h2d, d2h = self._h2d, self._d2h
-        blocks = [(b0, min(T, b0 + B)) for b0 in range(0, T, B)]
-        in_ev = [torch.cuda.Event() for _ in blocks]
+        blocks = self._blocks
         done_ev = [torch.cuda.Event() for _ in blocks]
         start = torch.cuda.Event()
         start.record(comp)
         h2d.wait_event(start)
         d2h.wait_event(start)
+        # each block's copy is followed by a 4-byte copy that sets its ready
+        # flag; the block's first step kernel waits for the flag in-kernel (a
+        # graph edge from the copy would end the PDL overlap of the chain)
         with torch.cuda.stream(h2d):
             for b, (b0, b1) in enumerate(blocks):
                 if self._copies[0]:
                     self._x_dev[b0:b1].copy_(self.x_host[b0:b1], non_blocking=True)
-                in_ev[b].record(h2d)
+                self._ready[b:b + 1].copy_(self._one, non_blocking=True)
 
         def copy_out(b):  # block b is final once the next block's first kernel finalised it
             done_ev[b].record(comp)
@@ -661,7 +711,6 @@ class HostPipeline:
                     self._out_host[b0:b1].copy_(self._o_dev[b0:b1], non_blocking=True)
 
         for b, (b0, b1) in enumerate(blocks):
-            comp.wait_event(in_ev[b])
             for i in range(b0, b1):
                 self._steps[i].run(prev=self._steps[i - 1] if i else None)
                 if i == b0 and b:
@@ -670,6 +719,7 @@ class HostPipeline:
         copy_out(len(blocks) - 1)
         comp.wait_stream(h2d)
         comp.wait_stream(d2h)
+        self._ready.copy_(self._zeros, non_blocking=True)  # re-arm for the next run
 
     def _capture(self):
         s = torch.cuda.Stream()

@@ -24,9 +24,8 @@ def main():
             pl[name] = tb.GemvPlan(tb.encode_tl1(tb.ternarize_weights(w, rows, cols)))
         plans.append(pl)
     slots = [[(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)] for pl in plans]
-    for T, blk, copies in ((100, 16, (True, True)), (100, 16, (False, False)),
-                           (100, 16, (True, False)), (100, 16, (False, True)),
-                           (100, 100, (True, True)), (200, 16, (True, True)), (400, 16, (True, True))):
+    for T, blk, copies in ((400, 16, (True, True)), (400, 32, (True, True)),
+                           (400, 16, (False, False)), (100, 16, (True, True))):
         pipe = tb.HostPipeline(slots, [H, I], steps=T, block=blk, _copies=copies)
         pipe.inputs[0].normal_()
         pipe.inputs[1].normal_()
