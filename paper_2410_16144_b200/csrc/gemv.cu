@@ -97,9 +97,18 @@ struct Cfg {
   // four per SM; TL2, whose decode needs more registers: 8 warps, two per SM)
   // -- the next steps' CTAs (programmatic dependent launch) quantise and
   // prefetch while this step's CTAs stream
-  static constexpr int kWarps = FU == 1 ? (FMT == TB_TL2 ? 8 : TB_FUSED_WARPS)
+#ifndef TB_TL2_WARPS
+#define TB_TL2_WARPS 8
+#endif
+#ifndef TB_TL2_MINB
+#define TB_TL2_MINB 2
+#endif
+#ifndef TB_TL2_RING
+#define TB_TL2_RING 4
+#endif
+  static constexpr int kWarps = FU == 1 ? (FMT == TB_TL2 ? TB_TL2_WARPS : TB_FUSED_WARPS)
                                        : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
-  static constexpr int kMinBlocks = FU == 1 ? (FMT == TB_TL2 ? 2 : TB_FUSED_MINB) : 1;
+  static constexpr int kMinBlocks = FU == 1 ? (FMT == TB_TL2 ? TB_TL2_MINB : TB_FUSED_MINB) : 1;
 #ifndef TB_MT1_RING
 #define TB_MT1_RING (TB_MT1_WARPS > 16 ? 3 : 4)
 #endif
@@ -107,7 +116,7 @@ struct Cfg {
   static constexpr int kStageBytesAll =
       kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + MT * Fmt<FMT>::kRecBytes);
   static constexpr int kFit = (225 * 1024) / (kWarps * kStageBytesAll);
-  static constexpr int kRing = FU == 1 ? (FMT == TB_TL2 ? 4 : TB_FUSED_RING)
+  static constexpr int kRing = FU == 1 ? (FMT == TB_TL2 ? TB_TL2_RING : TB_FUSED_RING)
                                : (MT == 1 ? TB_MT1_RING : (kFit >= 4 ? 4 : (kFit >= 2 ? kFit : 2)));
   static constexpr int kThreads = 32 * kWarps;
   // fused step: records live in a CTA-wide table after the ring, not per stage
