@@ -407,6 +407,74 @@ def test_fused_step_sequence(tb):
             steps[0].run(xs_dev[0], prev=steps[0])
 
 
+def test_fused_step_segments_and_clusters(tb):
+    """Fused steps over the full grid (CTA pairs sharing the quantisation
+    through DSMEM) with per-input warp segments, and with more input runs
+    than segments (one segment: CTAs quantise several inputs), chained."""
+    rng = np.random.default_rng(29)
+    k0, k1 = 1024, 2048
+    for fmt, enc in ((1, tb.encode_i2s), (2, tb.encode_tl1)):
+        for srcs in ((0, 1), (0, 1, 0, 1, 0)):
+            steps, truth = [], []
+            for sidx in range(2):
+                pairs, vals = [], []
+                for j, src in enumerate(srcs):
+                    rows, cols = (4096 if len(srcs) == 2 else 1536), (k0, k1)[src]
+                    v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+                    ws = 0.25 + 0.05 * j + 0.1 * sidx
+                    plan = tb.GemvPlan(enc(tb.TernaryMatrix(rows, cols, v, ws)),
+                                       out_dtype=torch.float64, want_acc=True)
+                    pairs.append((plan, src))
+                    vals.append((v, ws))
+                steps.append(tb.GemvStep(pairs, [k0, k1]))
+                truth.append(vals)
+            xs_host = [[_tie_vector(rng, k0), rng.standard_normal(k1).astype(np.float32)]
+                       for _ in range(3)]
+            xs_dev = [[torch.from_numpy(x).cuda() for x in xs] for xs in xs_host]
+
+            def check(si, xi):
+                q = [O.quantize(x, 1) for x in xs_host[xi]]
+                for (plan, src), (v, ws) in zip(steps[si].pairs, truth[si]):
+                    want = O.gemv_ref_int32(v, q[src][0])
+                    assert np.array_equal(host(plan.acc)[0], want), (fmt, srcs, si)
+                    np.testing.assert_array_equal(host(plan.out64)[0],
+                                                  want.astype(np.float64) * ws * q[src][1])
+
+            steps[0].run(xs_dev[0])
+            steps[1].run(xs_dev[1], prev=steps[0])
+            steps[0].run(xs_dev[2], prev=steps[1])
+            torch.cuda.synchronize()
+            check(1, 1)
+            steps[0].finalize()
+            torch.cuda.synchronize()
+            check(0, 2)
+
+
+def test_host_pipeline_block_ramps(tb):
+    """HostPipeline over step counts that exercise the copy-block ramps
+    (1 step, a partial ramp, ramp + full blocks + ramp down)."""
+    rng = np.random.default_rng(41)
+    v0 = rng.integers(-1, 2, size=(256, 512), dtype=np.int8)
+    v1 = rng.integers(-1, 2, size=(64, 768), dtype=np.int8)
+    plans = [tb.GemvPlan(tb.encode_i2s(tb.TernaryMatrix(256, 512, v0, 0.5))),
+             tb.GemvPlan(tb.encode_i2s(tb.TernaryMatrix(64, 768, v1, 0.25)))]
+    pairs = [(plans[0], 0), (plans[1], 1)]
+    for T in (1, 5, 70):
+        pipe = tb.HostPipeline([pairs, pairs], [512, 768], steps=T, block=8)
+        xs0 = rng.standard_normal((T, 512)).astype(np.float32)
+        xs1 = rng.standard_normal((T, 768)).astype(np.float32)
+        pipe.inputs[0].copy_(torch.from_numpy(xs0))
+        pipe.inputs[1].copy_(torch.from_numpy(xs1))
+        for _ in range(2):  # the ready flags re-arm between runs
+            outs = pipe.run()
+            for i in range(T):
+                (q0, s0, _), (q1, s1, _) = O.quantize(xs0[i], 1), O.quantize(xs1[i], 1)
+                w0 = (O.gemv_ref_int32(v0, q0).astype(np.float64) * 0.5 * s0).astype(np.float32)
+                w1 = (O.gemv_ref_int32(v1, q1).astype(np.float64) * 0.25 * s1).astype(np.float32)
+                np.testing.assert_array_equal(outs[0][i].numpy(), w0, err_msg=f"T={T} i={i}")
+                np.testing.assert_array_equal(outs[1][i].numpy(), w1, err_msg=f"T={T} i={i}")
+
+
 def test_fused_step_large_input(tb):
     """Inputs too large for the register-held quantiser take the looped path."""
     rng = np.random.default_rng(5)
