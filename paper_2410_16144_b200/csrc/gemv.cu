@@ -937,8 +937,10 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   TL_MARK(4);
   if constexpr (kFused) {
     if (!waited) {
+#ifndef TB_NO_TAILWAIT  // profiling variant (results invalid): no chain serialisation
       asm volatile("griddepcontrol.wait;" ::: "memory");
       fin_load();
+#endif
     }
     drain();
     // this step's scales (read by whoever finalises this batch), then the
