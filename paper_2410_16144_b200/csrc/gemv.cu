@@ -236,6 +236,12 @@ __device__ __forceinline__ void flush_tile(const GemvBatch &b, int j, int t,
   return;
 #endif
   const GemvJob J = job_at(b, j);
+#ifdef TB_I2S_MMA
+  if constexpr (FMT == TB_I2S && kI2sMma<MT>) {  // tensor-core fragments: direct REDs
+    acc.red_all(J.ws_acc, J.Npad, t * kRowTile, M);
+    return;
+  }
+#endif
   const int row = t * kRowTile + lane;
 #pragma unroll
   for (int m = 0; m < MT; ++m)

@@ -719,6 +719,46 @@ struct Acc<TB_I2S, MT, true> {
     }
     return out - __shfl_sync(0xffffffffu, cs, src);
   }
+  // Publish every token's row sums of this tile straight from the fragment
+  // layout (REDs into ws[token][row0 + row]): token columns need no shuffles
+  // at all, plane columns one (the plane pairs of a row sit in lanes t, t^1).
+  __device__ __forceinline__ void red_all(int32_t *ws, int npad, int row0, int M) const {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    if constexpr (kPlaneCols) {
+      const bool odd = lane & 1;
+      const int tok = t >> 1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int32_t e[4], o[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          e[r] = d[h][0][r] + (kSets == 4 ? d[h][2][r] : 0);
+          o[r] = d[h][1][r] + (kSets == 4 ? d[h][3][r] : 0);
+        }
+        int32_t lo = odd ? (o[0] >> 4) + (o[1] >> 6) : e[0] + (e[1] >> 2);
+        int32_t hi = odd ? (o[2] >> 4) + (o[3] >> 6) : e[2] + (e[3] >> 2);
+        lo += __shfl_xor_sync(0xffffffffu, lo, 1);
+        hi += __shfl_xor_sync(0xffffffffu, hi, 1);
+        if (!odd && (tok == 0 || tok < M)) {
+          int32_t *w = ws + (int64_t)tok * npad + row0 + g + 16 * h;
+          red_add_s32(w, lo - csum[0]);
+          red_add_s32(w + 8, hi - csum[0]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int nb = 0; nb < kSets; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int tok = 8 * nb + 2 * t + (r & 1);
+            if (tok < M)
+              red_add_s32(ws + (int64_t)tok * npad + row0 + g + 8 * (r >> 1) + 16 * h,
+                          d[h][nb][r] - csum[2 * nb + (r & 1)]);
+          }
+    }
+  }
 };
 
 __device__ __forceinline__ uint4 ldsm_x4(const void *p) {
