@@ -31,6 +31,18 @@ def main():
         xh = [torch.randn(M, h, generator=g, device="cuda") for _ in range(layers)]
         xi = [torch.randn(M, i, generator=g, device="cuda") for _ in range(layers)]
         pool = st.make_glues(xh, xi)
+    if os.environ.get("ONLY") == "gemv" and M > 1:  # timing only: the GEMVs without the glue
+        def gemv_only(*_):
+            for b in st.batches:
+                b.run(finalize=False)
+        st.token_pass = gemv_only
+    elif os.environ.get("ONLY") == "glue" and M > 1:  # timing only: the glues alone
+        def glue_only(xh_, xi_, pool_):
+            prev = None
+            for li, b in enumerate(st.batches):
+                pool_[li].retarget(prev).run()
+                prev = b
+        st.token_pass = glue_only
     for _ in range(4):
         st.token_pass(xh, xi, pool)
     torch.cuda.synchronize()
