@@ -4,7 +4,10 @@
 
 namespace tb {
 
-constexpr int kStageChunks = 4;  // chunks per ring stage (per warp)
+#ifndef TB_STAGE_CHUNKS
+#define TB_STAGE_CHUNKS 4
+#endif
+constexpr int kStageChunks = TB_STAGE_CHUNKS;  // chunks per ring stage (per warp)
 
 template <int FMT>
 struct Fmt {
