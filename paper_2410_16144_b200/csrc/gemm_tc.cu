@@ -290,7 +290,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
         GT(p, 4);
         tc_fence_after();
         const uint32_t aA = smem_u32(smem + s * stage_bytes), aB = smem_u32(bslots + bs * kBTileBytes);
+#ifdef TB_GEMM_HALF_MMA  // profiling variant (results invalid): one token sub-tile's MMAs
+        for (int mt = 0; mt < 1; ++mt) {
+#else
         for (int mt = 0; mt < MT; ++mt) {
+#endif
 #pragma unroll
           for (int k2 = 0; k2 < kGemmBK / 32; ++k2)
 #ifndef TB_GEMM_NO_MMA  // profiling variant: data movement only
