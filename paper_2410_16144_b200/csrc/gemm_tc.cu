@@ -259,7 +259,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
         GT(p, 0);
         const GemmJob &J = b.jobs[pc.j];
         uint8_t *st = smem + s * stage_bytes;
+#ifdef TB_GEMM_NO_A
+        mbar_arrive_expect_tx(&full[s], kPackedBytes);
+#else
         mbar_arrive_expect_tx(&full[s], a_bytes + kPackedBytes);
+#endif
+#ifdef TB_GEMM_NO_A  // profiling variant (results invalid): no activation loads
+        if (false) {
+        }
+#elif defined(TB_GEMM_NO_MC)  // each CTA copies the whole A stage itself (no multicast)
+        {
+          const uint8_t *srcA = J.act + (size_t)pc.kb * (b.Mpad * kGemmBK) + (size_t)pc.h * a_bytes;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(smem_u32(st)), "l"(srcA), "r"(a_bytes), "r"(smem_u32(&full[s]))
+              : "memory");
+        }
+#else
         const uint32_t half = a_bytes / kGemmCluster;
         const uint8_t *src =
             J.act + (size_t)pc.kb * (b.Mpad * kGemmBK) + (size_t)pc.h * a_bytes + crank * half;
@@ -268,6 +284,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
             " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(st) + crank * half),
             "l"(src), "r"(half), "r"(smem_u32(&full[s])), "h"((uint16_t)((1u << kGemmCluster) - 1))
             : "memory");
+#endif
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(st + a_bytes)),
@@ -357,9 +374,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
           for (int i = 0; i < 4; ++i) o[i] = make_uint4(0, 0, 0, 0);
         }
         // core matrix (row group rr/8, k chunk i): 128 B, row rr%8 at 16 B
+#ifndef TB_GEMM_NO_UNPACK  // profiling variant (results invalid): no B stores
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           *reinterpret_cast<uint4 *>(bt + ((rr >> 3) * 4 + i) * 128 + (rr & 7) * 16) = o[i];
+#else
+        if (o[0].x == 0x12345678u) *reinterpret_cast<uint4 *>(bt) = o[1];
+#endif
       }
 #ifdef TB_GEMM_TRACE_DEC
       if (tid == 128) GT(p, 5);
