@@ -405,6 +405,7 @@ def run_gpu(args, rank, world):
                                   "row-parallel down + NCCL int32 all-reduce)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "frac_vs_nominal_8000": round(achieved / 8000.0, 4),
                      "traffic": measured_traffic() if tp == 1 else None,
                      "kernel": ("tgemv_kernel<TL1,1,fused> one-launch step: quantise x_h, x_i + "
                                 "gate/up (14336x4096) + down (4096x14336) + previous finalize")
@@ -580,7 +581,8 @@ def run_prefill(torch, tb, copies=2, reps=10):
                         "one grouped tcgen05 kind::i8 launch",
             "tops": round(tops, 1), "us_per_layer": round(ms * 1e3, 1), "gop": round(ops / 1e9, 1),
             "peak_tops": round(peak, 1), "peak_kind": "cuBLASLt int8 torch._int_mm 8192^3, measured",
-            "frac": round(tops / peak, 4)}
+            "frac": round(tops / peak, 4),
+            "frac_vs_nominal_4500": round(tops / 4500.0, 4)}
 
 
 def run_stack(torch, tb, name, fmt, tokens=1, steps=10):
