@@ -20,7 +20,8 @@
 //
 // Operand layout: UMMA K-major, no swizzle -- "core matrices" of 8 rows x 16
 // bytes (128 contiguous bytes), K-adjacent core matrices 128 B apart (LBO),
-// 8-row groups 512 B apart (SBO) within a 64-byte K stage.  A is pre-tiled in
+// 8-row groups KC x 128 B apart (SBO; KC = 8 core matrices per 128-byte K
+// stage).  A is pre-tiled in
 // global memory into exactly this order (tb_gemm_tile_act: [k-stage][row
 // group][k core][8 rows][16 B], plus the per-token sums), so one 1-D bulk
 // copy moves a token sub-tile of a stage.
@@ -49,18 +50,26 @@
 namespace tb {
 
 constexpr int kGemmBN = 256;      // weight rows per tile (MMA N)
-constexpr int kGemmBK = 64;       // int8 K per stage = one packed 16-byte chunk per row
+// 128-K stages (two packed 16-byte chunks per row): the per-stage pipeline
+// cost (barrier round, TMA issue, unpack pass) was the limit at 64 K (~950
+// cycles per stage against 512 cycles of MMA); 125 -> 100 us on the cfg3 layer
+#ifndef TB_GEMM_BK
+#define TB_GEMM_BK 128
+#endif
+constexpr int kGemmBK = TB_GEMM_BK;  // int8 K per stage: 64 = one packed 16-byte chunk per row, 128 = two
+constexpr int kGemmKC = kGemmBK / 16;         // K core matrices per stage (per 8-row group)
+constexpr int kChunksPerStage = kGemmBK / 64;  // packed 16-byte chunks per row per stage
 constexpr int kGemmSubM = 128;    // MMA M
 constexpr int kGemmMaxMT = 2;     // tokens per CTA tile: 256 (M x N = 64K int32 = all of TMEM)
 constexpr int kGemmMaxM = 512;    // tokens per launch: up to two 256-token halves
 constexpr int kGemmThreads = 384;  // 12 warps: producer, MMA, (2 idle), 8 unpack/epilogue
-constexpr int kGemmStages = 8;   // load ring (A + packed weights): ~2 us of loads in flight
-constexpr int kGemmBSlots = 3;
+constexpr int kGemmStages = kGemmBK == 128 ? 4 : 8;  // load ring (A + packed weights): ~2 us of loads in flight
+constexpr int kGemmBSlots = kGemmBK == 128 ? 2 : 3;
 constexpr int kGemmCluster = 2;  // CTA pair sharing every A stage (TMA multicast)   // unpacked-weight (B operand) slots; reused as epilogue staging
 constexpr int kGemmMaxJobs = 8;
 constexpr int kSubTileBytes = kGemmSubM * kGemmBK;    // 8 KB
 constexpr int kBTileBytes = kGemmBN * kGemmBK;        // 16 KB
-constexpr int kPackedBytes = kGemmBN * kChunkBytes;   // 4 KB
+constexpr int kPackedBytes = kGemmBN * kChunkBytes * kChunksPerStage;  // 4 KB per 64 K
 constexpr int kEpiBytes = 8 * 32 * 36 * 4;            // 8 epilogue warps x 32x32 int32 (in the B slots)
 static_assert(kEpiBytes <= kGemmBSlots * kBTileBytes, "epilogue staging lives in the B slots");
 
@@ -92,7 +101,7 @@ struct GemmBatch {
 // K-adjacent core matrices, SBO = 512 B between 8-row groups, version 1.
 __device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128 >> 4) << 16) |
-         ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46);
+         ((uint64_t)((kGemmKC * 128) >> 4) << 32) | ((uint64_t)1 << 46);
 }
 
 // Instruction descriptor, kind::i8: D s32, A signed 8-bit, B unsigned 8-bit
@@ -288,7 +297,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(st + a_bytes)),
-            "l"(reinterpret_cast<uint64_t>(&J.bmap)), "r"(0), "r"(pc.kb), "r"(pc.n0 >> 5),
+            "l"(reinterpret_cast<uint64_t>(&J.bmap)), "r"(0), "r"(pc.kb * kChunksPerStage), "r"(pc.n0 >> 5),
             "r"(smem_u32(&full[s]))
             : "memory");
         GT(p, 1);
@@ -360,11 +369,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
       if (p >= (uint32_t)kGemmBSlots) mbar_spin(&bempty[bs], (p / kGemmBSlots - 1) & 1);
       if (tid == 128) GT(p, 2);
       const GemmJob &J = b.jobs[cc.j];
-      {
+#pragma unroll
+      for (int cs = 0; cs < kChunksPerStage; ++cs) {  // the row's packed chunks of this stage
         const int rr = r;
         uint4 o[4];
         if (cc.n0 + rr < J.Npad) {
-          const uint4 pk = *reinterpret_cast<const uint4 *>(st + a_bytes + rr * 16);
+          // TMA box [row tile][chunk][32 rows][16 B]
+          const uint4 pk = *reinterpret_cast<const uint4 *>(
+              st + a_bytes + (((rr >> 5) * kChunksPerStage + cs) * kRowTile + (rr & 31)) * 16);
           o[0] = code_planes<FMT>(pk.x);
           o[1] = code_planes<FMT>(pk.y);
           o[2] = code_planes<FMT>(pk.z);
@@ -373,11 +385,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
 #pragma unroll
           for (int i = 0; i < 4; ++i) o[i] = make_uint4(0, 0, 0, 0);
         }
-        // core matrix (row group rr/8, k chunk i): 128 B, row rr%8 at 16 B
+        // core matrix (row group rr/8, k core 4 cs + i): 128 B, row rr%8 at 16 B
 #ifndef TB_GEMM_NO_UNPACK  // profiling variant (results invalid): no B stores
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          *reinterpret_cast<uint4 *>(bt + ((rr >> 3) * 4 + i) * 128 + (rr & 7) * 16) = o[i];
+          *reinterpret_cast<uint4 *>(bt + ((rr >> 3) * kGemmKC + 4 * cs + i) * 128 + (rr & 7) * 16) = o[i];
 #else
         if (o[0].x == 0x12345678u) *reinterpret_cast<uint4 *>(bt) = o[1];
 #endif
@@ -517,13 +529,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
 // followed by the per-token sums int32 [Mpad] (the unsigned-code correction).
 __global__ void gemm_tile_act_kernel(const int8_t *__restrict__ act, int M, int64_t lda, int cols,
                                      int Mpad, int ks, uint8_t *__restrict__ out) {
-  const int64_t units = (int64_t)ks * Mpad * 4;  // 16-byte units
+  const int64_t units = (int64_t)ks * Mpad * kGemmKC;  // 16-byte units
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units;
        u += (int64_t)gridDim.x * blockDim.x) {
     const int r8 = (int)(u & 7);
     const int64_t q = u >> 3;  // (ks_i, g, c)
-    const int c = (int)(q & 3);
-    const int64_t q2 = q >> 2;
+    const int c = (int)(q % kGemmKC);
+    const int64_t q2 = q / kGemmKC;
     const int g = (int)(q2 % (Mpad / 8));
     const int ksi = (int)(q2 / (Mpad / 8));
     const int m = g * 8 + r8;
@@ -586,7 +598,7 @@ static bool encode_weight_map(CUtensorMap *map, const uint8_t *w, int C, int T) 
   if (!enc) return false;
   const cuuint64_t dims[3] = {kTileChunkBytes / 8, (cuuint64_t)C, (cuuint64_t)T};
   const cuuint64_t strides[2] = {kTileChunkBytes, (cuuint64_t)C * kTileChunkBytes};
-  const cuuint32_t box[3] = {kTileChunkBytes / 8, 1, kGemmBN / kRowTile};
+  const cuuint32_t box[3] = {kTileChunkBytes / 8, kChunksPerStage, kGemmBN / kRowTile};
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint8_t *>(w), dims, strides, box,
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -728,8 +740,10 @@ extern "C" int tb_gemm_batch(int fmt, int64_t njobs, const tb_gemm_desc *descs, 
     J.out32 = d.out32;
     J.N = (int)d.rows;
     J.Npad = (int)pad_up(d.rows, kRowTile);
-    J.C = (int)ceil_div(ref_row_bytes(fmt, d.cols), kChunkBytes);  // == stages of 64 K
-    if (!encode_weight_map(&J.bmap, d.tiled, J.C, (int)ceil_div(d.rows, kRowTile)))
+    J.C = (int)ceil_div(ref_row_bytes(fmt, d.cols), (int64_t)kChunkBytes * kChunksPerStage);  // K stages
+    // the tensor map walks the tiled layout's 16-byte chunks (tile stride C_chunks x 512 B)
+    if (!encode_weight_map(&J.bmap, d.tiled, (int)ceil_div(ref_row_bytes(fmt, d.cols), kChunkBytes),
+                           (int)ceil_div(d.rows, kRowTile)))
       return TB_ERR_CUDA;
     J.tile0 = tiles;  // in tile pairs
     J.ntiles = (int)ceil_div(d.rows, kGemmBN);
