@@ -63,8 +63,14 @@ constexpr int kGemmSubM = 128;    // MMA M
 constexpr int kGemmMaxMT = 2;     // tokens per CTA tile: 256 (M x N = 64K int32 = all of TMEM)
 constexpr int kGemmMaxM = 512;    // tokens per launch: up to two 256-token halves
 constexpr int kGemmThreads = 384;  // 12 warps: producer, MMA, (2 idle), 8 unpack/epilogue
-constexpr int kGemmStages = kGemmBK == 128 ? 4 : 8;  // load ring (A + packed weights): ~2 us of loads in flight
-constexpr int kGemmBSlots = kGemmBK == 128 ? 2 : 3;
+#ifndef TB_GEMM_STAGES
+#define TB_GEMM_STAGES (kGemmBK >= 192 ? 2 : kGemmBK == 128 ? 4 : 8)
+#endif
+constexpr int kGemmStages = TB_GEMM_STAGES;  // load ring (A + packed weights)
+#ifndef TB_GEMM_BSLOTS
+#define TB_GEMM_BSLOTS (kGemmBK >= 128 ? 2 : 3)
+#endif
+constexpr int kGemmBSlots = TB_GEMM_BSLOTS;
 constexpr int kGemmCluster = 2;  // CTA pair sharing every A stage (TMA multicast)   // unpacked-weight (B operand) slots; reused as epilogue staging
 constexpr int kGemmMaxJobs = 8;
 constexpr int kSubTileBytes = kGemmSubM * kGemmBK;    // 8 KB
