@@ -227,7 +227,7 @@ int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
 /* tb_gemv_step_launch `flags`: */
 #define TB_STEP_X_AFTER_WAIT 1 /* inputs written by the preceding kernel          */
 #define TB_STEP_ISOLATED 2     /* one launch at a time (no chained step to overlap):
-                                  one 16-warp CTA per SM instead of two 8-warp ones */
+                                  one 16-warp CTA per SM instead of four small ones */
 #define TB_STEP_STICKY_FLAGS 4 /* non-finite flags are only ever SET (the caller
                                   clears them): one flag can cover many steps     */
 typedef struct tb_step_input {

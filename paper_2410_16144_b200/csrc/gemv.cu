@@ -76,7 +76,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 #define TL_LMARK(i) TL_MARK(i)
 #endif
 
-// FU: 0 = records path; 1 = fused step, 8 warps, two CTAs per SM; 2 = fused
+// FU: 0 = records path; 1 = fused step, small CTAs, several per SM; 2 = fused
 // step, 16 warps, one CTA per SM (record tables too large for two CTAs)
 template <int FMT, int MT, int FU = 0>
 struct Cfg {
@@ -1181,7 +1181,7 @@ static int launch_batch(int fmt, GemvBatch &b, int maxM, cudaStream_t s) {
 }
 
 static int launch_step(int fmt, GemvBatch &b, int rec_tab_bytes, bool isolated, cudaStream_t s) {
-  // two 8-warp CTAs per SM (chained steps overlap) when the record tables
+  // small CTAs, several per SM (chained steps overlap) when the record tables
   // allow it; one 16-warp CTA per SM for big tables or an isolated launch
   const bool small = !isolated && rec_tab_bytes <= Cfg<TB_I2S, 1, 1>::kRecTabBytes;  // 40 KB
   if (fmt == TB_I2S || fmt == TB_TL1)  // TL1 tiles hold I2_S codes
