@@ -123,7 +123,10 @@ struct Cfg {
   static constexpr int kStageBytes =
       kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + (kFused ? 0 : MT) * Fmt<FMT>::kRecBytes);
   static constexpr int kRingBytes = kWarps * kRing * kStageBytes;
-  static constexpr int kRecTabBytes = kFused ? (kMinBlocks >= 2 ? 40 : 64) * 1024 : 0;  // records of all inputs
+#ifndef TB_SMALL_RECTAB_KB
+#define TB_SMALL_RECTAB_KB 40
+#endif
+  static constexpr int kRecTabBytes = kFused ? (kMinBlocks >= 2 ? TB_SMALL_RECTAB_KB : 64) * 1024 : 0;  // records of all inputs
   static constexpr int kSmem = kRingBytes + kRecTabBytes;
   static_assert(kSmem <= 227 * 1024 - 512, "ring does not fit in shared memory");
 };
