@@ -861,6 +861,8 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
   }
 #endif
   const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+  uint4 tq[3];  // TL2, one token: activation words of the current word pair
+  (void)tq;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t W = w[i];
@@ -907,14 +909,29 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
         code[3 * h + 1] = c1;
         code[3 * h + 2] = r - 3u * c1;  // r % 3
       }
+      if constexpr (MT == 1) {
+        // one token: the 12 activation words of a word pair in three 16-byte loads
+        if ((i & 1) == 0) {
+          const uint4 *Q = reinterpret_cast<const uint4 *>(rec0 + 24 * i);
+          tq[0] = Q[0];
+          tq[1] = Q[1];
+          tq[2] = Q[2];
+        }
+        const uint32_t a[6] = {(i & 1) ? tq[1].z : tq[0].x, (i & 1) ? tq[1].w : tq[0].y,
+                               (i & 1) ? tq[2].x : tq[0].z, (i & 1) ? tq[2].y : tq[0].w,
+                               (i & 1) ? tq[2].z : tq[1].x, (i & 1) ? tq[2].w : tq[1].y};
 #pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        if (m == 0 || m < M) {  // token 0 always exists: no branch for MT == 1
-          const uint2 *A = reinterpret_cast<const uint2 *>(rec0 + m * kTokStride + 24 * i);
-          const uint2 a01 = A[0], a23 = A[1], a45 = A[2];
-          const uint32_t a[6] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y};
+        for (int q = 0; q < 6; ++q) acc.v[0][q] = dp4a_us(code[q], a[q], acc.v[0][q]);
+      } else {
 #pragma unroll
-          for (int q = 0; q < 6; ++q) acc.v[m][q] = dp4a_us(code[q], a[q], acc.v[m][q]);
+        for (int m = 0; m < MT; ++m) {
+          if (m == 0 || m < M) {
+            const uint2 *A = reinterpret_cast<const uint2 *>(rec0 + m * kTokStride + 24 * i);
+            const uint2 a01 = A[0], a23 = A[1], a45 = A[2];
+            const uint32_t a[6] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y};
+#pragma unroll
+            for (int q = 0; q < 6; ++q) acc.v[m][q] = dp4a_us(code[q], a[q], acc.v[m][q]);
+          }
         }
       }
     }
