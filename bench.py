@@ -529,8 +529,8 @@ def run_prefill(torch, tb, copies=2, reps=10):
     lib = L.load()
     M, KV = 512, 1024
     g = torch.Generator(device="cuda").manual_seed(5)
-    xh = tb.quantize_activations(torch.randn(M, H, generator=g, device="cuda"))
-    xi = tb.quantize_activations(torch.randn(M, I, generator=g, device="cuda"))
+    xh = tb.quantize_tokens(torch.randn(M, H, generator=g, device="cuda"))
+    xi = tb.quantize_tokens(torch.randn(M, I, generator=g, device="cuda"))
     tiled = {}
     for qa, k in ((xh, H), (xi, I)):
         t = torch.empty(lib.tb_gemm_act_bytes(M, k), dtype=torch.uint8, device="cuda")

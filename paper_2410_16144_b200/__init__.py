@@ -15,6 +15,7 @@ from .core import (
     TernaryMatrix,
     make_result,
     quantize_activations,
+    quantize_tokens,
     round_half_away,
     ternarize_weights,
 )

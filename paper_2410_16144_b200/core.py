@@ -9,8 +9,10 @@ messages.  Arithmetic runs in the sm_100a kernels of libternary_b200.so
   * ``ternarize_weights``     -> core.py:104-113 (scale = NumPy-pairwise mean)
   * ``make_result``           -> core.py:99-101
 
-Extension over the reference: ``quantize_activations`` also accepts a 2-D
-[M, K] batch of tokens (one absmax scale per token, as M reference calls).
+``quantize_activations`` keeps the reference semantics exactly: any input
+shape is flattened to one vector with one scale (core.py:123).  The batched
+extension is ``quantize_tokens``: a 2-D [M, K] input is M tokens with one
+absmax scale each, i.e. M reference calls in one launch.
 """
 
 from __future__ import annotations
@@ -28,6 +30,7 @@ __all__ = [
     "GemvResult",
     "ternarize_weights",
     "quantize_activations",
+    "quantize_tokens",
     "round_half_away",
     "make_result",
     "device",
@@ -106,6 +109,17 @@ class QuantizedActivations:
     scales: torch.Tensor | None = field(default=None, compare=False, repr=False)
     _trusted: bool = field(default=False, compare=False, repr=False)
     _cache: dict = field(default_factory=dict, compare=False, repr=False)
+    # set by quantize_*(check_finite=False): ``scale`` is read from the device
+    # scales[0] on first access instead of at quantisation time (no sync)
+    _lazy_scale: bool = field(default=False, compare=False, repr=False)
+
+    def __getattribute__(self, name):
+        if name == "scale" and object.__getattribute__(self, "_lazy_scale"):
+            v = float(object.__getattribute__(self, "scales")[0].item())
+            object.__setattr__(self, "scale", v)
+            object.__setattr__(self, "_lazy_scale", False)
+            return v
+        return object.__getattribute__(self, name)
 
     def __post_init__(self):
         d = to_device(self.data, torch.int8)
@@ -114,6 +128,7 @@ class QuantizedActivations:
         K = d.shape[-1]
         if self.original_len < 1 or self.original_len > K:
             raise ValueError("original_len must be in [1, len(data)]")
+        lazy = object.__getattribute__(self, "_lazy_scale")
         if not self._trusted:
             if d.numel() and int(d.min()) < -127:
                 raise ValueError("activation value -128 is never produced")
@@ -123,9 +138,12 @@ class QuantizedActivations:
                 raise ValueError("scale must be positive and finite")
         object.__setattr__(self, "data", d.contiguous())
         if self.scales is None:
+            if lazy:
+                raise ValueError("a lazily read scale needs the device scales")
             object.__setattr__(self, "scales", torch.full(
                 (self.tokens,), float(self.scale), dtype=torch.float64, device=d.device))
-        object.__setattr__(self, "scale", float(self.scale))
+        if not lazy:
+            object.__setattr__(self, "scale", float(self.scale))
 
     @property
     def tokens(self) -> int:
@@ -247,47 +265,75 @@ def quantize_into(x: torch.Tensor, q: torch.Tensor, scales: torch.Tensor,
                L.ptr(flag), L.stream_ptr(stream)), "quantize")
 
 
-def quantize_activations(x, pad_to: int = 1, *, check_finite: bool = True
-                         ) -> QuantizedActivations:
-    """Absmax int8 quantisation, zero-padded to a multiple of ``pad_to``."""
+def _host_f64(x):
+    """Host view of a CPU input as float64 (any dtype: bf16, int8, requires_grad)."""
+    if isinstance(x, torch.Tensor):
+        return x.detach().to(torch.float64).numpy()
+    return np.asarray(x, dtype=np.float64)
+
+
+def _quantize(x, pad_to: int, batched: bool, check_finite: bool) -> QuantizedActivations:
     if pad_to not in (1, 2, 3, 4):
         raise ValueError("pad_to must be in {1, 2, 3, 4}")
     if isinstance(x, torch.Tensor):
-        xt = x
         is32 = x.dtype == torch.float32
+        on_host = x.device.type == "cpu"
     else:
-        a = np.asarray(x)
-        is32 = a.dtype == np.float32
-        xt = a
-    xd = to_device(xt, torch.float32 if is32 else torch.float64)
-    one = xd.dim() <= 1
-    xd = xd.reshape(1, -1) if one else xd.reshape(xd.shape[0], -1)
+        x = np.asarray(x)
+        is32 = x.dtype == np.float32
+        on_host = True
+    # float32 stays float32 (x / scale is then formed from the exact float32
+    # value, as NumPy does after its float64 cast); everything else -> float64
+    xd = to_device(x, torch.float32 if is32 else torch.float64)
+    if batched:
+        if xd.dim() != 2:
+            raise ValueError("quantize_tokens expects a 2-D [tokens, K] input")
+    else:
+        xd = xd.reshape(1, -1)  # core.py:123: any shape is one vector
     M, K = xd.shape
-    if K < 1:
+    if K < 1 or M < 1:
         raise ValueError("empty activation vector")
     xd = xd.contiguous()
     Kp = _pad(K, pad_to)
     q = torch.empty((M, Kp), dtype=torch.int8, device=xd.device)
     scales = torch.empty(M, dtype=torch.float64, device=xd.device)
-    host = None  # host input: the verdict and token 0's scale come from the host copy
-    if check_finite and (not isinstance(x, torch.Tensor) or x.device.type == "cpu"):
-        host = (x.numpy() if isinstance(x, torch.Tensor) else np.asarray(x)).reshape(M, K)
-    if host is not None:
-        # no device round trip: max|x| is exact in any precision, and the
-        # scale is the reference's float64 amax / 127 (core.py:128-130), the
-        # same value the kernel computes from the device copy
-        am = np.abs(host).max(axis=1)  # one pass: NaN / inf propagate into the max
+    lazy = False
+    if check_finite and on_host:
+        # host input: the finiteness verdict and token 0's scale come from a
+        # float64 host view (no device round trip); max|x| of the float64 view
+        # is the reference's amax exactly (core.py:123-129), so s0 equals the
+        # device-computed scales[0]
+        am = np.abs(_host_f64(x).reshape(M, K)).max(axis=1)  # NaN / inf propagate
         if not np.isfinite(am).all():
             raise ValueError("activations must be finite")
         amax0 = float(am[0])
         s0 = amax0 / 127.0 if amax0 > 0 else 1.0
         quantize_into(xd, q, scales, None)
-    else:
-        flag = torch.zeros(1, dtype=torch.int32, device=xd.device) if check_finite else None
+    elif check_finite:
+        flag = torch.zeros(1, dtype=torch.int32, device=xd.device)
         quantize_into(xd, q, scales, flag)
-        if check_finite and int(flag.item()):
+        if int(flag.item()):
             raise ValueError("activations must be finite")
-        s0 = float(scales[0].item()) if check_finite else 1.0
-    data = q[0] if one else q
+        s0 = float(scales[0].item())
+    else:
+        quantize_into(xd, q, scales, None)
+        s0, lazy = 0.0, True
+    data = q if batched else q[0]
     return QuantizedActivations(data=data, scale=s0, original_len=K, scales=scales,
-                                _trusted=True)
+                                _trusted=True, _lazy_scale=lazy)
+
+
+def quantize_activations(x, pad_to: int = 1, *, check_finite: bool = True
+                         ) -> QuantizedActivations:
+    """Absmax int8 quantisation, zero-padded to a multiple of ``pad_to``
+    (core.py:116-134): the input is flattened to ONE vector with one scale.
+    ``check_finite=False`` skips the host-side verdict (no device sync); the
+    ``scale`` attribute is then read from the device on first access."""
+    return _quantize(x, pad_to, False, check_finite)
+
+
+def quantize_tokens(x, pad_to: int = 1, *, check_finite: bool = True) -> QuantizedActivations:
+    """Batched extension: x [M, K] is M tokens, each quantised as its own
+    reference call (one absmax scale per token); ``data`` is [M, K_pad],
+    ``scales`` [M] and ``scale`` token 0's."""
+    return _quantize(x, pad_to, True, check_finite)

@@ -52,7 +52,7 @@ def test_quantize_golden(tb):
 
 def test_quantize_batch_and_errors(tb):
     x = np.random.default_rng(5).standard_normal((7, 333)).astype(np.float32)
-    qa = tb.quantize_activations(x, pad_to=3)
+    qa = tb.quantize_tokens(x, pad_to=3)
     for i in range(7):
         d, s, _ = O.quantize(x[i], 3)
         assert np.array_equal(host(qa.data[i]), d) and host(qa.scales)[i] == s
@@ -62,6 +62,38 @@ def test_quantize_batch_and_errors(tb):
         tb.quantize_activations([1.0, np.nan])
     with pytest.raises(ValueError, match="empty activation vector"):
         tb.quantize_activations(np.zeros(0))
+
+
+def test_quantize_reference_shape_semantics(tb):
+    """core.py:123 flattens ANY input to one vector with one scale: a (1, K)
+    row and a (K, 1) column are one token, not K tokens."""
+    x = np.random.default_rng(6).standard_normal(50).astype(np.float32)
+    d, s, _ = O.quantize(x, 2)
+    for shaped in (x.reshape(1, -1), x.reshape(-1, 1), x.reshape(5, 10)):
+        qa = tb.quantize_activations(shaped, pad_to=2)
+        assert qa.data.dim() == 1 and qa.tokens == 1
+        assert np.array_equal(host(qa.data), d) and qa.scale == s
+
+
+def test_quantize_scale_matches_device_for_every_dtype(tb):
+    """The host fast path's scale (reference attribute) equals the device
+    scales[0] for every accepted input dtype, incl. bf16, requires_grad and
+    an int8 -128 (whose |x| must not wrap)."""
+    rng = np.random.default_rng(9)
+    base = rng.standard_normal(300)
+    cases = [base.astype(np.float32), base, base.astype(np.float16),
+             np.array([-128, 5, 3], dtype=np.int8), np.array([7, -3], dtype=np.int64),
+             torch.from_numpy(base.astype(np.float32)).to(torch.bfloat16),
+             torch.from_numpy(base.astype(np.float32)).requires_grad_(True)]
+    for x in cases:
+        qa = tb.quantize_activations(x, pad_to=4)
+        ref = x.detach().to(torch.float64).numpy() if isinstance(x, torch.Tensor) else x
+        d, s, _ = O.quantize(np.asarray(ref, dtype=np.float64), 4)
+        assert qa.scale == float(host(qa.scales)[0]) == s, type(x)
+        assert np.array_equal(host(qa.data), d)
+    # check_finite=False: no sync at quantisation, the scale is read lazily
+    qa = tb.quantize_activations(base, pad_to=1, check_finite=False)
+    assert qa.scale == float(host(qa.scales)[0]) == O.quantize(base, 1)[1]
 
 
 def test_records_quantizer_golden(tb):
@@ -288,7 +320,7 @@ def test_batched_tokens_match_single(tb):
                           (tb.KernelKind.TL2, tb.encode_tl2)):
             p = enc(m)
             for M in (1, 2, 3, 5, 8, 13):
-                qa = tb.quantize_activations(x[:M], pad_to=tb.KERNEL_PAD[kind])
+                qa = tb.quantize_tokens(x[:M], pad_to=tb.KERNEL_PAD[kind])
                 r = tb.gemv_parallel(kind, p, qa)
                 want = np.stack([O.gemv_ref_int32(v, O.quantize(x[i], 1)[0]) for i in range(M)])
                 assert np.array_equal(host(r.accumulators), want), (kind, M)
@@ -314,7 +346,7 @@ def test_gemv_plan_fp32_output(tb):
     x = rng.standard_normal((4, 4096)).astype(np.float32)
     for enc, pad in ((tb.encode_i2s, 4), (tb.encode_tl1, 2), (tb.encode_tl2, 3)):
         plan = tb.GemvPlan(enc(m), max_tokens=4, out_dtype=torch.float32, want_acc=True)
-        qa = tb.quantize_activations(x, pad_to=pad)
+        qa = tb.quantize_tokens(x, pad_to=pad)
         out = host(plan.run(qa.data, qa.scales)).astype(np.float64)
         for i in range(4):
             d, s, _ = O.quantize(x[i], 1)
@@ -553,7 +585,7 @@ def test_prefill_gemm_tensor_cores(tb, M, rows, cols):
     v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
     x = rng.standard_normal((M, cols)).astype(np.float32)
     x[0, : min(cols, 4)] = [127.0, -0.5, 0.5, 2.5][: min(cols, 4)]
-    qa = tb.quantize_activations(torch.from_numpy(x).cuda())
+    qa = tb.quantize_tokens(torch.from_numpy(x).cuda())
     q = host(qa.data.reshape(M, -1))
     scales = host(qa.scales)
     want = np.stack([O.gemv_ref_int32(v, q[m]) for m in range(M)])
@@ -574,8 +606,8 @@ def test_prefill_gemm_batch_grouped(tb):
     lib = L.load()
     rng = np.random.default_rng(3)
     M, H, I = 256, 512, 1024
-    xh = tb.quantize_activations(torch.from_numpy(rng.standard_normal((M, H)).astype(np.float32)).cuda())
-    xi = tb.quantize_activations(torch.from_numpy(rng.standard_normal((M, I)).astype(np.float32)).cuda())
+    xh = tb.quantize_tokens(torch.from_numpy(rng.standard_normal((M, H)).astype(np.float32)).cuda())
+    xi = tb.quantize_tokens(torch.from_numpy(rng.standard_normal((M, I)).astype(np.float32)).cuda())
     shapes = [(H, H, xh), (128, H, xh), (128, H, xh), (H, H, xh), (I, H, xh), (I, H, xh), (H, I, xi)]
     descs = (L.GemmDesc * len(shapes))()
     keep, wants = [], []
@@ -698,7 +730,7 @@ def _run_large(tb, cname, formats=("i2s", "tl1", "tl2")):
     for name, mm, k, seed in case["acts"]:
         x = torch.from_numpy(activations(seed, mm, k))
         for pad in (1, 2, 3, 4):
-            qa = tb.quantize_activations(x, pad_to=pad)
+            qa = tb.quantize_tokens(x, pad_to=pad)
             assert sha(host(qa.data)) == gold["acts"][name][f"data_p{pad}"]
             assert [float(s).hex() for s in host(qa.scales)] == gold["acts"][name]["scales"]
     for wname, aname in case["gemv"]:
@@ -708,7 +740,7 @@ def _run_large(tb, cname, formats=("i2s", "tl1", "tl2")):
         g = gold["gemv"][f"{wname}:{aname}"]
         for f, p in packs.items():
             kind, _, pad = kinds[f]
-            qa = tb.quantize_activations(x, pad_to=pad)
+            qa = tb.quantize_tokens(x, pad_to=pad)
             r = tb.gemv_parallel(kind, p, qa)
             acc = host(r.accumulators).reshape(mm, -1)
             out = host(r.output).reshape(mm, -1)

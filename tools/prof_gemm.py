@@ -57,8 +57,8 @@ def main():
     enc = tb.encode_i2s if a.fmt == "i2s" else tb.encode_tl1
     M = a.m
     g = torch.Generator(device="cuda").manual_seed(0)
-    xh = tb.quantize_activations(torch.randn(M, H, generator=g, device="cuda"))
-    xi = tb.quantize_activations(torch.randn(M, I, generator=g, device="cuda"))
+    xh = tb.quantize_tokens(torch.randn(M, H, generator=g, device="cuda"))
+    xi = tb.quantize_tokens(torch.randn(M, I, generator=g, device="cuda"))
     shapes = [("q", H, H, xh), ("k", KV, H, xh), ("v", KV, H, xh), ("o", H, H, xh),
               ("gate", I, H, xh), ("up", I, H, xh), ("down", H, I, xi)]
     if a.only:
