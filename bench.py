@@ -1,27 +1,36 @@
-"""Benchmark: ternary-linear tokens/s at M=1 decode on BASELINE.json config 1.
+"""Benchmark: ternary-linear decode tokens/s on BASELINE.json configs[4].
 
-Workload (BASELINE.json configs[1]): the TL1 FFN block of a Llama-3-8B-shaped
-layer at M=1 -- gate and up (K=4096 -> N=14336) on one freshly quantised
-activation vector, down (K=14336 -> N=4096) on another, exactly the per-layer
-work of the reference bench's token pass (pkg/src/ternpack/bench.py:138-153):
-per-token absmax int8 quantisation + (implicit) TL1 LUT + exact int32 GEMV +
-rescale.  One "step" = one token through that block.
+Headline workload (the largest configuration of BASELINE.json that fits one
+B200): cfg4, the ~100B-parameter ternary projection stack -- 80 layers,
+hidden 10240 (q/o 10240x10240, k/v 10240->1280, gate/up 10240->32768, down
+32768->10240), I2_S, M=1 decode -- exactly the reference bench's token pass
+(pkg/src/ternpack/bench.py:138-153): per layer, two freshly quantised
+activation vectors (hidden for q/k/v/o/gate/up, intermediate for down) and 7
+exact int32 GEMVs rescaled by w_scale * a_scale.  One step = one token
+through all 80 layers (24.9 GB of packed weights, far above the 126 MB L2,
+so every step streams from HBM with no flush needed).
 
-  value   device-resident throughput: K steps captured in one CUDA graph,
-          inputs already in HBM, weights rotated over 6 distinct copies
-          (265 MB > 126 MB L2) so every step streams from HBM.
-  e2e     the same steps through the public Python API (quantize_activations
-          + gemv_parallel) with pinned HOST inputs and the float64 results
-          read back to the host inside the timed region.
-  roofline  the TL1 GEMV kernel timed alone (graph of back-to-back launches
-          over the rotating copies, CUDA events): algorithmic bytes per
-          launch / mean launch time vs MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline  the C port of the reference byte-table CPU kernels
-          (oracle/c/tern_oracle.c) on this host, bounded sample.
+  value     device-resident throughput: K token passes captured in one CUDA
+            graph (one fused step launch per layer), inputs already in HBM.
+  e2e       the same token passes through the public API with HOST buffers:
+            tb.HostPipeline over the 80 layers -- per token, the 80 layers'
+            float32 inputs copied in from pinned host memory and all 560
+            float32 output vectors copied back, inside the timed region.
+  roofline  the fused step kernel (one launch per layer): algorithmic bytes
+            per launch / its mean launch duration over the
+            timed region, against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline  the C port of the reference's byte-table CPU kernels
+            (oracle/c), one layer timed on the host cores, x 80.
+  configs   every other BASELINE config (cfg0, cfg1, cfg2 I2_S / TL2, cfg3
+            prefill, cfg4 M=8), each with its own value, roofline fraction,
+            e2e and cpu_baseline.
 
-``--impl reference`` times that CPU port alone on the same workload (rank 0).
-Multi-GPU (torchrun, N>1): tensor parallel -- gate/up column-parallel, down
-row-parallel with an NCCL all-reduce of the int32 partial accumulators.
+``--gpus N`` (N > 1) runs tensor parallel, strong scaling: the same cfg4
+stack sharded over N ranks (column-parallel q/k/v/gate/up, row-parallel
+o/down), the row-parallel int32 partials summed by our NVLink peer-memory
+kernel (``--collective peer``, default) or NCCL (``--collective nccl``).
+Without torchrun in the environment, ``--gpus N`` launches the N ranks
+itself.  ``--impl reference`` times the CPU port alone on the same workload.
 """
 
 from __future__ import annotations
@@ -40,39 +49,45 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-H, I = 4096, 14336
-NCOPY = 6
-NX = 64
 METRIC = "ternary-linear tokens/s (M=1 decode)"
+H1, I1 = 4096, 14336           # cfg1 / cfg2 / cfg3 shapes (Llama-3-8B)
+CFG4 = {"hidden": 10240, "kv": 1280, "inter": 32768, "layers": 80}
+STACK_SEED = 11
 
 
-def tl1_bytes(rows, cols):
-    return rows * (-(-(-(-cols // 2) * 2 // 2) // 2))
+def headline_config(world: int) -> dict:
+    """The workload dict of the headline line -- identical in both arms."""
+    return {"workload": "cfg4: ~100B-shaped ternary projection stack, 80 layers, hidden 10240 "
+                        "(q/o 10240x10240, k/v 10240->1280, gate/up 10240->32768, "
+                        "down 32768->10240), I2_S, M=1 decode",
+            "format": "I2_S", "layers": 80, "tokens_per_step": 1,
+            "weights": "seeded N(0,0.02) latent -> absmean ternary (core.py:104-113)",
+            "activations": "fresh N(0,1) per layer, per-token absmax int8 (bench.py:141-142)",
+            "l2": "24.9 GB packed weights per step >> 126 MB L2 (no flush needed)",
+            "parallelism": f"tp{world}"}
 
 
-def algo_bytes_gemv(rows, cols, m=1):
-    # packed weights (reference TL1 size) + int8 activations + fp32 outputs
-    return tl1_bytes(rows, cols) + m * cols + 4 * m * rows
-
-
-def measured_traffic():
-    """DRAM bytes per launch of the step kernel from the committed ncu --set full
-    capture (profiles/r1_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            d = json.load(f)
-        return int(d["dram_bytes_read"] + d["dram_bytes_write"])
-    except Exception:
-        return None
-
+# ---------------------------------------------------------------------------
+# measurement helpers
+# ---------------------------------------------------------------------------
 
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def measured_traffic(name):
+    """dram bytes read + write per launch of the named kernel capture
+    (profiles/r2_traffic.json, from an ncu --set full capture), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
+            d = json.load(f)[name]
+        return int(d["dram_bytes_read"] + d["dram_bytes_write"])
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -83,9 +98,7 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index=0):
-        self.index = index
-        self.proc = None
-        self.lines = []
+        self.index, self.proc, self.lines = index, None, []
 
     def __enter__(self):
         try:
@@ -93,8 +106,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
         return self
@@ -133,311 +145,377 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=5).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def graph_time(torch, fn, reps=1):
+    """Capture fn() once into a CUDA graph, replay once untimed, then time
+    ``reps`` replays with CUDA events on the capture stream (ms per replay)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, g
+
+
+def roofline(bytes_per_launch, launch_us, kernel, traffic=None, source=""):
+    peak, kind = measured_peak()
+    ach = bytes_per_launch / (launch_us * 1e-6) / 1e9
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(ach / peak, 4), "frac_vs_nominal_8000": round(ach / 8000.0, 4),
+            "traffic": traffic, "kernel": kernel, "bytes_per_launch": int(bytes_per_launch),
+            "launch_us": round(launch_us, 3), "launch_us_source": source,
+            "peak_kind": f"{kind} hbm_gbs (copy)"}
+
+
 # ---------------------------------------------------------------------------
-# CPU port of the reference (oracle/c) -- baseline and --impl reference
+# CPU port of the reference (oracle/c): cpu_baseline and --impl reference
 # ---------------------------------------------------------------------------
 
-def cpu_token_runner(gate, up, down):
-    """Returns f(xh, xi) running one reference-style TL1 FFN token on the CPU port."""
+def _co():
     from oracle import c_oracle as CO
-    g1, g2 = H // 2, I // 2
+    return CO
+
+
+def cpu_stack_layer(fmt, mats, h, i):
+    """f(xh, xi, threads): one layer of the reference token pass on the CPU
+    port (bench.py:138-153): 2 quantisations (+ TL2 LUTs), 7 byte-table GEMVs.
+    ``mats``: [(reference planes tuple, input index)] in layer order."""
+    CO = _co()
+    pad = 4 if fmt == "i2s" else 3
 
     def run(xh, xi, threads):
-        qh, _ = CO.quantize(xh, 2)
-        lut_h = CO.lut_tl1(qh, g1)
-        CO.gemv_tl1(gate, lut_h, threads)
-        CO.gemv_tl1(up, lut_h, threads)
-        qi, _ = CO.quantize(xi, 2)
-        lut_i = CO.lut_tl1(qi, g2)
-        CO.gemv_tl1(down, lut_i, threads)
-
+        qh, _ = CO.quantize(xh, pad)
+        qi, _ = CO.quantize(xi, pad)
+        if fmt == "tl2":
+            luts = [CO.lut_tl2(qh, len(qh) // 3), CO.lut_tl2(qi, len(qi) // 3)]
+        for planes, src in mats:
+            if fmt == "i2s":
+                CO.gemv_i2s(planes[0], qh if src == 0 else qi, threads)
+            else:
+                CO.gemv_tl2(planes[0], planes[1], luts[src], threads)
     return run
 
 
-def cpu_baseline(gate, up, down, budget_s=12.0):
-    from oracle import c_oracle as CO
-    run = cpu_token_runner(gate, up, down)
-    rng = np.random.default_rng(7)
-    xh = rng.standard_normal(H).astype(np.float32)
-    xi = rng.standard_normal(I).astype(np.float32)
+def time_cpu(run, args_fn, budget_s, threads_list):
+    """Best rate (calls/s) over the thread counts, each timed for ~budget/len."""
     best = None
-    ncpu = os.cpu_count() or 1
-    for threads in sorted({1, CO.max_threads(), ncpu}):
-        run(xh, xi, threads)  # warm
+    for t in threads_list:
+        run(*args_fn(0), t)  # warm
         n, t0 = 0, time.perf_counter()
-        while time.perf_counter() - t0 < budget_s / 2:
-            run(xh, xi, threads)
+        while True:
+            run(*args_fn(n), t)
             n += 1
-        tps = n / (time.perf_counter() - t0)
-        if best is None or tps > best[0]:
-            best = (tps, threads, n)
-    return {"value": round(best[0], 3), "unit": "tokens/s", "cores": best[1], "kind": "port",
-            "sample": f"{best[2]} TL1 FFN tokens (gate+up+down, quantise+LUT+byte-table gather) "
-                      f"on {best[1]} thread(s); best of threads in {{1, {ncpu}}}; host has {ncpu} CPUs"}
+            el = time.perf_counter() - t0
+            if el >= budget_s / len(threads_list):
+                break
+        rate = n / el
+        if best is None or rate > best[0]:
+            best = (rate, t, n)
+    return best
+
+
+def cpu_threads():
+    CO = _co()
+    ncpu = os.cpu_count() or 1
+    return sorted({1, CO.max_threads(), ncpu}), ncpu
+
+
+def cpu_baseline_stack(fmt, mats, h, i, layers, budget_s):
+    rng = np.random.default_rng(7)
+    X = [(rng.standard_normal(h).astype(np.float32), rng.standard_normal(i).astype(np.float32))
+         for _ in range(4)]
+    run = cpu_stack_layer(fmt, mats, h, i)
+    ths, ncpu = cpu_threads()
+    rate, t, n = time_cpu(run, lambda k: X[k % 4], budget_s, ths)
+    return {"value": round(rate / layers, 4), "unit": "tokens/s", "cores": t, "kind": "port",
+            "sample": f"{n} layers (2 quantise + 7 {fmt.upper()} byte-table GEMVs, M=1) on {t} "
+                      f"thread(s), rate / {layers} layers; best of threads in {ths}; host "
+                      f"{ncpu} CPUs ({cpu_model()})"}
 
 
 # ---------------------------------------------------------------------------
-# GPU side
+# headline: cfg4 stack, M=1, tp = world
 # ---------------------------------------------------------------------------
 
-def make_tl1(tb, torch, rows, cols, seed):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    w = torch.randn(rows, cols, generator=g, device="cuda", dtype=torch.float32) * 0.02
-    m = tb.ternarize_weights(w, rows, cols)
-    del w
-    return tb.encode_tl1(m)
+def make_collective(args, rank, world):
+    import torch.distributed as dist
+
+    from paper_2410_16144_b200 import tp as TP
+    if world == 1:
+        return None
+    if args.collective == "peer" and dist.get_backend() == "nccl":
+        return TP.PeerAllReduce(rank, world)
+    return TP.TorchAllReduce()
 
 
-def shard_rows(p, tb, torch, r0, r1):
-    """Column-parallel shard: rows [r0, r1) of a packed TL1 matrix (tp.column_shard)."""
-    from paper_2410_16144_b200 import tp
-    (data,) = tp.column_shard((p.data,), r0, r1)
-    return tb.PackedTL1(rows=r1 - r0, cols=p.cols, padded_cols=p.padded_cols,
-                        data=data.contiguous(), scale=p.scale, trusted=True)
-
-
-def shard_cols(p, tb, torch, k0, k1):
-    """Row-parallel shard: K-slice [k0, k1) as a byte slice (tp.row_shard)."""
-    from paper_2410_16144_b200 import tp
-    (data,), cols = tp.row_shard("tl1", (p.data,), p.cols, k0, k1)
-    return tb.PackedTL1(rows=p.rows, cols=cols, padded_cols=cols + (cols & 1),
-                        data=data.contiguous(), scale=p.scale, trusted=True)
-
-
-def run_gpu(args, rank, world):
+def run_headline(args, rank, world):
     import torch
     import torch.distributed as dist
 
     import paper_2410_16144_b200 as tb
+    from paper_2410_16144_b200.stack import LayerStack
 
-    dev = torch.device("cuda", _local_device(torch))
-    torch.cuda.set_device(dev)
-    # N > 1: independent decode replicas by default (each GPU holds the block
-    # and decodes its own token stream -- no data-path collective, weak
-    # scaling); --parallel tp shards the block instead (column-parallel
-    # gate/up, row-parallel down + one NCCL int32 all-reduce per token).
-    tp = world if args.parallel == "tp" else 1
-    # ---- weights: NCOPY distinct seeded copies, TP-sharded
-    plans = []
-    gate_full_bytes = 0
-    for c in range(NCOPY):
-        gen = torch.Generator(device="cuda").manual_seed(1000 + c + (rank * 97 if tp == 1 else 0))
-        mats = {}
-        for name, rows, cols in (("gate", I, H), ("up", I, H), ("down", H, I)):
-            w = torch.randn(rows, cols, generator=gen, device="cuda", dtype=torch.float32) * 0.02
-            m = tb.ternarize_weights(w, rows, cols)
-            del w
-            if tp == 1:
-                p = tb.encode_tl1(m)
-            elif name in ("gate", "up"):
-                per = rows // tp
-                full = tb.encode_tl1(m)
-                p = shard_rows(full, tb, torch, rank * per, (rank + 1) * per)
-            else:
-                per = cols // tp
-                p = shard_cols(tb.encode_tl1(m), tb, torch, rank * per, (rank + 1) * per)
-            p.tiled()
-            mats[name] = p
-        if c == 0:
-            gate_full_bytes = mats["gate"].data.numel()
-            host_copy = {k: v.data.cpu().numpy() for k, v in mats.items()} if tp == 1 else None
-        plans.append({
-            "gate": tb.GemvPlan(mats["gate"], out_dtype=torch.float32),
-            "up": tb.GemvPlan(mats["up"], out_dtype=torch.float32),
-            "down": tb.GemvPlan(mats["down"], out_dtype=(torch.float32 if tp == 1 else None),
-                                want_acc=(tp > 1)),
-            "mats": mats,
-        })
-        for p in mats.values():
-            p._cache.pop("ref_dropped", None)
+    dev = torch.cuda.current_device()
+    coll = make_collective(args, rank, world)
+    t0 = time.perf_counter()
+    st = LayerStack(CFG4, fmt="i2s", seed=STACK_SEED, tokens=1, tp_rank=rank, tp_world=world,
+                    collective=coll)
+    build_s = time.perf_counter() - t0
+    L, h, i = CFG4["layers"], CFG4["hidden"], CFG4["inter"]
+    g = torch.Generator(device="cuda").manual_seed(99)  # same inputs on every rank
+    XH = torch.randn(L, h, generator=g, device="cuda")
+    XI = torch.randn(L, i, generator=g, device="cuda")
+    xh, xi = list(XH), list(XI)
+
+    def run_steps(n):
+        for _ in range(n):
+            st.token_pass(xh, xi)
+
+    run_steps(args.warmup)
     torch.cuda.synchronize()
-
-    gen = torch.Generator(device="cuda").manual_seed(77 + rank)
-    XH = torch.randn(NX, H, generator=gen, device="cuda", dtype=torch.float32)
-    XI = torch.randn(NX, I, generator=gen, device="cuda", dtype=torch.float32)
-    # activation records: quantisation fused with the GEMV input layout; the
-    # gate/up pair shares one record buffer (one quantisation per input vector)
-    from paper_2410_16144_b200 import _lib as L
-    rec_h = tb.ActRecords(L.TL1, 1, H)
-    rec_i = tb.ActRecords(L.TL1, 1, I)
-    out_down = torch.empty((1, H), dtype=torch.float32, device=dev)
-    kloc = I // tp
-    # row-parallel down (tp > 1): every rank quantises the full vector (same
-    # per-token scale as the reference) and contracts its K-slice
-    rec_i_loc = rec_i.chunk_slice(rank * kloc // 64, (rank + 1) * kloc // 64) if tp > 1 else rec_i
-    # gate, up and down of one token in ONE grouped launch (independent GEMVs)
-    for pl in plans:
-        pl["batch"] = tb.GemvBatch([(pl["gate"], rec_h), (pl["up"], rec_h),
-                                    (pl["down"], rec_i_loc)])
-        if tp == 1:  # fused one-launch step: input 0 = x_h (gate, up), 1 = x_i (down)
-            pl["step"] = tb.GemvStep([(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)], [H, I])
-    tail = tb.StepGlue([])
-
-    if tp == 1:
-        # A decode step is ONE launch (tb_gemv_step_launch): every CTA quantises
-        # the token's two input vectors itself, streams gate+up+down, and then
-        # finalises the previous step's outputs (scales -> fp32 outputs).
-        def step(i, prev):
-            pl = plans[i % NCOPY]
-            pl["step"].run([XH[i % NX], XI[i % NX]], prev=prev["step"] if prev else None)
-            return pl
-
-        def run_steps(n):
-            prev = None
-            for i in range(n):
-                prev = step(i, prev)
-            if prev is not None:
-                prev["step"].finalize()  # the last step's outputs
-
-        launches_per_step = 1
-    else:
-        # tp > 1: glue (finalise + quantise) and grouped GEMV launches; the down
-        # projection's int32 partials are all-reduced before its rescale.
-        glues = [tb.StepGlue([(XH[j:j + 1], rec_h), (XI[j:j + 1], rec_i)]) for j in range(NX)]
-
-        def step(i, prev):
-            pl = plans[i % NCOPY]
-            glues[i % NX].retarget(prev["batch"] if prev is not None else None).run()
-            pl["batch"].run(finalize=True)
-            dist.all_reduce(pl["down"].acc, op=dist.ReduceOp.SUM)
-            L.check(L.load().tb_scale_outputs(
-                pl["down"].acc.data_ptr(), 1, H, float(pl["mats"]["down"].scale),
-                rec_i.scales.data_ptr(), None, out_down.data_ptr(), L.stream_ptr()), "scale")
-            return None
-
-        def run_steps(n):
-            for i in range(n):
-                step(i, None)
-
-        launches_per_step = 4  # glue + grouped GEMV + finalize + rescale (+ NCCL)
-
-    # ---- warm-up (eager, also configures kernel attributes before capture)
-    run_steps(max(args.warmup, NCOPY))
-    torch.cuda.synchronize()
-
-    # ---- device-resident timed region: K steps in one CUDA graph (NCCL
-    #      collectives are capturable; a gloo functional check runs eagerly)
-    capturable = world == 1 or dist.get_backend() == "nccl"
+    capturable = coll is None or coll.capturable
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
-    graph = torch.cuda.CUDAGraph()
+    graph = None
     if capturable:
+        graph = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             with torch.cuda.graph(graph, stream=s):
                 run_steps(args.steps)
         torch.cuda.synchronize()
-        graph.replay()  # untimed replay (first replay uploads the graph)
+        with torch.cuda.stream(s):
+            graph.replay()  # untimed (uploads the graph)
         torch.cuda.synchronize()
 
-        def timed_region():
+        def timed():
             graph.replay()
     else:
-        def timed_region():
+        def timed():
             run_steps(args.steps)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
-        e0.record()
-        timed_region()
-        e1.record()
+    with ClockSampler(dev) as clk:
+        with torch.cuda.stream(s):
+            e0.record()
+            timed()
+            e1.record()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    ms_per_step = ms / args.steps
-
-    # ---- roofline: the dominant kernel timed alone, back-to-back over the
-    #      rotating copies in a graph (tp1: the fused step kernel -- quantise +
-    #      gate/up/down GEMV + previous finalize; tp>1: the grouped GEMV)
-    R = 4 * NCOPY
-    g2 = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(s):
-        with torch.cuda.graph(g2, stream=s):
-            for i in range(R):
-                if tp == 1:
-                    plans[i % NCOPY]["step"].run([XH[i % NX], XI[i % NX]],
-                                                 prev=plans[(i - 1) % NCOPY]["step"])
-                else:
-                    plans[i % NCOPY]["batch"].run(finalize=False)
-    g2.replay()
-    torch.cuda.synchronize()
-    e0.record()
-    g2.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    chain_ms = e0.elapsed_time(e1) / R
-    # tp1: the timed region IS the step kernel chain (K step launches + one
-    # trailing finalize), so the kernel's average launch duration over the
-    # timed region is ms_per_step (conservative: the finalize is included);
-    # the 24-launch chain above is reported beside it
-    gemv_ms = ms_per_step if tp == 1 else chain_ms
-    for pl in plans:  # finalise what is pending (resets the workspaces)
-        if tp == 1:
-            pl["step"].finalize()
-        else:
-            tail.retarget(pl["batch"]).run()
-    torch.cuda.synchronize()
-    rows_loc = I // tp
-    gemv_bytes = (algo_bytes_gemv(rows_loc, H) * 2 + tl1_bytes(H, kloc) + kloc + 4 * H)
-    peak, peak_kind = measured_peak()
-    achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
-
-    replicas = world if tp == 1 else 1
-    result = {
-        "metric": METRIC, "value": round(replicas * 1000.0 / ms_per_step, 2), "unit": "tokens/s",
+    ms_step = ms / args.steps
+    # the timed region is the step-kernel chain (80 fused launches per token,
+    # + at tp > 1 one peer reduction per layer): a launch's mean duration is
+    # the region time / launches (conservative: the tail finalize is inside)
+    launch_us = ms_step * 1e3 / L
+    per_launch = st.algo_bytes / L
+    res = {
+        "metric": METRIC, "value": round(1000.0 / ms_step, 3), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-        "scaling": "weak" if replicas > 1 else "strong", "vs_baseline": None, "dtype": "i8",
-        "data": "synthetic (seeded N(0,0.02) latent weights -> absmean ternary, N(0,1) activations)",
-        "config": {"workload": "cfg1: TL1 FFN block, gate/up 4096->14336 + down 14336->4096, M=1",
-                   "format": "TL1", "tokens_per_step": replicas,
-                   "l2": f"{NCOPY} rotating weight copies ({NCOPY * 3 * gate_full_bytes / 1e6:.0f} MB "
-                         "packed per rank) > 126 MB L2",
-                   "parallelism": (f"dp{world} (independent decode replicas, no collective)"
-                                   if replicas > 1 else "tp1") if tp == 1 else
-                                  f"tp{tp} (col-parallel gate/up, "
-                                  "row-parallel down + NCCL int32 all-reduce)"},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "frac_vs_nominal_8000": round(achieved / 8000.0, 4),
-                     "traffic": measured_traffic() if tp == 1 else None,
-                     "kernel": ("tgemv_kernel<TL1,1,fused> one-launch step: quantise x_h, x_i + "
-                                "gate/up (14336x4096) + down (4096x14336) + previous finalize")
-                               if tp == 1 else "tgemv_kernel<TL1,1> grouped gate+up+down",
-                     "bytes_per_launch": gemv_bytes, "launch_us": round(gemv_ms * 1e3, 3),
-                     "launch_us_source": ("timed region / K step launches (incl. the one trailing "
-                                          "finalize)" if tp == 1 else
-                                          f"{R}-launch graph of the grouped GEMV alone"),
-                     "launch_us_chain24": round(chain_ms * 1e3, 3),
-                     "peak_kind": f"{peak_kind} hbm_gbs (copy)"},
-        "gpu_launches": launches_per_step * args.steps + (1 if tp == 1 else 0),
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "i8",
+        "data": "synthetic (seeded N(0,0.02) latent weights -> absmean ternary I2_S; "
+                "N(0,1) activations)",
+        "config": headline_config(world),
+        "roofline": roofline(per_launch, launch_us,
+                             "tgemv_kernel<I2S,1,fused>: one layer = quantise x_h, x_i + "
+                             "q/k/v/o/gate/up/down grouped GEMV + previous layer's finalize"
+                             + (f" (this rank's tp{world} shards)" if world > 1 else ""),
+                             measured_traffic("cfg4_layer_step") if world == 1 else None,
+                             f"timed region / ({args.steps} steps x {L} layer launches)"),
+        "gpu_launches": args.steps * (L + 1 + (L if world > 1 else 0)),
         "clocks": clk.summary(),
+        "build_s": round(build_s, 1),
     }
+    if world > 1:
+        res["collective"] = type(coll).__name__
+        res["roofline"]["note"] = ("per-rank bytes of its shards; the launch time includes "
+                                   "the row-parallel reduction")
+    graph = None
+    # ---- e2e: the public API from host memory (rank 0, tp1)
+    if rank == 0 and world == 1 and not args.no_e2e:
+        res["e2e"] = e2e_stack(torch, tb, st, args.steps)
+    elif world > 1:
+        res["e2e"] = None
+        res["e2e_note"] = "tp > 1: host-buffer pass not measured (device-resident value only)"
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        mats = [((p.p.data.cpu().numpy(),), sh[3]) for p, sh in zip(st.layers[0], st.shapes)]
+        res["cpu_baseline"] = cpu_baseline_stack("i2s", mats, h, i, L, args.cpu_budget)
+    del st
+    torch.cuda.empty_cache()
+    return res
 
-    # ---- e2e through the public API with host buffers: every step copies its
-    #      two f32 input vectors in from pinned host memory, runs, and copies
-    #      its three fp32 output vectors back to pinned host memory
-    if rank == 0 and not args.no_e2e and tp == 1:
-        n_e2e = max(10, min(args.steps, 200))
-        xh_h = torch.randn(NX, H).pin_memory()
-        xi_h = torch.randn(NX, I).pin_memory()
-        # (a) the serving form: n_e2e independent steps in one HostPipeline
-        #     run (H2D / step kernels / D2H overlapped on three streams), the
-        #     weights rotating over the NCOPY copies as in `value`
-        # 400 steps per run: the first block's copy in and the last block's
-        # copy back (not hidden behind kernels) amortise over the run
-        n_pipe = 400
+
+def e2e_stack(torch, tb, st, steps):
+    """One token pass through tb.HostPipeline per step: the layers' inputs
+    from pinned host memory in, every projection's fp32 output out."""
+    L, h, i = st.nlayers, st.ks[0], st.ks[1]
+    pairs = [[(p, sh[3]) for p, sh in zip(plans, st.shapes)] for plans in st.layers]
+    pipe = tb.HostPipeline(pairs, [h, i], steps=L)
+    g = torch.Generator().manual_seed(5)
+    pipe.inputs[0].copy_(torch.randn(L, h, generator=g))
+    pipe.inputs[1].copy_(torch.randn(L, i, generator=g))
+    for _ in range(2):
+        pipe.run()
+    n = max(5, min(steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        pipe.run()
+    dt = (time.perf_counter() - t0) / n
+    rows = sum(sh[1] for sh in st.shapes)
+    out = {"value": round(1.0 / dt, 3), "unit": "tokens/s",
+           "h2d_bytes_per_step": L * (h + i) * 4, "d2h_bytes_per_step": L * rows * 4,
+           "steps": n,
+           "path": f"tb.HostPipeline.run() over the {L} layers: per token, the layers' f32 "
+                   "inputs H2D from pinned host memory and all 7 f32 output vectors of every "
+                   "layer D2H to pinned host memory, copies on two streams overlapping the "
+                   "fused-step chain; wall clock incl. the per-token sync"}
+    del pipe
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the other BASELINE configs (rank 0, one GPU)
+# ---------------------------------------------------------------------------
+
+def run_cfg0(torch, tb, args, copies=32, steps=200):
+    """configs[0]: one I2_S GEMV, M=1, 4096 x 4096 -- one fused launch per
+    token (quantise + GEMV + previous finalize), rotating over 32 weight
+    copies (134 MB > L2) in a CUDA graph."""
+    n = k = 4096
+    g = torch.Generator(device="cuda").manual_seed(3)
+    plans, steps_obj = [], []
+    for _ in range(copies):
+        w = torch.randn(n, k, generator=g, device="cuda") * 0.02
+        plan = tb.GemvPlan(tb.encode_i2s(tb.ternarize_weights(w, n, k)), out_dtype=torch.float32)
+        plans.append(plan)
+        steps_obj.append(tb.GemvStep([(plan, 0)], [k]))
+        del w
+    X = torch.randn(16, k, generator=g, device="cuda")
+
+    def run(cnt):
+        for j in range(cnt):
+            steps_obj[j % copies].run([X[j % 16]], prev=steps_obj[(j - 1) % copies])
+        steps_obj[(cnt - 1) % copies].finalize()
+
+    run(copies)
+    torch.cuda.synchronize()
+    ms, _ = graph_time(torch, lambda: run(steps))
+    us = ms * 1e3 / steps
+    algo = n * k // 4 + k + 4 * n
+    out = {"workload": "cfg0: I2_S GEMV M=1, 4096x4096, one fused launch per token "
+                       "(32 rotating weight copies, 134 MB > L2)",
+           "value": round(1e6 / us, 1), "unit": "tokens/s", "us_per_gemv": round(us, 3),
+           "roofline": roofline(algo, us, "tgemv_kernel<I2S,1,fused> (one GEMV per launch)",
+                                measured_traffic("cfg0_gemv"), "graph of 200 chained launches")}
+    if not args.no_e2e:
+        pipe = tb.HostPipeline([[(p, 0)] for p in plans[:8]], [k], steps=400)
+        pipe.inputs[0].copy_(torch.randn(400, k))
+        for _ in range(2):
+            pipe.run()
+        reps = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            pipe.run()
+            reps.append(time.perf_counter() - t0)
+        e = sorted(reps)[2] / 400
+        out["e2e"] = {"value": round(1 / e, 1), "unit": "tokens/s", "h2d_bytes_per_step": 4 * k,
+                      "d2h_bytes_per_step": 4 * n, "steps": 400,
+                      "path": "tb.HostPipeline: 400 independent GEMVs per run, pinned host f32 "
+                              "inputs in / f32 outputs out, median of 5 runs"}
+        del pipe
+    if not args.no_cpu_baseline:
+        CO = _co()
+        packed = plans[0].p.data.cpu().numpy()
+        xs = [np.random.default_rng(s).standard_normal(k).astype(np.float32) for s in range(4)]
+
+        def one(x, t):
+            q, _ = CO.quantize(x, 4)
+            CO.gemv_i2s(packed, q, t)
+        ths, ncpu = cpu_threads()
+        rate, t, cnt = time_cpu(one, lambda j: (xs[j % 4],), args.cpu_budget / 4, ths)
+        out["cpu_baseline"] = {"value": round(rate, 2), "unit": "tokens/s", "cores": t,
+                               "kind": "port",
+                               "sample": f"{cnt} GEMVs (quantise + I2_S byte-table gather) on {t} "
+                                         f"thread(s); best of {ths}; {ncpu} CPUs ({cpu_model()})"}
+    return out
+
+
+def run_cfg1(torch, tb, args, ncopy=6, nx=64):
+    """configs[1]: the TL1 FFN block at M=1 -- gate and up (4096 -> 14336) on
+    one quantised vector, down (14336 -> 4096) on another, one fused launch
+    per token, rotating over 6 weight copies (264 MB > L2)."""
+    plans = []
+    for c in range(ncopy):
+        gen = torch.Generator(device="cuda").manual_seed(1000 + c)
+        mats = {}
+        for name, rows, cols in (("gate", I1, H1), ("up", I1, H1), ("down", H1, I1)):
+            w = torch.randn(rows, cols, generator=gen, device="cuda", dtype=torch.float32) * 0.02
+            mats[name] = tb.encode_tl1(tb.ternarize_weights(w, rows, cols))
+            del w
+        pl = {k: tb.GemvPlan(v, out_dtype=torch.float32) for k, v in mats.items()}
+        pl["mats"] = mats
+        pl["step"] = tb.GemvStep([(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)], [H1, I1])
+        plans.append(pl)
+    gen = torch.Generator(device="cuda").manual_seed(77)
+    XH = torch.randn(nx, H1, generator=gen, device="cuda")
+    XI = torch.randn(nx, I1, generator=gen, device="cuda")
+
+    def run(n):
+        prev = None
+        for j in range(n):
+            pl = plans[j % ncopy]
+            pl["step"].run([XH[j % nx], XI[j % nx]], prev=prev["step"] if prev else None)
+            prev = pl
+        prev["step"].finalize()
+
+    run(max(args.warmup, ncopy))
+    torch.cuda.synchronize()
+    K = 400
+    ms, _ = graph_time(torch, lambda: run(K))
+    us = ms * 1e3 / K
+    tl1 = lambda r, c: r * (-(-(-(-c // 2) * 2 // 2) // 2))  # noqa: E731  packing.py:46-48
+    algo = 2 * (tl1(I1, H1) + H1 + 4 * I1) + tl1(H1, I1) + I1 + 4 * H1
+    out = {"workload": "cfg1: TL1 FFN block, gate/up 4096->14336 + down 14336->4096, M=1, one "
+                       "fused launch per token (6 rotating weight copies, 264 MB > L2)",
+           "value": round(1e6 / us, 1), "unit": "tokens/s", "us_per_step": round(us, 3),
+           "roofline": roofline(algo, us, "tgemv_kernel<TL1,1,fused>: quantise x_h, x_i + "
+                                "gate/up/down + previous finalize",
+                                measured_traffic("cfg1_step"), f"graph of {K} chained launches")}
+    if not args.no_e2e:
         pipe = tb.HostPipeline([[(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)]
-                                for pl in plans], [H, I], steps=n_pipe)
-        for i in range(n_pipe):
-            pipe.inputs[0][i].copy_(xh_h[i % NX])
-            pipe.inputs[1][i].copy_(xi_h[i % NX])
+                                for pl in plans], [H1, I1], steps=400)
+        g = torch.Generator().manual_seed(6)
+        pipe.inputs[0].copy_(torch.randn(400, H1, generator=g))
+        pipe.inputs[1].copy_(torch.randn(400, I1, generator=g))
         for _ in range(3):
             pipe.run()
         reps = []
@@ -445,99 +523,150 @@ def run_gpu(args, rank, world):
             t0 = time.perf_counter()
             pipe.run()
             reps.append(time.perf_counter() - t0)
-        e2e_s = sorted(reps)[len(reps) // 2] / n_pipe
-        result["e2e"] = {"value": round(1.0 / e2e_s, 2), "unit": "tokens/s",
-                         "h2d_bytes_per_step": (H + I) * 4,
-                         "d2h_bytes_per_step": (2 * I + H) * 4,
-                         "steps": n_pipe,
-                         "path": "tb.HostPipeline.run(): per step, pinned host f32 inputs -> H2D "
-                                 "copy -> fused step kernel (PDL chain) -> D2H copy of the fp32 "
-                                 "outputs to pinned host memory; copies and kernels on three "
-                                 "streams in one CUDA graph; wall clock incl. the final sync "
-                                 "(median of 5 runs)"}
-
-        # (b) one token at a time, synchronous (latency-bound): HostStep
-        hosts = [tb.HostStep([(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)], [H, I])
+        e = sorted(reps)[2] / 400
+        out["e2e"] = {"value": round(1 / e, 1), "unit": "tokens/s",
+                      "h2d_bytes_per_step": (H1 + I1) * 4, "d2h_bytes_per_step": (2 * I1 + H1) * 4,
+                      "steps": 400, "path": "tb.HostPipeline: 400 independent FFN tokens per "
+                                            "run, pinned host in/out, median of 5 runs"}
+        del pipe
+        # one token at a time, synchronous (decode latency)
+        hosts = [tb.HostStep([(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)], [H1, I1])
                  for pl in plans]
-
-        def e2e_step(i):
-            return hosts[i % NCOPY]([xh_h[i % NX], xi_h[i % NX]])
-
-        for i in range(5):
-            e2e_step(i)
+        xh_h = torch.randn(nx, H1).pin_memory()
+        xi_h = torch.randn(nx, I1).pin_memory()
+        for j in range(5):
+            hosts[j % ncopy]([xh_h[j % nx], xi_h[j % nx]])
+        n = 50
         t0 = time.perf_counter()
-        for i in range(n_e2e):
-            e2e_step(i)
-        sync_s = (time.perf_counter() - t0) / n_e2e
-        result["e2e_sync"] = {"value": round(1.0 / sync_s, 2), "unit": "tokens/s",
-                              "us_per_token": round(sync_s * 1e6, 2), "steps": n_e2e,
-                              "path": "tb.HostStep: one token per call (H2D, fused step, "
-                                      "finalize into mapped pinned memory, stream sync)"}
-
-        # the reference-shaped per-call API (quantize_activations + gemv_parallel
-        # per projection, float64 GemvResult.output to host)
-        K = tb.KernelKind
-
-        def api_step(i):
-            mats = plans[i % NCOPY]["mats"]
-            qa_h = tb.quantize_activations(xh_h[i % NX], pad_to=2)
-            rg = tb.gemv_parallel(K.TL1, mats["gate"], qa_h)
-            ru = tb.gemv_parallel(K.TL1, mats["up"], qa_h)
-            qa_i = tb.quantize_activations(xi_h[i % NX], pad_to=2)
-            rd = tb.gemv_parallel(K.TL1, mats["down"], qa_i)
-            return rg.output.cpu(), ru.output.cpu(), rd.output.cpu()
-
-        for i in range(3):
-            api_step(i)
+        for j in range(n):
+            hosts[j % ncopy]([xh_h[j % nx], xi_h[j % nx]])
+        dt = (time.perf_counter() - t0) / n
+        out["e2e_sync"] = {"value": round(1 / dt, 1), "unit": "tokens/s",
+                           "us_per_token": round(dt * 1e6, 2), "steps": n,
+                           "path": "tb.HostStep: one token per call (H2D, step, finalize into "
+                                   "mapped pinned memory, sync)"}
+        # the reference call pattern: quantize_activations + gemv_parallel x3
+        KK = tb.KernelKind
+        for _ in range(2):  # warm every copy's lazily built workspace and outputs
+            for pl in plans:
+                m = pl["mats"]
+                qa = tb.quantize_activations(xh_h[0], pad_to=2)
+                for nm in ("gate", "up"):
+                    tb.gemv_parallel(KK.TL1, m[nm], qa)
+                tb.gemv_parallel(KK.TL1, m["down"], tb.quantize_activations(xi_h[0], pad_to=2))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for i in range(n_e2e):
-            api_step(i)
-        torch.cuda.synchronize()
-        api_s = (time.perf_counter() - t0) / n_e2e
-        result["e2e_reference_api"] = {
-            "value": round(1.0 / api_s, 2), "unit": "tokens/s", "steps": n_e2e,
-            "h2d_bytes_per_step": (H + I) * 4, "d2h_bytes_per_step": (2 * I + H) * 8,
-            "path": "tb.quantize_activations + tb.gemv_parallel(TL1) x3 (reference call "
-                    "pattern, bench.py:138-153), float64 outputs to host"}
+        for j in range(n):
+            m = plans[j % ncopy]["mats"]
+            qh = tb.quantize_activations(xh_h[j % nx], pad_to=2)
+            rg = tb.gemv_parallel(KK.TL1, m["gate"], qh)
+            ru = tb.gemv_parallel(KK.TL1, m["up"], qh)
+            rd = tb.gemv_parallel(KK.TL1, m["down"], tb.quantize_activations(xi_h[j % nx],
+                                                                              pad_to=2))
+            rg.output.cpu(), ru.output.cpu(), rd.output.cpu()
+        dt = (time.perf_counter() - t0) / n
+        out["e2e_reference_api"] = {
+            "value": round(1 / dt, 1), "unit": "tokens/s", "steps": n,
+            "h2d_bytes_per_step": (H1 + I1) * 4, "d2h_bytes_per_step": (2 * I1 + H1) * 8,
+            "path": "tb.quantize_activations + tb.gemv_parallel(TL1) x3 per token (the "
+                    "reference call pattern, bench.py:138-153), float64 outputs to host"}
+    if not args.no_cpu_baseline:
+        CO = _co()
+        host = {k: plans[0]["mats"][k].data.cpu().numpy() for k in ("gate", "up", "down")}
+        rng = np.random.default_rng(7)
+        xs = [(rng.standard_normal(H1).astype(np.float32),
+               rng.standard_normal(I1).astype(np.float32)) for _ in range(4)]
 
-    if rank == 0 and tp == 1 and not args.no_prefill:
-        result["prefill"] = run_prefill(torch, tb)
-    if rank == 0 and tp == 1 and args.stacks:
-        result["stacks"] = {}
-        for spec in args.stacks.split(","):
-            if spec == "cfg0":
-                result["stacks"][spec] = run_cfg0(torch, tb)
-                continue
-            name, fmt, m = spec.split(":")
-            result["stacks"][spec] = run_stack(torch, tb, name, fmt, int(m))
+        def one(xh, xi, t):
+            qh, _ = CO.quantize(xh, 2)
+            lh = CO.lut_tl1(qh, H1 // 2)
+            CO.gemv_tl1(host["gate"], lh, t)
+            CO.gemv_tl1(host["up"], lh, t)
+            qi, _ = CO.quantize(xi, 2)
+            CO.gemv_tl1(host["down"], CO.lut_tl1(qi, I1 // 2), t)
+        ths, ncpu = cpu_threads()
+        rate, t, cnt = time_cpu(one, lambda j: xs[j % 4], args.cpu_budget / 2, ths)
+        out["cpu_baseline"] = {"value": round(rate, 2), "unit": "tokens/s", "cores": t,
+                               "kind": "port",
+                               "sample": f"{cnt} TL1 FFN tokens (quantise + LUT + byte-table "
+                                         f"gathers) on {t} thread(s); best of {ths}; {ncpu} CPUs "
+                                         f"({cpu_model()})"}
+    del plans
+    torch.cuda.empty_cache()
+    return out
 
-    if rank == 0 and not args.no_cpu_baseline and tp == 1:
-        result["cpu_baseline"] = cpu_baseline(host_copy["gate"], host_copy["up"],
-                                              host_copy["down"], budget_s=args.cpu_budget)
-    return result
+
+def run_stack_cfg(torch, tb, args, name, fmt, tokens, passes=10):
+    """configs[2] (cfg2, I2_S / TL2) and configs[4] at M=8: M-token decode
+    through the whole stack, one launch per layer (M=1) or glue + grouped
+    GEMV per layer (M > 1)."""
+    from paper_2410_16144_b200.stack import STACKS, LayerStack
+    cfg = STACKS[name]
+    t0 = time.perf_counter()
+    st = LayerStack(cfg, fmt=fmt, seed=STACK_SEED, tokens=tokens)
+    build_s = time.perf_counter() - t0
+    g = torch.Generator(device="cuda").manual_seed(99)
+    L, h, i = st.nlayers, cfg["hidden"], cfg["inter"]
+    if tokens == 1:
+        XH = torch.randn(L, h, generator=g, device="cuda")
+        XI = torch.randn(L, i, generator=g, device="cuda")
+        xh, xi, glues = list(XH), list(XI), None
+    else:
+        XH = torch.randn(L, tokens, h, generator=g, device="cuda")
+        XI = torch.randn(L, tokens, i, generator=g, device="cuda")
+        xh = xi = None
+        glues = st.make_glues(XH, XI)
+    st.token_pass(xh, xi, glues)
+    torch.cuda.synchronize()
+    ms, _ = graph_time(torch, lambda: [st.token_pass(xh, xi, glues) for _ in range(passes)])
+    ms /= passes
+    launches = L if tokens == 1 else 2 * L
+    kern = (f"tgemv_kernel<{fmt.upper()},1,fused> per layer" if tokens == 1 else
+            f"glue_kernel + tgemv_kernel<{fmt.upper()},{tokens}> per layer")
+    out = {"workload": f"{name}: {L} layers, hidden {h}, {fmt.upper()}, M={tokens}",
+           "value": round(tokens * 1000.0 / ms, 2), "unit": "tokens/s",
+           "ms_per_token_pass": round(ms, 4), "algo_bytes_per_pass": int(st.algo_bytes),
+           "roofline": roofline(st.algo_bytes / L, ms * 1e3 / L, kern,
+                                measured_traffic(f"{name}_{fmt}_m{tokens}"),
+                                f"graph of {passes} token passes / {L} layers"),
+           "launches_per_pass": launches + 1, "build_s": round(build_s, 1)}
+    if tokens == 1 and not args.no_e2e:
+        out["e2e"] = e2e_stack(torch, tb, st, 20)
+    if not args.no_cpu_baseline:
+        if fmt == "i2s":
+            mats = [((p.p.data.cpu().numpy(),), sh[3]) for p, sh in zip(st.layers[0], st.shapes)]
+        else:
+            mats = [((p.p.index_data.cpu().numpy(), p.p.sign_data.cpu().numpy()), sh[3])
+                    for p, sh in zip(st.layers[0], st.shapes)]
+        cb = cpu_baseline_stack(fmt, mats, h, i, L, args.cpu_budget / 2)
+        if tokens > 1:  # the reference has no multi-token path: M tokens = M passes
+            cb["sample"] += f"; M={tokens} costs {tokens} such passes (rate is per token)"
+        out["cpu_baseline"] = cb
+    del st
+    torch.cuda.empty_cache()
+    return out
 
 
-def run_prefill(torch, tb, copies=2, reps=10):
-    """BASELINE configs[3]: one Llama-3-8B-shaped layer of prefill GEMMs at
-    M=512 (I2_S), q/k/v/o/gate/up on x_h and down on x_i, in ONE grouped
-    tcgen05 launch (tb_gemm_batch); int8 TOPS = 2*M*sum(N*K) / time, against
-    the cuBLASLt int8 throughput measured here (torch._int_mm, 8192^3)."""
+def run_cfg3(torch, tb, args, copies=2, reps=10):
+    """configs[3]: one Llama-3-8B-shaped layer at M=512 (I2_S): per-token
+    quantisation of x_h [512, 4096] and x_i [512, 14336], their tensor-core
+    tiling (tb_gemm_tile_act) and ONE grouped tcgen05 kind::i8 launch over
+    q/k/v/o/gate/up/down -- all inside the timed region.
+    int8 TOPS = 2 * M * sum(N * K) / time."""
     import ctypes as C
 
     from paper_2410_16144_b200 import _lib as L
+    from paper_2410_16144_b200.core import quantize_into
     lib = L.load()
     M, KV = 512, 1024
     g = torch.Generator(device="cuda").manual_seed(5)
-    xh = tb.quantize_tokens(torch.randn(M, H, generator=g, device="cuda"))
-    xi = tb.quantize_tokens(torch.randn(M, I, generator=g, device="cuda"))
-    tiled = {}
-    for qa, k in ((xh, H), (xi, I)):
-        t = torch.empty(lib.tb_gemm_act_bytes(M, k), dtype=torch.uint8, device="cuda")
-        L.check(lib.tb_gemm_tile_act(qa.data.data_ptr(), M, qa.data.stride(0), k, t.data_ptr(),
-                                     L.stream_ptr()), "gemm_tile_act")
-        tiled[k] = (qa, t)
-    shapes = [(H, H), (KV, H), (KV, H), (H, H), (I, H), (I, H), (H, I)]
+    XH = torch.randn(M, H1, generator=g, device="cuda")
+    XI = torch.randn(M, I1, generator=g, device="cuda")
+    q = {k: torch.empty((M, k), dtype=torch.int8, device="cuda") for k in (H1, I1)}
+    sc = {k: torch.empty(M, dtype=torch.float64, device="cuda") for k in (H1, I1)}
+    til = {k: torch.empty(lib.tb_gemm_act_bytes(M, k), dtype=torch.uint8, device="cuda")
+           for k in (H1, I1)}
+    shapes = [(H1, H1), (KV, H1), (KV, H1), (H1, H1), (I1, H1), (I1, H1), (H1, I1)]
     ops = 2 * M * sum(n * k for n, k in shapes)
     layers = []
     for _ in range(copies):
@@ -549,214 +678,227 @@ def run_prefill(torch, tb, copies=2, reps=10):
             del w
             main, _ = p.tiled()
             out = torch.empty((M, n), dtype=torch.float32, device="cuda")
-            qa, t = tiled[k]
-            d.tiled, d.rows, d.cols, d.act_tiled = main.data_ptr(), n, k, t.data_ptr()
-            d.a_scale, d.w_scale, d.out32 = qa.scales.data_ptr(), float(p.scale), out.data_ptr()
+            d.tiled, d.rows, d.cols, d.act_tiled = main.data_ptr(), n, k, til[k].data_ptr()
+            d.a_scale, d.w_scale, d.out32 = sc[k].data_ptr(), float(p.scale), out.data_ptr()
             keep.append((p, main, out))
         layers.append((descs, keep))
-    s = L.stream_ptr()
 
-    def run(i):
-        L.check(lib.tb_gemm_batch(L.I2S, len(shapes), C.cast(layers[i % copies][0], C.c_void_p),
-                                  M, s), "gemm_batch")
+    def gemm(j):
+        L.check(lib.tb_gemm_batch(L.I2S, len(shapes), C.cast(layers[j % copies][0], C.c_void_p),
+                                  M, L.stream_ptr()), "gemm_batch")
 
-    def timed(fn, n):
-        fn(0)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(n):
-            fn(i)
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / n
+    def layer(j, xh=XH, xi=XI):
+        for x, k in ((xh, H1), (xi, I1)):
+            quantize_into(x, q[k], sc[k])
+            L.check(lib.tb_gemm_tile_act(q[k].data_ptr(), M, k, k, til[k].data_ptr(),
+                                         L.stream_ptr()), "gemm_tile_act")
+        gemm(j)
 
-    ms = timed(run, reps)
+    layer(0)
+    torch.cuda.synchronize()
+    ms, _ = graph_time(torch, lambda: [layer(j) for j in range(reps)])
+    ms /= reps
+    ms_gemm, _ = graph_time(torch, lambda: [gemm(j) for j in range(reps)])
+    ms_gemm /= reps
     a = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda")
     bt = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda").t()
-    peak_ms = timed(lambda i: torch._int_mm(a, bt), 5)
-    peak = 2 * 8192 ** 3 / (peak_ms * 1e-3) / 1e12
+    pk_ms, _ = graph_time(torch, lambda: [torch._int_mm(a, bt) for _ in range(5)])
+    peak = 2 * 8192 ** 3 / (pk_ms / 5 * 1e-3) / 1e12
+    del a, bt
     tops = ops / (ms * 1e-3) / 1e12
-    return {"workload": "cfg3: one Llama-3-8B-shaped layer (q,k,v,o,gate,up,down), M=512, I2_S, "
-                        "one grouped tcgen05 kind::i8 launch",
-            "tops": round(tops, 1), "us_per_layer": round(ms * 1e3, 1), "gop": round(ops / 1e9, 1),
-            "peak_tops": round(peak, 1), "peak_kind": "cuBLASLt int8 torch._int_mm 8192^3, measured",
-            "frac": round(tops / peak, 4),
-            "frac_vs_nominal_4500": round(tops / 4500.0, 4)}
+    tops_g = ops / (ms_gemm * 1e-3) / 1e12
+    out = {"workload": "cfg3: one Llama-3-8B-shaped layer (q,k,v,o,gate,up,down), M=512, I2_S: "
+                       "quantise + tile + one grouped tcgen05 kind::i8 GEMM launch",
+           "value": round(M * 1000.0 / ms, 1), "unit": "tokens/s (prefill, one layer)",
+           "tops": round(tops, 1), "us_per_layer": round(ms * 1e3, 1),
+           "gemm_only_tops": round(tops_g, 1), "gemm_only_us": round(ms_gemm * 1e3, 1),
+           "gop": round(ops / 1e9, 1),
+           "roofline": {"bound": "tensor", "achieved": round(tops_g, 1), "peak": round(peak, 1),
+                        "unit": "TOPS", "frac": round(tops_g / peak, 4),
+                        "frac_vs_nominal_4500": round(tops_g / 4500.0, 4),
+                        "kernel": "tgemm_kernel (tcgen05.mma kind::i8, TMEM accumulators)",
+                        "peak_kind": "cuBLASLt int8 (torch._int_mm 8192^3) measured in this run",
+                        "traffic": None}}
+    if not args.no_e2e:
+        xh_h = torch.randn(M, H1).pin_memory()
+        xi_h = torch.randn(M, I1).pin_memory()
+        outs_h = [torch.empty((M, n), dtype=torch.float32).pin_memory() for n, _ in shapes]
+        xh_d, xi_d = torch.empty_like(XH), torch.empty_like(XI)
 
+        def e2e_layer():
+            xh_d.copy_(xh_h, non_blocking=True)
+            xi_d.copy_(xi_h, non_blocking=True)
+            layer(0, xh_d, xi_d)
+            for oh, (_, _, od) in zip(outs_h, layers[0][1]):
+                oh.copy_(od, non_blocking=True)
+        e2e_layer()
+        torch.cuda.synchronize()
+        n = 10
+        t0 = time.perf_counter()
+        for _ in range(n):
+            e2e_layer()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / n
+        rows = sum(nn for nn, _ in shapes)
+        out["e2e"] = {"value": round(M / dt, 1), "unit": "tokens/s (prefill, one layer)",
+                      "h2d_bytes_per_step": M * (H1 + I1) * 4, "d2h_bytes_per_step": M * rows * 4,
+                      "steps": n, "path": "pinned host f32 x_h, x_i -> H2D -> quantise + tile + "
+                                          "GEMM -> all 7 f32 [512, N] outputs D2H; wall clock"}
+    if not args.no_cpu_baseline:
+        CO = _co()
+        packed = layers[0][1][0][0].data.cpu().numpy()  # q projection, 4096 x 4096
+        xs = XH[:16].cpu().numpy()
 
-def run_stack(torch, tb, name, fmt, tokens=1, steps=10):
-    """BASELINE configs 2 / 4: M-token decode through the whole layer stack,
-    one launch per layer (M=1) or glue + grouped GEMV per layer (M > 1)."""
-    from paper_2410_16144_b200.stack import STACKS, LayerStack
-    cfg = STACKS[name]
-    t0 = time.perf_counter()
-    st = LayerStack(cfg, fmt=fmt, seed=11, tokens=tokens)
-    build_s = time.perf_counter() - t0
-    g = torch.Generator(device="cuda").manual_seed(99)
-    L = st.nlayers
-    if tokens == 1:
-        XH = torch.randn(L, cfg["hidden"], generator=g, device="cuda")
-        XI = torch.randn(L, cfg["inter"], generator=g, device="cuda")
-        xh, xi = list(XH), list(XI)
-        glues = None
-    else:
-        XH = torch.randn(L, tokens, cfg["hidden"], generator=g, device="cuda")
-        XI = torch.randn(L, tokens, cfg["inter"], generator=g, device="cuda")
-        xh = xi = None
-        glues = st.make_glues(XH, XI)
-    st.token_pass(xh, xi, glues)
-    torch.cuda.synchronize()
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(s):
-        with torch.cuda.graph(graph, stream=s):
-            for _ in range(steps):
-                st.token_pass(xh, xi, glues)
-    graph.replay()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    graph.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    peak, _ = measured_peak()
-    gbs = st.algo_bytes / (ms * 1e-3) / 1e9
-    out = {"workload": f"{name}: {L} layers, hidden {cfg['hidden']}, {fmt.upper()}, M={tokens}",
-           "tokens_per_s": round(tokens * 1000.0 / ms, 1), "ms_per_token_pass": round(ms, 4),
-           "algo_bytes_per_pass": int(st.algo_bytes), "hbm_gbs": round(gbs, 1),
-           "frac": round(gbs / peak, 4), "launches_per_pass": L + 1 if tokens == 1 else 2 * L + 1,
-           "build_s": round(build_s, 1)}
-    del graph, st
+        def one(x, t):
+            qq, _ = CO.quantize(x, 4)
+            CO.gemv_i2s(packed, qq, t)
+        ths, ncpu = cpu_threads()
+        rate, t, cnt = time_cpu(one, lambda j: (xs[j % 16],), args.cpu_budget / 4, ths)
+        # q-projection GEMVs/s -> layer tokens/s by the MAC ratio
+        frac_q = (H1 * H1) / sum(nn * kk for nn, kk in shapes)
+        out["cpu_baseline"] = {"value": round(rate * frac_q, 3),
+                               "unit": "tokens/s (prefill, one layer)",
+                               "tops": round(rate * 2 * H1 * H1 / 1e12, 5), "cores": t,
+                               "kind": "port",
+                               "sample": f"{cnt} per-token q-projection GEMVs (4096x4096, quantise"
+                                         f" + byte-table gather; the reference has no GEMM, "
+                                         f"SPEC.md:346) on {t} thread(s), scaled to the "
+                                         f"7-projection layer by MACs; best of {ths}; {ncpu} CPUs "
+                                         f"({cpu_model()})"}
+    del layers
     torch.cuda.empty_cache()
     return out
 
 
-def run_cfg0(torch, tb, copies=32, steps=200):
-    """BASELINE configs[0]: one I2_S GEMV, M=1, 4096 x 4096 -- one fused
-    launch per token (quantise + GEMV + previous finalize), rotating over
-    32 weight copies (134 MB > L2) in a CUDA graph."""
-    n = k = 4096
-    g = torch.Generator(device="cuda").manual_seed(3)
-    steps_obj = []
-    for _ in range(copies):
-        w = torch.randn(n, k, generator=g, device="cuda") * 0.02
-        plan = tb.GemvPlan(tb.encode_i2s(tb.ternarize_weights(w, n, k)), out_dtype=torch.float32)
-        steps_obj.append(tb.GemvStep([(plan, 0)], [k]))
-        del w
-    X = torch.randn(16, k, generator=g, device="cuda")
+# ---------------------------------------------------------------------------
+# --impl reference
+# ---------------------------------------------------------------------------
 
-    def run(cnt):
-        for i in range(cnt):
-            steps_obj[i % copies].run([X[i % 16]], prev=steps_obj[(i - 1) % copies])
-        steps_obj[(cnt - 1) % copies].finalize()
-
-    run(copies)
-    torch.cuda.synchronize()
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(s):
-        with torch.cuda.graph(graph, stream=s):
-            run(steps)
-    graph.replay()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    graph.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    us = e0.elapsed_time(e1) * 1e3 / steps
-    algo = n * k // 4 + k + 4 * n
-    peak, _ = measured_peak()
-    return {"workload": "cfg0: I2_S GEMV M=1, 4096x4096, one fused launch per token",
-            "tokens_per_s": round(1e6 / us, 1), "us_per_gemv": round(us, 3),
-            "algo_bytes": algo, "hbm_gbs": round(algo / (us * 1e-6) / 1e9, 1),
-            "frac": round(algo / (us * 1e-6) / 1e9 / peak, 4),
-            "note": "4.2 MB per launch: launch/latency-bound, not bandwidth-bound"}
-
-
-def run_reference(args):
-    """--impl reference: the C port of the reference CPU kernels, all host threads."""
-    import torch  # noqa: F401  (weights are generated with the same packer)
-    from oracle import c_oracle as CO
+def host_stack_layer(seed, cfg):
+    """One cfg4 layer generated on the host: seeded N(0, 0.02) float32 latent
+    matrices, absmean-ternarised (core.py:104-113 arithmetic, in row blocks)
+    and packed to the reference I2_S bytes (packing.py:200-206)."""
     from oracle import ternpack_oracle as O
+    from paper_2410_16144_b200.stack import stack_shapes
+    mats = []
+    for mi, (name, rows, cols, src) in enumerate(stack_shapes(cfg)):
+        rng = np.random.default_rng(seed * 1_000_003 + mi)
+        w = rng.standard_normal((rows, cols), dtype=np.float32)
+        w *= np.float32(0.02)
+        blk = max(1, (64 << 20) // (8 * cols))
+        tot = 0.0
+        for r0 in range(0, rows, blk):
+            tot += float(np.abs(w[r0:r0 + blk].astype(np.float64)).sum())
+        scale = tot / (rows * cols)
+        packed = np.empty((rows, -(-cols // 4)), dtype=np.uint8)
+        for r0 in range(0, rows, blk):
+            v = np.clip(O.round_half_away(w[r0:r0 + blk].astype(np.float64) / scale), -1, 1)
+            packed[r0:r0 + blk] = O.encode_i2s(v.astype(np.int8))
+        del w
+        mats.append(((packed,), src))
+    return mats
 
-    rng = np.random.default_rng(1000)
-    mats = {}
-    for name, rows, cols in (("gate", I, H), ("up", I, H), ("down", H, I)):
-        v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)  # ternary draw (bench.py:102)
-        mats[name] = O.encode_tl1(v)
-    run = cpu_token_runner(mats["gate"], mats["up"], mats["down"])
-    threads = os.cpu_count() or 1
-    xs = np.random.default_rng(7)
-    XH = xs.standard_normal((NX, H)).astype(np.float32)
-    XI = xs.standard_normal((NX, I)).astype(np.float32)
-    for i in range(args.warmup):
-        run(XH[i % NX], XI[i % NX], threads)
+
+def run_reference(args, world):
+    """The reference's CPU path (its byte-table kernels, C port in oracle/c)
+    on the headline workload, all host threads: each timed step is one layer
+    of the 80-layer token pass (2 quantisations + 7 GEMVs), value = 1 / (80 x
+    mean layer time)."""
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        run(XH[i % NX], XI[i % NX], threads)
-    dt = (time.perf_counter() - t0) / args.steps
-    v = round(1.0 / dt, 3)
-    return {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": 0,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i8",
-        "data": "synthetic", "config": {"workload": "cfg1: TL1 FFN block, gate/up 4096->14336 + "
-                                                    "down 14336->4096, M=1", "format": "TL1"},
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} timed TL1 FFN tokens, {threads} OpenMP threads, "
-                                   f"C port of the reference byte-table kernels (oracle/c); "
-                                   f"reference package itself is not shipped to the box"},
-        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    mats = host_stack_layer(STACK_SEED, CFG4)
+    gen_s = time.perf_counter() - t0
+    h, i, L = CFG4["hidden"], CFG4["inter"], CFG4["layers"]
+    run = cpu_stack_layer("i2s", mats, h, i)
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(7)
+    X = [(rng.standard_normal(h).astype(np.float32), rng.standard_normal(i).astype(np.float32))
+         for _ in range(4)]
+    for j in range(args.warmup):
+        run(*X[j % 4], threads)
+    t0 = time.perf_counter()
+    for j in range(args.steps):
+        run(*X[j % 4], threads)
+    dt_layer = (time.perf_counter() - t0) / args.steps
+    v = round(1.0 / (L * dt_layer), 5)
+    sample = (f"{args.steps} timed layers of the cfg4 token pass (2 quantise + 7 I2_S byte-table "
+              f"GEMVs, M=1) on {threads} OpenMP threads, tokens/s = 1 / (80 x layer time); C port "
+              f"of the reference byte-table kernels (oracle/c: _fast.byte_gemv + i2s tables); "
+              f"{threads} CPUs ({cpu_model()}); weights generated on the host in {gen_s:.0f} s")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(L * dt_layer * 1e3, 2), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "i8",
+            "data": "synthetic (seeded N(0,0.02) latent weights -> absmean ternary I2_S; "
+                    "N(0,1) activations)",
+            "config": headline_config(world),
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
 
 
-def _local_device(torch):
-    """LOCAL_RANK's GPU.  TB_BENCH_SHARE_GPU=1 folds ranks onto the visible
-    GPUs -- a functional check of the tp > 1 code path on a 1-GPU box (with
-    TB_BENCH_DIST_BACKEND=gloo), never a measurement."""
-    lr = int(os.environ.get("LOCAL_RANK", 0))
-    if os.environ.get("TB_BENCH_SHARE_GPU") == "1":
-        lr %= torch.cuda.device_count()
-    return lr
+# ---------------------------------------------------------------------------
+
+def _spawn(args):
+    """--gpus N without a torchrun environment: launch the N ranks ourselves."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--collective", default="peer", choices=["peer", "nccl"],
+                    help="tp > 1: row-parallel reduction by our peer-memory kernel or NCCL")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="skip the other BASELINE configs")
+    ap.add_argument("--configs", default="cfg0,cfg1,cfg2:i2s,cfg2:tl2,cfg3,cfg4:m8",
+                    help="secondary config lines (comma list)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-prefill", action="store_true")
-    ap.add_argument("--stacks", default="cfg0,cfg2:i2s:1,cfg2:tl2:1",
-                    help="layer-stack decode lines, name:fmt:M comma list ('' = none); "
-                         "e.g. cfg4:i2s:1,cfg4:i2s:8")
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--parallel", default="dp", choices=["dp", "tp"],
-                    help="N > 1: independent replicas (dp, default) or tensor parallel (tp)")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
 
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(run_reference(args)), flush=True)
+            print(json.dumps(run_reference(args, world)), flush=True)
         return
 
+    import torch
     if world > 1:
-        import torch
         import torch.distributed as dist
-        torch.cuda.set_device(_local_device(torch))
+        lr = int(os.environ.get("LOCAL_RANK", 0))
+        if os.environ.get("TB_BENCH_SHARE_GPU") == "1":  # functional check only (1-GPU box)
+            lr %= torch.cuda.device_count()
+        torch.cuda.set_device(lr)
         dist.init_process_group(os.environ.get("TB_BENCH_DIST_BACKEND", "nccl"))
-    res = run_gpu(args, rank, world)
+    res = run_headline(args, rank, world)
+    if rank == 0 and world == 1 and not args.headline_only:
+        import paper_2410_16144_b200 as tb
+        res["configs"] = {}
+        fns = {"cfg0": lambda: run_cfg0(torch, tb, args),
+               "cfg1": lambda: run_cfg1(torch, tb, args),
+               "cfg2:i2s": lambda: run_stack_cfg(torch, tb, args, "cfg2", "i2s", 1),
+               "cfg2:tl2": lambda: run_stack_cfg(torch, tb, args, "cfg2", "tl2", 1),
+               "cfg3": lambda: run_cfg3(torch, tb, args),
+               "cfg4:m8": lambda: run_stack_cfg(torch, tb, args, "cfg4", "i2s", 8, passes=4)}
+        for name in [c for c in args.configs.split(",") if c]:
+            try:
+                res["configs"][name] = fns[name]()
+            except Exception as e:  # a secondary line must not lose the headline
+                res["configs"][name] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

@@ -244,6 +244,19 @@ int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
                          const int32_t *src, int64_t ninputs, const int64_t *input_k,
                          void *table_host, int64_t *total_chunks,
                          int64_t *max_entries);
+/* As tb_gemv_step_prepare, plus col0[j] (NULL = all 0): job j contracts input
+ * columns [col0[j], col0[j] + descs[j].cols) of input src[j] -- a row-parallel
+ * (K-sharded) projection whose per-token scale is that of the FULL input
+ * vector (core.py:128: absmax over the whole token).  col0 must be a multiple
+ * of one record chunk (64 weights for I2_S / TL1, 96 for TL2); a shard that
+ * ends before the input does is zero-padded to whole chunks by tb_repack, so
+ * the columns it does not own contribute exactly 0.
+ * Replaces nothing in the reference (its thread pool splits rows only,
+ * kernels.py:181-186); it is the SURVEY §8(e) row-parallel shard.            */
+int tb_gemv_step_prepare_cols(int fmt, int64_t njobs, const tb_gemv_desc *descs,
+                              const int32_t *src, const int64_t *col0, int64_t ninputs,
+                              const int64_t *input_k, void *table_host,
+                              int64_t *total_chunks, int64_t *max_entries);
 int tb_gemv_step_launch(int fmt, const void *table_device, int64_t njobs,
                         int64_t total_chunks, int64_t ninputs,
                         const tb_step_input *inputs, int32_t flags,
@@ -307,6 +320,43 @@ int tb_gemv_ref_int32(const int8_t *values, int64_t rows, int64_t cols,
                       const int8_t *act, int32_t *acc_out, void *stream);
 int tb_gemv_f32_ref(const int8_t *values, int64_t rows, int64_t cols,
                     float w_scale, const float *x, float *out, void *stream);
+
+/* ---- tensor parallel: row-parallel reduction over NVLink peer memory -----
+ * (allreduce.cu; SURVEY §8(e).  The reference has no multi-device path; its
+ * determinism contract -- any partition of the rows gives the same result,
+ * SPEC.md:333 / kernels.py:181-186 -- is kept by summing the row-parallel
+ * shards' int32 partial accumulators exactly before the scale of
+ * core.py:99-101.)  A rank's partials of every layer live in one symmetric
+ * buffer (tb_sym_alloc) that every peer maps (tb_ipc_*); flags are a
+ * symmetric uint32[8] per rank, ctrl a rank-local zeroed uint32[2].
+ * tb_rowpar_allreduce: one launch per layer, a programmatic dependent of the
+ * step that finalised the partials; signals this rank's epoch to every peer,
+ * waits for theirs, sums layer_off + [seg.off, seg.off + seg.n) over all
+ * ranks and writes out32 = f32(f64(sum) * w_scale * *a_scale) (+ the int32
+ * sums if acc_out).  ctas = 0: automatic.  Graph-capturable.
+ * tb_rowpar_allreduce_emulated: all `world` ranks in ONE grid on one device
+ * (tests): parts/flags/ctrl per rank, segs [world][nseg].                    */
+typedef struct tb_rowpar_seg {
+  int64_t off, n;
+  double w_scale;
+  const double *a_scale;
+  float *out32;
+  int32_t *acc_out;
+} tb_rowpar_seg;
+int tb_sym_alloc(int64_t bytes, void **ptr);  /* cudaMalloc + zero (IPC-able) */
+int tb_sym_free(void *ptr);
+int tb_ipc_handle_bytes(void);
+int tb_ipc_get_handle(const void *ptr, void *handle_out);
+int tb_ipc_open(const void *handle, void **ptr);
+int tb_ipc_close(void *ptr);
+int tb_rowpar_allreduce(int world, int rank, const int32_t *const *parts,
+                        uint32_t *const *flags, uint32_t *ctrl, int64_t layer_off,
+                        int64_t nseg, const tb_rowpar_seg *segs, int32_t ctas,
+                        void *stream);
+int tb_rowpar_allreduce_emulated(int world, const int32_t *const *parts,
+                                 uint32_t *const *flags, uint32_t *const *ctrl,
+                                 int64_t layer_off, int64_t nseg,
+                                 const tb_rowpar_seg *segs, int32_t ctas, void *stream);
 
 #ifdef __cplusplus
 }

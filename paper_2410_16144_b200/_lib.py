@@ -57,6 +57,7 @@ _SIGS = {
     "tb_gemv_batch_launch": (_i32, [_i32, _p, _i64, _i64, _i32, _i64, _i32, _p]),
     "tb_step_glue": (_i32, [_p, _i64, _i64, _i64, _p, _p]),
     "tb_gemv_step_prepare": (_i32, [_i32, _i64, _p, _p, _i64, _p, _p, _p, _p]),
+    "tb_gemv_step_prepare_cols": (_i32, [_i32, _i64, _p, _p, _p, _i64, _p, _p, _p, _p]),
     "tb_gemv_step_launch": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _i32, _p, _i64, _p, _p, _p]),
     "tb_gemv_batch_finalize": (_i32, [_p, _i64, _i64, _p]),
     "tb_gemv_lut": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _p, _p]),
@@ -66,6 +67,14 @@ _SIGS = {
     "tb_gemm_i8": (_i32, [_i32, _p, _i64, _i64, _p, _i64, _i64, _p, _f64, _p, _p, _p, _p, _p]),
     "tb_gemm_act_bytes": (_i64, [_i64, _i64]),
     "tb_gemm_tile_act": (_i32, [_p, _i64, _i64, _i64, _p, _p]),
+    "tb_sym_alloc": (_i32, [_i64, _p]),
+    "tb_sym_free": (_i32, [_p]),
+    "tb_ipc_handle_bytes": (_i32, []),
+    "tb_ipc_get_handle": (_i32, [_p, _p]),
+    "tb_ipc_open": (_i32, [_p, _p]),
+    "tb_ipc_close": (_i32, [_p]),
+    "tb_rowpar_allreduce": (_i32, [_i32, _i32, _p, _p, _p, _i64, _i64, _p, _i32, _p]),
+    "tb_rowpar_allreduce_emulated": (_i32, [_i32, _p, _p, _p, _i64, _i64, _p, _i32, _p]),
 }
 
 class GemvDesc(C.Structure):
@@ -90,6 +99,13 @@ class GemmDesc(C.Structure):
     _fields_ = [("tiled", _p), ("rows", _i64), ("cols", _i64), ("act_tiled", _p),
                 ("a_scale", _p), ("w_scale", _f64), ("acc_out", _p), ("out64", _p),
                 ("out32", _p)]
+
+
+class RowparSeg(C.Structure):
+    """Mirror of tb_rowpar_seg (include/ternary_b200.h)."""
+
+    _fields_ = [("off", _i64), ("n", _i64), ("w_scale", _f64), ("a_scale", _p), ("out32", _p),
+                ("acc_out", _p)]
 
 
 class StepInput(C.Structure):

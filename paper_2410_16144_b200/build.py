@@ -21,7 +21,8 @@ LIB = OUT_DIR / "libternary_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
-SOURCES = ["abi.cu", "quantize.cu", "pack.cu", "gemv.cu", "gemv_aux.cu", "gemm_tc.cu"]
+SOURCES = ["abi.cu", "quantize.cu", "pack.cu", "gemv.cu", "gemv_aux.cu", "gemm_tc.cu",
+           "allreduce.cu"]
 
 
 def _sources():

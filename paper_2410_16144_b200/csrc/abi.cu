@@ -30,7 +30,7 @@ extern "C" const char *tb_strerror(int status) {
   }
 }
 
-extern "C" int tb_abi_version(void) { return 3; }
+extern "C" int tb_abi_version(void) { return 4; }
 
 extern "C" int tb_device_sm_count(int device) {
   int v = 0;

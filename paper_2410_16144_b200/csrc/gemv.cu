@@ -146,6 +146,8 @@ struct GemvJob {
   int start;  // first flat chunk of this job
   int end;    // one past its last flat chunk (start + T * C)
   int src;    // fused step: index of the input vector this job contracts
+  int c0;     // fused step: first record chunk of that input (a row-parallel
+              // K-shard contracts input columns [64 c0, ...) -- 96 c0 for TL2)
 };
 
 // Fused decode step (tgemv_kernel<FMT, 1, true>): the launch quantises its own
@@ -873,7 +875,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       C = J.C;
       M = J.M;
       T = (J.end - J.start) / J.C;
-      if constexpr (kFused) rtab = rtab_base + b.in.off[J.src];
+      if constexpr (kFused) rtab = rtab_base + b.in.off[J.src] + J.c0 * F::kRecBytes;
     };
     load_shape();
     Acc<FMT, MT> acc;
@@ -1181,6 +1183,7 @@ static int make_job(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign, in
   J.start = (int)start;
   J.end = (int)(start + T * C);
   J.src = 0;
+  J.c0 = 0;
   return TB_OK;
 }
 
@@ -1347,29 +1350,43 @@ extern "C" int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t n
   return launch_batch(fmt, b, max_m, static_cast<cudaStream_t>(stream));
 }
 
-extern "C" int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
-                                    const int32_t *src, int64_t ninputs, const int64_t *input_k,
-                                    void *table_host, int64_t *total_chunks,
-                                    int64_t *max_entries) {
+extern "C" int tb_gemv_step_prepare_cols(int fmt, int64_t njobs, const tb_gemv_desc *descs,
+                                         const int32_t *src, const int64_t *col0,
+                                         int64_t ninputs, const int64_t *input_k,
+                                         void *table_host, int64_t *total_chunks,
+                                         int64_t *max_entries) {
   if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !descs || !src || !input_k ||
       ninputs < 1 || ninputs > kMaxStepInputs || !table_host || !total_chunks || !max_entries)
     return TB_ERR_ARGUMENT;
+  // one record chunk = 16 packed bytes = 64 I2_S / TL1 weights, 96 TL2 weights
+  const int64_t chunk_w = fmt == TB_TL2 ? 96 : 64;
   GemvJob *host = static_cast<GemvJob *>(table_host);
   int64_t start = 0, maxE = 1;
   for (int64_t j = 0; j < njobs; ++j) {
     const tb_gemv_desc &d = descs[j];
-    if (src[j] < 0 || src[j] >= ninputs || d.M != 1 || d.cols != input_k[src[j]])
+    const int64_t c0 = col0 ? col0[j] : 0;
+    if (src[j] < 0 || src[j] >= ninputs || d.M != 1 || c0 < 0 || c0 % chunk_w ||
+        (c0 == 0 ? d.cols != input_k[src[j]] : c0 + d.cols > input_k[src[j]]))
       return TB_ERR_ARGUMENT;
     int st = make_job(fmt, d.tiled, d.tiled_sign, d.rows, d.cols, nullptr, 1, d.a_scale,
                       d.w_scale, d.workspace, d.acc_out, d.out64, d.out32, start, host[j], true);
     if (st != TB_OK) return st;
     host[j].src = src[j];
+    host[j].c0 = (int)(c0 / chunk_w);
     start = host[j].end;
     maxE = std::max(maxE, (int64_t)host[j].Npad);
   }
   *total_chunks = start;
   *max_entries = maxE;
   return TB_OK;
+}
+
+extern "C" int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
+                                    const int32_t *src, int64_t ninputs, const int64_t *input_k,
+                                    void *table_host, int64_t *total_chunks,
+                                    int64_t *max_entries) {
+  return tb_gemv_step_prepare_cols(fmt, njobs, descs, src, nullptr, ninputs, input_k, table_host,
+                                   total_chunks, max_entries);
 }
 
 extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t njobs,

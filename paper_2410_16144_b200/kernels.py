@@ -402,7 +402,10 @@ class GemvStep:
         import numpy as np
 
         lib = L.load()
-        fmts = {p.p.FMT for p, _ in pairs}
+        # (plan, input) or (plan, input, col0): a row-parallel K-shard reads
+        # input columns [col0, col0 + cols) and uses the full input's scale
+        pairs = [tuple(pr) if len(pr) == 3 else (pr[0], pr[1], 0) for pr in pairs]
+        fmts = {p.p.FMT for p, _, _ in pairs}
         if len(fmts) != 1:
             raise ValueError("one format per step")
         if not 1 <= len(input_k) <= 4:
@@ -416,12 +419,18 @@ class GemvStep:
                       else torch.zeros(len(input_k), dtype=torch.int32, device=dev))
         descs = (L.GemvDesc * len(pairs))()
         src = (C.c_int32 * len(pairs))()
+        col0 = (C.c_int64 * len(pairs))()
         ks = (C.c_int64 * len(input_k))(*self.input_k)
-        for i, (d, (plan, v)) in enumerate(zip(descs, pairs)):
+        chunk_w = 96 if self.fmt == L.TL2 else 64
+        for i, (d, (plan, v, c0)) in enumerate(zip(descs, pairs)):
             if not 0 <= v < len(input_k):
                 raise ValueError("input index out of range")
-            if plan.p.cols != self.input_k[v]:
+            if c0 % chunk_w or c0 < 0:
+                raise ValueError(f"col0 must be a non-negative multiple of {chunk_w}")
+            if (plan.p.cols != self.input_k[v]) if c0 == 0 else \
+                    (c0 + plan.p.cols > self.input_k[v]):
                 raise ValueError("dimension mismatch: input length != matrix cols")
+            col0[i] = c0
             d.tiled = plan.main.data_ptr()
             d.tiled_sign = plan.sign.data_ptr() if plan.sign is not None else None
             d.rows, d.cols = plan.p.rows, plan.p.cols
@@ -435,9 +444,9 @@ class GemvStep:
         host = np.zeros(lib.tb_gemv_job_bytes() * len(pairs), dtype=np.uint8)
         total = C.c_int64()
         maxe = C.c_int64()
-        L.check(lib.tb_gemv_step_prepare(self.fmt, len(pairs), C.cast(descs, C.c_void_p),
-                                         C.cast(src, C.c_void_p), len(input_k),
-                                         C.cast(ks, C.c_void_p),
+        L.check(lib.tb_gemv_step_prepare_cols(self.fmt, len(pairs), C.cast(descs, C.c_void_p),
+                                              C.cast(src, C.c_void_p), C.cast(col0, C.c_void_p),
+                                              len(input_k), C.cast(ks, C.c_void_p),
                                          host.ctypes.data_as(C.c_void_p), C.byref(total),
                                          C.byref(maxe)), "gemv_step_prepare")
         self.table = torch.from_numpy(host).to(dev)
@@ -532,13 +541,13 @@ class HostStep:
         self.x_dev = [self.x_dev_all[o:o + k] for o, k in zip(offs, input_k)]
         self.out_host = []
         host_pairs = []
-        for plan, v in pairs:
+        for plan, *rest in pairs:
             o = torch.empty((1, plan.p.rows), dtype=out_dtype).pin_memory()
             self.out_host.append(o[0])
             host_pairs.append((types.SimpleNamespace(
                 p=plan.p, main=plan.main, sign=plan.sign, ws=plan.ws, acc=None,
                 out32=o if out_dtype == torch.float32 else None,
-                out64=o if out_dtype == torch.float64 else None), v))
+                out64=o if out_dtype == torch.float64 else None), *rest))
         self.flags_host = torch.zeros(len(input_k), dtype=torch.int32).pin_memory()
         self._flags_np = self.flags_host.numpy()  # shares the pinned buffer
         self.step = GemvStep(host_pairs, input_k, flags=self.flags_host, isolated=True)
@@ -609,8 +618,8 @@ class HostPipeline:
         if steps < 1 or block < 1:
             raise ValueError("steps and block must be >= 1")
         npairs = len(slot_pairs[0])
-        rows = [plan.p.rows for plan, _ in slot_pairs[0]]
-        if any(len(sp) != npairs or [plan.p.rows for plan, _ in sp] != rows for sp in slot_pairs):
+        rows = [pr[0].p.rows for pr in slot_pairs[0]]
+        if any(len(sp) != npairs or [pr[0].p.rows for pr in sp] != rows for sp in slot_pairs):
             raise ValueError("every slot must hold the same projections")
         dev = slot_pairs[0][0][0].main.device
         self.input_k = [int(k) for k in input_k]
@@ -632,15 +641,16 @@ class HostPipeline:
         # non-finite verdicts, sticky and zero-copy in mapped pinned memory
         self._flags = torch.zeros((R, len(self.input_k)), dtype=torch.int32).pin_memory()
         self._flags_np = self._flags.numpy()
-        self._ws = [[torch.zeros_like(plan.ws) for plan, _ in sp] for sp in slot_pairs]
+        self._ws = [[torch.zeros_like(pr[0].ws) for pr in sp] for sp in slot_pairs]
         self._steps = []
         for i in range(steps):
             r = i % R
             pairs = []
-            for (plan, v), ws, oo in zip(slot_pairs[r], self._ws[r], ooffs):
+            for (plan, *rest), ws, oo in zip(slot_pairs[r], self._ws[r], ooffs):
                 o = self._o_dev[i:i + 1, oo:oo + plan.p.rows]
                 pairs.append((types.SimpleNamespace(p=plan.p, main=plan.main, sign=plan.sign,
-                                                    ws=ws, acc=None, out32=o, out64=None), v))
+                                                    ws=ws, acc=None, out32=o, out64=None),
+                              *rest))
             st = GemvStep(pairs, self.input_k, flags=self._flags[r], sticky_flags=True)
             st.bind([self._x_dev[i, o:o + k] for o, k in zip(offs, self.input_k)])
             self._steps.append(st)

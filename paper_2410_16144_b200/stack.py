@@ -1,4 +1,4 @@
-"""Layer-stack decode runner for BASELINE configs 2 and 4 (M=1 and small M).
+"""Layer-stack decode runner for BASELINE configs 2 and 4, tensor parallel.
 
 The reference times a stack as per-layer GEMV passes over freshly quantised
 activations (bench._token_pass_int, pkg/src/ternpack/bench.py:138-153: per
@@ -9,7 +9,30 @@ one grouped GEMV, the previous layer's outputs finalised after its own work);
 for M > 1 a layer is a StepGlue (finalise + quantise M tokens) and a
 GemvBatch.  Weights are generated like BASELINE.json's configs: seeded
 N(0, 0.02) latent matrices, absmean-ternarised on the GPU (core.py:104-113),
-packed to I2_S or TL2 and repacked to the tiled layout.
+packed to I2_S / TL1 / TL2 and repacked to the tiled layout.
+
+Tensor parallel (``tp_world > 1``; one process per GPU):
+
+* column-parallel q/k/v/gate/up: rank r owns rows [r0, r1) of the packed
+  matrix (a byte slice, tp.column_shard) and writes its output rows only;
+* row-parallel o/down: rank r owns input columns [k0, k1) (tp.row_shard,
+  k0 a multiple of one record chunk), reads those columns of the replicated
+  input vector -- quantised whole, so the per-token scale is the reference's
+  absmax over the full token (core.py:128) -- and produces int32 partial
+  accumulators.  Once a layer's step has been finalised (by the next
+  layer's step), the layer's partials (o and down, one contiguous int32
+  buffer) are summed over the ranks and only then scaled,
+  out = f64(sum) * w_scale * a_scale (core.py:99-101): integer sums are
+  exact and order independent, so every tp degree is bit-identical to tp=1
+  and to the reference.
+
+The sum goes through a ``Collective``: ``tp.PeerAllReduce`` (ours: one
+kernel over NVLink peer memory that sums and scales; the default),
+``tp.TorchAllReduce`` (NCCL / gloo through torch.distributed, then the
+scale kernel: the baseline) or ``tp.EmulatedGroup`` (all ranks in one
+process on one GPU, for tests).  The weight matrices are generated whole
+on every rank from the same seeds (so the weight scale is the full
+matrix's, as in the reference) and then sliced.
 """
 
 from __future__ import annotations
@@ -17,18 +40,23 @@ from __future__ import annotations
 import torch
 
 from . import _lib as L
+from . import tp as TP
 from .core import ternarize_weights
 from .kernels import ActRecords, GemvBatch, GemvPlan, GemvStep, StepGlue
-from .packing import encode_i2s, encode_tl1, encode_tl2
+from .packing import PackedI2S, PackedTL1, PackedTL2, encode_i2s, encode_tl1, encode_tl2
 
-__all__ = ["STACKS", "stack_shapes", "LayerStack"]
+__all__ = ["STACKS", "stack_shapes", "LayerStack", "ROW_PARALLEL", "packed_bytes"]
 
-# (hidden, q/o out, k/v out, intermediate, layers) -- BASELINE.json configs 2 and 4
+# (hidden, k/v out, intermediate, layers) -- BASELINE.json configs 2 and 4
 STACKS = {
     "cfg2": {"hidden": 4096, "kv": 1024, "inter": 14336, "layers": 32},
     "cfg4": {"hidden": 10240, "kv": 1280, "inter": 32768, "layers": 80},
 }
 _ENC = {"i2s": encode_i2s, "tl1": encode_tl1, "tl2": encode_tl2}
+_FMT = {"i2s": L.I2S, "tl1": L.TL1, "tl2": L.TL2}
+ROW_PARALLEL = ("o", "down")
+# one record chunk (16 packed bytes): the granularity of a row-parallel K-shard
+CHUNK_W = {"i2s": 64, "tl1": 64, "tl2": 96}
 
 
 def stack_shapes(cfg: dict):
@@ -39,58 +67,153 @@ def stack_shapes(cfg: dict):
 
 
 def packed_bytes(fmt: str, rows: int, cols: int) -> int:
+    """Reference packed size (packing.py:42-53)."""
     lib = L.load()
     if fmt == "tl2":
         return rows * (lib.tb_ref_row_bytes(L.TL2, cols) + lib.tb_ref_sign_row_bytes(cols))
-    return rows * lib.tb_ref_row_bytes(L.I2S if fmt == "i2s" else L.TL1, cols)
+    return rows * lib.tb_ref_row_bytes(_FMT[fmt], cols)
+
+
+def shard_plan(cfg: dict, fmt: str, rank: int, world: int):
+    """Per projection of one layer: (name, rows, cols, input, kind, lo, hi) --
+    kind 'col' owns rows [lo, hi), 'row' owns input columns [lo, hi), 'full'
+    is unsharded (world 1).  Row boundaries are whole 32-row tiles where the
+    sizes allow; column boundaries whole record chunks."""
+    out = []
+    for name, rows, cols, src in stack_shapes(cfg):
+        if world == 1:
+            out.append((name, rows, cols, src, "full", 0, rows))
+        elif name in ROW_PARALLEL:
+            lo, hi = TP.shard_range(cols, world, rank, CHUNK_W[fmt])
+            out.append((name, rows, cols, src, "row", lo, hi))
+        else:
+            lo, hi = TP.shard_range(rows, world, rank, 32 if rows % (32 * world) == 0 else 1)
+            out.append((name, rows, cols, src, "col", lo, hi))
+    return out
+
+
+def _slice(p, fmt: str, kind: str, lo: int, hi: int):
+    """Shard of a packed reference matrix as a packed matrix of its own."""
+    if kind == "full":
+        return p
+    if fmt == "tl2":
+        planes = (p.index_data, p.sign_data)
+    else:
+        planes = (p.data,)
+    if kind == "col":
+        sl = TP.column_shard(planes, lo, hi)
+        rows, cols = hi - lo, p.cols
+    else:
+        sl, cols = TP.row_shard(_FMT[fmt], planes, p.cols, lo, hi)
+        rows = p.rows
+    pad = {"i2s": 4, "tl1": 2, "tl2": 6}[fmt]
+    pc = -(-cols // pad) * pad
+    sl = tuple(t.contiguous() for t in sl)
+    if fmt == "i2s":
+        return PackedI2S(rows=rows, cols=cols, padded_cols=pc, data=sl[0], scale=p.scale,
+                         trusted=True)
+    if fmt == "tl1":
+        return PackedTL1(rows=rows, cols=cols, padded_cols=pc, data=sl[0], scale=p.scale,
+                         trusted=True)
+    return PackedTL2(rows=rows, cols=cols, padded_cols=pc, index_data=sl[0], sign_data=sl[1],
+                     scale=p.scale, trusted=True)
 
 
 class LayerStack:
-    """All layers of a config resident on one GPU, plus per-layer launch objects."""
+    """All layers of a config (this rank's shards) resident on one GPU, plus
+    the per-layer launch objects."""
 
     def __init__(self, cfg: dict, fmt: str = "i2s", seed: int = 0, tokens: int = 1,
-                 layers: int | None = None, device=None):
+                 layers: int | None = None, device=None, tp_rank: int = 0, tp_world: int = 1,
+                 collective=None, part_alloc=None):
         if fmt not in _ENC:
             raise ValueError(f"unknown format {fmt}")
+        if tp_world > 1 and tokens != 1:
+            raise ValueError("tensor-parallel stacks decode one token per step (M=1)")
+        if tp_world > 1 and collective is None:
+            raise ValueError("a tensor-parallel stack needs a collective")
         self.cfg, self.fmt, self.tokens = cfg, fmt, tokens
+        self.rank, self.world, self.coll = tp_rank, tp_world, collective
         self.nlayers = layers or cfg["layers"]
         dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
         self.shapes = stack_shapes(cfg)
+        self.plan = shard_plan(cfg, fmt, tp_rank, tp_world)
+        h, i = cfg["hidden"], cfg["inter"]
+        self.ks = [h, i]
+        # row-parallel partials of a layer: one contiguous int32 buffer
+        # [o rows | down rows] (symmetric across ranks for the peer kernel)
+        self.rp = [(j, s[1]) for j, s in enumerate(self.plan) if s[4] == "row"]
+        self.part_len = sum(r for _, r in self.rp)
+        self.parts = None
+        if part_alloc is None and collective is not None:
+            part_alloc = collective.part_alloc
+        if self.rp:
+            n = self.nlayers * self.part_len
+            self.parts = (part_alloc(n) if part_alloc is not None else
+                          torch.zeros(n, dtype=torch.int32, device=dev)).view(self.nlayers, -1)
+            self.rp_out = torch.empty((self.nlayers, self.part_len), dtype=torch.float32,
+                                      device=dev)
         self.layers = []
         gen = torch.Generator(device=dev)
         for li in range(self.nlayers):
             plans = []
-            for mi, (_, rows, cols, _) in enumerate(self.shapes):
+            for mi, (name, rows, cols, src, kind, lo, hi) in enumerate(self.plan):
                 gen.manual_seed(seed * 1_000_003 + li * 131 + mi)
                 w = torch.randn(rows, cols, generator=gen, device=dev) * 0.02
                 p = _ENC[fmt](ternarize_weights(w, rows, cols))
                 del w
-                plans.append(GemvPlan(p, max_tokens=tokens, out_dtype=torch.float32))
+                p = _slice(p, fmt, kind, lo, hi)
+                rowpar = kind == "row"
+                plan = GemvPlan(p, max_tokens=tokens,
+                                out_dtype=None if rowpar else torch.float32)
+                if rowpar:  # partials land in the layer's slice of the symmetric buffer
+                    off = sum(r for j, r in self.rp if j < mi)
+                    plan.acc = self.parts[li, off:off + rows].view(1, rows)
+                plans.append(plan)
             self.layers.append(plans)
-        self.algo_bytes = sum(packed_bytes(fmt, r, c) + tokens * c + 4 * tokens * r
-                              for _, r, c, _ in self.shapes) * self.nlayers
-        h, i = cfg["hidden"], cfg["inter"]
-        self.ks = [h, i]
+        # algorithmic bytes (SURVEY §8(d)) of THIS rank's shards: packed bytes
+        # + M * (columns contracted) int8 activations + 4 * M * (rows written)
+        self.algo_bytes = sum(packed_bytes(fmt, p.p.rows, p.p.cols) + tokens * p.p.cols
+                              + 4 * tokens * p.p.rows for p in self.layers[0]) * self.nlayers
         if tokens == 1:
-            self.steps = [GemvStep([(p, s[3]) for p, s in zip(plans, self.shapes)], self.ks)
+            self.steps = [GemvStep([(p, s[3], s[5] if s[4] == "row" else 0)
+                                    for p, s in zip(plans, self.plan)], self.ks)
                           for plans in self.layers]
         else:
             self.rec = [ActRecords(L.TL2 if fmt == "tl2" else L.I2S, tokens, k) for k in self.ks]
-            self.batches = [GemvBatch([(p, self.rec[s[3]]) for p, s in zip(plans, self.shapes)])
+            self.batches = [GemvBatch([(p, self.rec[s[3]]) for p, s in zip(plans, self.plan)])
                             for plans in self.layers]
             self.tail = StepGlue([])
+        if self.rp:
+            # what the reduction scales: per row-parallel projection
+            # (rows, w_scale, the step's device scale of its input)
+            self.rp_jobs = []
+            for li in range(self.nlayers):
+                segs, off = [], 0
+                for j, rows in self.rp:
+                    p = self.layers[li][j]
+                    segs.append((off, rows, float(p.p.scale), self.steps[li].scales[self.plan[j][3]]))
+                    off += rows
+                self.rp_jobs.append(segs)
+            self.coll.bind(self)
 
+    # ------------------------------------------------------------- decode
     def token_pass(self, xh, xi, glue_pool=None):
         """Launch one token pass (all layers); layer l reads xh[l], xi[l]
         (device float32 vectors [K] for M=1, or the fixed [M, K] buffers bound
         in ``glue_pool`` for M > 1).  Outputs of the last layer are finalised
-        at the end.  Capturable in a CUDA graph."""
+        at the end.  Capturable in a CUDA graph (with a capturable collective)."""
         if self.tokens == 1:
             prev = None
             for li, st in enumerate(self.steps):
                 st.run([xh[li], xi[li]], prev=prev)
+                if prev is not None and self.rp:
+                    self.coll.reduce_layer(self, li - 1)  # step li finalised layer li-1
                 prev = st
             prev.finalize()
+            if self.rp:
+                self.coll.reduce_layer(self, self.nlayers - 1)
         else:
             prev = None
             for li, b in enumerate(self.batches):
@@ -103,3 +226,15 @@ class LayerStack:
         """M > 1: one StepGlue per layer quantising rows of XH[l] / XI[l] ([M, K])."""
         return [StepGlue([(XH[li], self.rec[0]), (XI[li], self.rec[1])])
                 for li in range(self.nlayers)]
+
+    def outputs(self, li: int) -> dict:
+        """Layer li's fp32 outputs by projection name (after its reduction):
+        column shards give this rank's rows, row-parallel ones the full rows."""
+        res = {}
+        for j, (name, rows, cols, src, kind, lo, hi) in enumerate(self.plan):
+            if kind == "row":
+                off = sum(r for jj, r in self.rp if jj < j)
+                res[name] = self.rp_out[li, off:off + rows]
+            else:
+                res[name] = self.layers[li][j].out32[0]
+        return res

@@ -41,7 +41,7 @@ def test_python_binding_covers_header(lib):
 
 
 def test_host_only_entry_points(lib):
-    assert lib.tb_abi_version() == 3
+    assert lib.tb_abi_version() == 4
     assert lib.tb_strerror(0) == b"ok"
     assert b"argument" in lib.tb_strerror(1)
     for cols in (1, 2, 3, 4, 5, 6, 7, 12, 13, 768, 4096, 4092, 14336, 10240, 32768):

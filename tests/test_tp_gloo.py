@@ -150,3 +150,17 @@ def test_gloo_tensor_parallel(fmt, world):
         msgs.append(errors.get())
     assert all(p.exitcode == 0 for p in procs), msgs
     assert not msgs, msgs
+
+
+def test_stack_shard_plan_alignment():
+    """cfg4 shards: row-parallel K bounds on record chunks, column shards whole tiles."""
+    from paper_2410_16144_b200.stack import STACKS, shard_plan
+    for world in (2, 4, 8):
+        for r in range(world):
+            for name, rows, cols, src, kind, lo, hi in shard_plan(STACKS["cfg4"], "i2s", r, world):
+                if kind == "row":
+                    assert lo % 64 == 0 and (hi == cols or hi % 64 == 0)
+                else:
+                    assert lo % 32 == 0 and (hi - lo) * world == rows
+
+
