@@ -19,8 +19,9 @@ so every step streams from HBM with no flush needed).
   roofline  the fused step kernel (one launch per layer): algorithmic bytes
             per launch / its mean launch duration over the
             timed region, against MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline  the C port of the reference's byte-table CPU kernels
-            (oracle/c), one layer timed on the host cores, x 80.
+  cpu_baseline  the unmodified reference (baseline/_ref: ternpack's own
+            token pass, numba) on one layer, timed on the host cores, x 80;
+            the C port of its byte-table kernels (oracle/c) beside it.
   configs   every other BASELINE config (cfg0, cfg1, cfg2 I2_S / TL2, cfg3
             prefill, cfg4 M=8), each with its own value, roofline fraction,
             e2e and cpu_baseline.
@@ -30,7 +31,9 @@ stack sharded over N ranks (column-parallel q/k/v/gate/up, row-parallel
 o/down), the row-parallel int32 partials summed by our NVLink peer-memory
 kernel (``--collective peer``, default) or NCCL (``--collective nccl``).
 Without torchrun in the environment, ``--gpus N`` launches the N ranks
-itself.  ``--impl reference`` times the CPU port alone on the same workload.
+itself.  ``--impl reference`` times the unmodified reference package
+(baseline/_ref, ternpack's own token pass) on the host cores on the same
+workload, the C port beside it.
 """
 
 from __future__ import annotations
@@ -256,6 +259,97 @@ def cpu_baseline_stack(fmt, mats, h, i, layers, budget_s):
 
 
 # ---------------------------------------------------------------------------
+# the unmodified reference package (baseline/_ref, pip --target install of
+# /root/reference/pkg): ternpack's own token pass on the host cores
+# ---------------------------------------------------------------------------
+
+def ref_ternpack():
+    """Import ``ternpack`` from baseline/_ref, or None when it is absent."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(path, "ternpack", "__init__.py")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    # numba's on-disk cache: keep it out of the repo copy
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/tb_numba_cache")
+    try:
+        import ternpack
+        import ternpack.bench  # noqa: F401
+        return ternpack
+    except Exception:
+        return None
+
+
+def ref_layer(tp, fmt, mats):
+    """One layer of reference packed matrices from [(planes, scale, rows,
+    cols)] -- the bytes our generator (or LayerStack) produced, wrapped in
+    the reference's own PackedI2S / PackedTL2 (packing.py:77-197)."""
+    out = []
+    for planes, scale, rows, cols in mats:
+        if fmt == "i2s":
+            out.append(tp.PackedI2S(rows=rows, cols=cols, padded_cols=-(-cols // 4) * 4,
+                                    data=planes[0], scale=float(scale)))
+        else:
+            out.append(tp.PackedTL2(rows=rows, cols=cols, padded_cols=-(-cols // 6) * 6,
+                                    index_data=planes[0], sign_data=planes[1],
+                                    scale=float(scale)))
+    return out
+
+
+def time_ref_layer(tp, fmt, layer, h, i, budget_s, min_steps=1, max_steps=None, threads=None):
+    """ternpack.bench._token_pass_int (bench.py:138-153) over ONE layer: its
+    own 2 quantisations (+ TL2 LUTs) and 7 gemv_parallel calls, activations
+    from its own rng.  One warm call (numba JIT, validate()) untimed; then
+    layers until the budget (at least ``min_steps``).  -> (s per layer, n, threads)."""
+    kind = tp.KernelKind.I2_S if fmt == "i2s" else tp.KernelKind.TL2
+    threads = threads or os.cpu_count() or 1
+    rng = np.random.default_rng(1)
+    tp.bench._token_pass_int(kind, [layer], h, i, rng, threads)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        tp.bench._token_pass_int(kind, [layer], h, i, rng, threads)
+        n += 1
+        el = time.perf_counter() - t0
+        if n >= min_steps and (el >= budget_s or (max_steps and n >= max_steps)):
+            break
+    return el / n, n, threads
+
+
+def ref_baseline_stack(fmt, mats, h, i, layers, budget_s):
+    """cpu_baseline from the real reference (kind "reference"); None when
+    baseline/_ref is not importable (the caller then uses the C port)."""
+    tp = ref_ternpack()
+    if tp is None:
+        return None
+    layer = ref_layer(tp, fmt, mats)
+    dt, n, th = time_ref_layer(tp, fmt, layer, h, i, budget_s)
+    return {"value": round(1.0 / (layers * dt), 5), "unit": "tokens/s", "cores": th,
+            "kind": "reference",
+            "sample": f"{n} layers of ternpack.bench._token_pass_int ({fmt.upper()}, M=1: 2 "
+                      f"quantize_activations + 7 gemv_parallel, numba) on {th} threads, "
+                      f"tokens/s = 1 / ({layers} x layer time); host {os.cpu_count()} CPUs "
+                      f"({cpu_model()}); unmodified reference from baseline/_ref"}
+
+
+def stack_cpu_baselines(fmt, st, h, i, layers, budget_s):
+    """(cpu_baseline, port line): the reference itself when it is installed
+    (the port timed beside it), else the C port alone."""
+    p0 = [p.p for p in st.layers[0]]
+    if fmt == "i2s":
+        planes = [(p.data.cpu().numpy(),) for p in p0]
+    else:
+        planes = [(p.index_data.cpu().numpy(), p.sign_data.cpu().numpy()) for p in p0]
+    port = cpu_baseline_stack(fmt, [(pl, sh[3]) for pl, sh in zip(planes, st.shapes)],
+                              h, i, layers, budget_s / 2)
+    ref = ref_baseline_stack(fmt, [(pl, p.scale, sh[1], sh[2])
+                                   for pl, p, sh in zip(planes, p0, st.shapes)],
+                             h, i, layers, budget_s / 2)
+    if ref is None:
+        return port, None
+    return ref, port
+
+
+# ---------------------------------------------------------------------------
 # headline: cfg4 stack, M=1, tp = world
 # ---------------------------------------------------------------------------
 
@@ -367,8 +461,9 @@ def run_headline(args, rank, world):
         res["e2e"] = None
         res["e2e_note"] = "tp > 1: host-buffer pass not measured (device-resident value only)"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        mats = [((p.p.data.cpu().numpy(),), sh[3]) for p, sh in zip(st.layers[0], st.shapes)]
-        res["cpu_baseline"] = cpu_baseline_stack("i2s", mats, h, i, L, args.cpu_budget)
+        res["cpu_baseline"], port = stack_cpu_baselines("i2s", st, h, i, L, args.cpu_budget)
+        if port is not None:
+            res["cpu_baseline_port"] = port
     del st
     torch.cuda.empty_cache()
     return res
@@ -633,15 +728,12 @@ def run_stack_cfg(torch, tb, args, name, fmt, tokens, passes=10):
     if tokens == 1 and not args.no_e2e:
         out["e2e"] = e2e_stack(torch, tb, st, 20)
     if not args.no_cpu_baseline:
-        if fmt == "i2s":
-            mats = [((p.p.data.cpu().numpy(),), sh[3]) for p, sh in zip(st.layers[0], st.shapes)]
-        else:
-            mats = [((p.p.index_data.cpu().numpy(), p.p.sign_data.cpu().numpy()), sh[3])
-                    for p, sh in zip(st.layers[0], st.shapes)]
-        cb = cpu_baseline_stack(fmt, mats, h, i, L, args.cpu_budget / 2)
+        cb, port = stack_cpu_baselines(fmt, st, h, i, L, args.cpu_budget / 2)
         if tokens > 1:  # the reference has no multi-token path: M tokens = M passes
             cb["sample"] += f"; M={tokens} costs {tokens} such passes (rate is per token)"
         out["cpu_baseline"] = cb
+        if port is not None:
+            out["cpu_baseline_port"] = port
     del st
     torch.cuda.empty_cache()
     return out
@@ -702,6 +794,8 @@ def run_cfg3(torch, tb, args, copies=2, reps=10):
     ms_gemm /= reps
     a = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda")
     bt = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda").t()
+    torch._int_mm(a, bt)  # cuBLASLt init / workspace outside the capture
+    torch.cuda.synchronize()
     pk_ms, _ = graph_time(torch, lambda: [torch._int_mm(a, bt) for _ in range(5)])
     peak = 2 * 8192 ** 3 / (pk_ms / 5 * 1e-3) / 1e12
     del a, bt
@@ -777,7 +871,8 @@ def run_cfg3(torch, tb, args, copies=2, reps=10):
 def host_stack_layer(seed, cfg):
     """One cfg4 layer generated on the host: seeded N(0, 0.02) float32 latent
     matrices, absmean-ternarised (core.py:104-113 arithmetic, in row blocks)
-    and packed to the reference I2_S bytes (packing.py:200-206)."""
+    and packed to the reference I2_S bytes (packing.py:200-206).
+    -> [((packed,), scale, rows, cols, input)]."""
     from oracle import ternpack_oracle as O
     from paper_2410_16144_b200.stack import stack_shapes
     mats = []
@@ -795,44 +890,68 @@ def host_stack_layer(seed, cfg):
             v = np.clip(O.round_half_away(w[r0:r0 + blk].astype(np.float64) / scale), -1, 1)
             packed[r0:r0 + blk] = O.encode_i2s(v.astype(np.int8))
         del w
-        mats.append(((packed,), src))
+        mats.append(((packed,), scale, rows, cols, src))
     return mats
 
 
 def run_reference(args, world):
-    """The reference's CPU path (its byte-table kernels, C port in oracle/c)
-    on the headline workload, all host threads: each timed step is one layer
-    of the 80-layer token pass (2 quantisations + 7 GEMVs), value = 1 / (80 x
-    mean layer time)."""
+    """The reference's CPU path on the headline workload, all host threads.
+    Each timed step is one layer of the 80-layer token pass, run by the
+    UNMODIFIED reference (baseline/_ref: ternpack.bench._token_pass_int --
+    2 quantize_activations + 7 gemv_parallel, numba byte-table kernels);
+    value = 1 / (80 x mean layer time).  The C port (oracle/c) is timed
+    beside it on a short sample; it alone is used if baseline/_ref is absent."""
     t0 = time.perf_counter()
     mats = host_stack_layer(STACK_SEED, CFG4)
     gen_s = time.perf_counter() - t0
     h, i, L = CFG4["hidden"], CFG4["inter"], CFG4["layers"]
-    run = cpu_stack_layer("i2s", mats, h, i)
     threads = os.cpu_count() or 1
+    # the C port, a short sample beside the reference
+    run = cpu_stack_layer("i2s", [(pl, src) for pl, _, _, _, src in mats], h, i)
     rng = np.random.default_rng(7)
     X = [(rng.standard_normal(h).astype(np.float32), rng.standard_normal(i).astype(np.float32))
          for _ in range(4)]
-    for j in range(args.warmup):
-        run(*X[j % 4], threads)
-    t0 = time.perf_counter()
-    for j in range(args.steps):
-        run(*X[j % 4], threads)
-    dt_layer = (time.perf_counter() - t0) / args.steps
-    v = round(1.0 / (L * dt_layer), 5)
-    sample = (f"{args.steps} timed layers of the cfg4 token pass (2 quantise + 7 I2_S byte-table "
-              f"GEMVs, M=1) on {threads} OpenMP threads, tokens/s = 1 / (80 x layer time); C port "
-              f"of the reference byte-table kernels (oracle/c: _fast.byte_gemv + i2s tables); "
-              f"{threads} CPUs ({cpu_model()}); weights generated on the host in {gen_s:.0f} s")
+    run(*X[0], threads)
+    np_, t0 = 0, time.perf_counter()
+    while np_ < 3 or time.perf_counter() - t0 < 3.0:
+        run(*X[np_ % 4], threads)
+        np_ += 1
+    port_v = 1.0 / (L * (time.perf_counter() - t0) / np_)
+    tp = ref_ternpack()
+    if tp is not None:
+        layer = ref_layer(tp, "i2s", [(pl, sc, r, c) for pl, sc, r, c, _ in mats])
+        for _ in range(max(0, args.warmup - 1)):  # time_ref_layer makes one more warm call
+            tp.bench._token_pass_int(tp.KernelKind.I2_S, [layer], h, i,
+                                     np.random.default_rng(2), threads)
+        dt, n, _ = time_ref_layer(tp, "i2s", layer, h, i, 0.0, min_steps=args.steps)
+        kind = "reference"
+        what = ("unmodified reference from baseline/_ref: ternpack.bench._token_pass_int over "
+                "one layer (2 quantize_activations + 7 gemv_parallel(I2_S), numba)")
+    else:
+        for j in range(args.warmup):
+            run(*X[j % 4], threads)
+        t0 = time.perf_counter()
+        for j in range(args.steps):
+            run(*X[j % 4], threads)
+        dt, n = (time.perf_counter() - t0) / args.steps, args.steps
+        kind = "port"
+        what = ("C port of the reference byte-table kernels (oracle/c), baseline/_ref absent: "
+                "2 quantise + 7 I2_S GEMVs")
+    v = round(1.0 / (L * dt), 5)
+    sample = (f"{n} timed layers of the cfg4 token pass (M=1) on {threads} threads, "
+              f"tokens/s = 1 / (80 x layer time); {what}; {threads} CPUs ({cpu_model()}); "
+              f"weights generated on the host in {gen_s:.0f} s")
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(L * dt_layer * 1e3, 2), "higher_is_better": True,
+            "ms_per_step": round(L * dt * 1e3, 2), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "i8",
             "data": "synthetic (seeded N(0,0.02) latent weights -> absmean ternary I2_S; "
                     "N(0,1) activations)",
             "config": headline_config(world),
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": kind,
                              "sample": sample},
+            "cpu_port": {"value": round(port_v, 5), "unit": "tokens/s", "cores": threads,
+                         "kind": "port", "sample": f"{np_} layers of the C port (oracle/c)"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
@@ -896,7 +1015,9 @@ def main():
             try:
                 res["configs"][name] = fns[name]()
             except Exception as e:  # a secondary line must not lose the headline
-                res["configs"][name] = {"error": f"{type(e).__name__}: {e}"}
+                import traceback
+                res["configs"][name] = {"error": f"{type(e).__name__}: {e}",
+                                        "where": traceback.format_exc()[-1500:]}
             torch.cuda.synchronize()
             torch.cuda.empty_cache()
     if rank == 0:

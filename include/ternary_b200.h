@@ -250,7 +250,9 @@ int tb_gemv_step_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
  * vector (core.py:128: absmax over the whole token).  col0 must be a multiple
  * of one record chunk (64 weights for I2_S / TL1, 96 for TL2); a shard that
  * ends before the input does is zero-padded to whole chunks by tb_repack, so
- * the columns it does not own contribute exactly 0.
+ * the columns it does not own contribute exactly 0.  With col0 non-NULL
+ * every job is such a window (col0[j] + cols <= K); with col0 NULL every
+ * job must contract its whole input (cols == K).
  * Replaces nothing in the reference (its thread pool splits rows only,
  * kernels.py:181-186); it is the SURVEY §8(e) row-parallel shard.            */
 int tb_gemv_step_prepare_cols(int fmt, int64_t njobs, const tb_gemv_desc *descs,

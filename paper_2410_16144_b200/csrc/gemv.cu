@@ -1366,7 +1366,7 @@ extern "C" int tb_gemv_step_prepare_cols(int fmt, int64_t njobs, const tb_gemv_d
     const tb_gemv_desc &d = descs[j];
     const int64_t c0 = col0 ? col0[j] : 0;
     if (src[j] < 0 || src[j] >= ninputs || d.M != 1 || c0 < 0 || c0 % chunk_w ||
-        (c0 == 0 ? d.cols != input_k[src[j]] : c0 + d.cols > input_k[src[j]]))
+        (col0 ? c0 + d.cols > input_k[src[j]] : d.cols != input_k[src[j]]))
       return TB_ERR_ARGUMENT;
     int st = make_job(fmt, d.tiled, d.tiled_sign, d.rows, d.cols, nullptr, 1, d.a_scale,
                       d.w_scale, d.workspace, d.acc_out, d.out64, d.out32, start, host[j], true);

@@ -404,6 +404,7 @@ class GemvStep:
         lib = L.load()
         # (plan, input) or (plan, input, col0): a row-parallel K-shard reads
         # input columns [col0, col0 + cols) and uses the full input's scale
+        windowed = [len(pr) == 3 for pr in pairs]
         pairs = [tuple(pr) if len(pr) == 3 else (pr[0], pr[1], 0) for pr in pairs]
         fmts = {p.p.FMT for p, _, _ in pairs}
         if len(fmts) != 1:
@@ -427,8 +428,8 @@ class GemvStep:
                 raise ValueError("input index out of range")
             if c0 % chunk_w or c0 < 0:
                 raise ValueError(f"col0 must be a non-negative multiple of {chunk_w}")
-            if (plan.p.cols != self.input_k[v]) if c0 == 0 else \
-                    (c0 + plan.p.cols > self.input_k[v]):
+            if (c0 + plan.p.cols > self.input_k[v]) if windowed[i] else \
+                    (plan.p.cols != self.input_k[v]):
                 raise ValueError("dimension mismatch: input length != matrix cols")
             col0[i] = c0
             d.tiled = plan.main.data_ptr()

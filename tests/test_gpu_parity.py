@@ -418,7 +418,7 @@ def test_fused_step_sequence(tb):
             st = steps[si]
             q = [O.quantize(x, 1) for x in xs_host[xi]]
             np.testing.assert_array_equal(host(st.scales), [q[0][1], q[1][1]])
-            for (plan, src), (v, ws) in zip(st.pairs, truth[si]):
+            for (plan, src, _), (v, ws) in zip(st.pairs, truth[si]):
                 want = O.gemv_ref_int32(v, q[src][0])
                 assert np.array_equal(host(plan.acc)[0], want), (fmt, si, v.shape)
                 np.testing.assert_array_equal(host(plan.out64)[0],
@@ -466,7 +466,7 @@ def test_fused_step_segments_and_clusters(tb):
 
             def check(si, xi):
                 q = [O.quantize(x, 1) for x in xs_host[xi]]
-                for (plan, src), (v, ws) in zip(steps[si].pairs, truth[si]):
+                for (plan, src, _), (v, ws) in zip(steps[si].pairs, truth[si]):
                     want = O.gemv_ref_int32(v, q[src][0])
                     assert np.array_equal(host(plan.acc)[0], want), (fmt, srcs, si)
                     np.testing.assert_array_equal(host(plan.out64)[0],
