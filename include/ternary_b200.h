@@ -290,6 +290,15 @@ int tb_gemv(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign,
 int64_t tb_gemm_act_bytes(int64_t M, int64_t cols);
 int tb_gemm_tile_act(const int8_t *act, int64_t M, int64_t lda, int64_t cols,
                      uint8_t *act_tiled, void *stream);
+/* quantize_activations (core.py:116-134) of M <= 512 float32 tokens [M][ldx]
+ * straight into the tensor-core operand (the bytes tb_gemm_tile_act writes
+ * for the int8 codes, plus scale[M] float64) in one launch; nonfinite_flag
+ * (may be NULL) is OR-ed with 1 if any input is NaN/inf (the caller raises
+ * "activations must be finite").  TB_ERR_UNSUPPORTED for cols > 163840
+ * (use tb_quantize_f32 + tb_gemm_tile_act).  Replaces, for a prefill batch,
+ * the reference's per-token quantize_activations calls (bench.py:141-142).  */
+int tb_gemm_quantize_act(const float *x, int64_t M, int64_t cols, int64_t ldx, double *scale,
+                         int32_t *nonfinite_flag, uint8_t *act_tiled, void *stream);
 typedef struct tb_gemm_desc {
   const uint8_t *tiled;
   int64_t rows, cols;

@@ -584,6 +584,135 @@ __global__ void gemm_rowsum_kernel(const int8_t *__restrict__ act, int M, int64_
   }
 }
 
+// quantize_activations (core.py:116-134) straight into the GEMM's A layout:
+// float32 tokens [M][ldx] -> the bytes tb_gemm_tile_act writes (tiled int8
+// codes + per-token sums) and the float64 scales, in ONE launch.  A cluster
+// of S CTAs owns one 8-token row group; CTA r of the cluster owns K stages
+// [r*kps, (r+1)*kps).  Warp w handles token 8g + w:
+//   1. integer max of |x| bits over its slice (exact: float32 -> float64 is
+//      monotonic), cluster max through DSMEM -> scale = amax / 127 (fp64);
+//   2. quantise (quantize_fast: fp32 product, exact fp64 fallback at ties),
+//      16 codes per lane in code-plane order, staged in shared memory so the
+//      CTA writes whole 1 KB (stage, row group) blocks;
+//   3. per-token code sums reduced over the cluster by rank 0.
+// x is read twice (the second pass hits L2).
+__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t qa_mapa(uint32_t saddr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t qa_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t qa_cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
+__global__ void __launch_bounds__(256) gemm_quantize_act_kernel(
+    const float *__restrict__ x, int M, int K, int64_t ldx, int Mpad, int ks, int kps,
+    double *__restrict__ scale, int32_t *flag, uint8_t *__restrict__ out) {
+  extern __shared__ uint4 qa_stage[];  // [kps][kGemmKC][8 rows] 16-byte units
+  __shared__ uint32_t s_amax[8];
+  __shared__ int32_t s_sum[8];
+  const int S = (int)qa_cluster_size();
+  const int rank = (int)qa_cluster_rank();
+  const int g = blockIdx.x / S;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = g * 8 + w;
+  const int ks0 = rank * kps;
+  const int nks = max(0, min(ks, ks0 + kps) - ks0);
+  const int64_t k0 = (int64_t)ks0 * kGemmBK;
+  const int64_t k1 = std::min<int64_t>((int64_t)(ks0 + nks) * kGemmBK, (int64_t)K);
+  const float *row = x + (int64_t)m * ldx;
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | (uintptr_t)(ldx * 4)) & 15) == 0;
+  // ---- 1. absmax
+  uint32_t amax = 0;
+  if (m < M) {
+    int64_t k = k0 + lane * 4;
+    if (vec)
+      for (; k + 3 < k1; k += 128) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + k));
+        amax = max(amax, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
+                             max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
+      }
+    for (; k < k1; k += 128)
+      for (int i = 0; i < 4 && k + i < k1; ++i)
+        amax = max(amax, __float_as_uint(row[k + i]) & 0x7fffffffu);
+  }
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  if (lane == 0) s_amax[w] = amax;
+  cluster_sync_all();
+  if (lane < S) amax = ld_cluster_u32(qa_mapa(smem_u32(&s_amax[w]), lane));
+  else amax = 0;
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  const double a = (double)__uint_as_float(amax);
+  const double sc = a > 0.0 ? a / 127.0 : 1.0;
+  const double inv_s = 1.0 / sc;
+  const float inv_sf = (float)inv_s;
+  if (rank == 0 && lane == 0 && m < M) {
+    scale[m] = sc;
+    if (amax >= 0x7f800000u && flag) atomicOr(flag, 1);
+  }
+  // ---- 2. codes, staged per CTA
+  int32_t sum = 0;
+  const int units = nks * kGemmKC;  // 16-column units of this CTA's slice
+  for (int u = lane; u < units; u += 32) {
+    const int64_t k = k0 + (int64_t)u * 16;
+    uint32_t wd[4] = {0, 0, 0, 0};
+    if (m < M && k < K) {
+      float f[16];
+      if (vec && k + 16 <= K) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 v = __ldg(reinterpret_cast<const float4 *>(row + k) + i);
+          f[4 * i] = v.x, f[4 * i + 1] = v.y, f[4 * i + 2] = v.z, f[4 * i + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) f[i] = k + i < K ? row[k + i] : 0.0f;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int q = quantize_fast(f[i], inv_sf, sc, inv_s);
+        sum += q;
+        wd[i >> 2] |= (uint32_t)(uint8_t)(int8_t)q << (8 * (i & 3));
+      }
+    }
+    // 4x4 byte transpose: word s = (a[s], a[4+s], a[8+s], a[12+s])
+    const uint32_t t0 = prmt(wd[0], wd[1], 0x5140u), t1 = prmt(wd[0], wd[1], 0x7362u);
+    const uint32_t t2 = prmt(wd[2], wd[3], 0x5140u), t3 = prmt(wd[2], wd[3], 0x7362u);
+    qa_stage[u * 8 + w] = make_uint4(prmt(t0, t2, 0x5410u), prmt(t0, t2, 0x7632u),
+                                     prmt(t1, t3, 0x5410u), prmt(t1, t3, 0x7632u));
+  }
+  sum = __reduce_add_sync(0xffffffffu, sum);
+  if (lane == 0) s_sum[w] = sum;
+  __syncthreads();
+  // whole (stage, row group) blocks: kGemmKC x 8 rows x 16 B = 1 KB contiguous
+  const int G = Mpad / 8;
+  uint4 *o4 = reinterpret_cast<uint4 *>(out);
+  for (int i = threadIdx.x; i < nks * kGemmKC * 8; i += 256) {
+    const int ksl = i / (kGemmKC * 8), j = i % (kGemmKC * 8);
+    o4[((int64_t)(ks0 + ksl) * G + g) * (kGemmKC * 8) + j] = qa_stage[i];
+  }
+  cluster_sync_all();
+  // ---- 3. per-token sums (rank 0), after every rank published its part
+  if (rank == 0 && threadIdx.x < 8) {
+    int32_t t = 0;
+    for (int r = 0; r < S; ++r) t += (int32_t)ld_cluster_u32(qa_mapa(smem_u32(&s_sum[threadIdx.x]), r));
+    reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK)[g * 8 + threadIdx.x] = t;
+  }
+  cluster_sync_all();  // peers' shared memory stays alive until rank 0 has read it
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -716,6 +845,44 @@ extern "C" int tb_gemm_tile_act(const int8_t *act, int64_t M, int64_t lda, int64
                                           reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK));
   TB_CHECK_LAUNCH();
   return TB_OK;
+}
+
+extern "C" int tb_gemm_quantize_act(const float *x, int64_t M, int64_t cols, int64_t ldx,
+                                    double *scale, int32_t *nonfinite_flag, uint8_t *out,
+                                    void *stream) {
+  if (!x || !scale || !out || M < 1 || M > kGemmMaxM || cols < 1 || ldx < cols ||
+      cols > (int64_t)1 << 30 || (reinterpret_cast<uintptr_t>(out) & 15))
+    return TB_ERR_ARGUMENT;
+  const int Mpad = (int)gemm_mpad(M);
+  const int ks = (int)gemm_stages_of(cols);
+  int S = std::min(8, ks);
+  const int kps = (int)ceil_div(ks, S);
+  S = (int)ceil_div(ks, kps);  // no empty ranks
+  const int smem = kps * kGemmKC * 8 * 16;
+  if (smem > 160 * 1024) return TB_ERR_UNSUPPORTED;  // K > 163840: tb_quantize + tb_gemm_tile_act
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_quantize_act_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             160 * 1024) != cudaSuccess)
+      return TB_ERR_CUDA;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(Mpad / 8 * S));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_quantize_act_kernel, x, (int)M, (int)cols, ldx, Mpad, ks,
+                            kps, scale, nonfinite_flag, out) == cudaSuccess
+             ? TB_OK
+             : TB_ERR_CUDA;
 }
 
 extern "C" int tb_gemm_batch(int fmt, int64_t njobs, const tb_gemm_desc *descs, int64_t M,

@@ -329,6 +329,7 @@ class GemvBatch:
         self.njobs, self.total, self.max_m = len(pairs), total.value, maxm.value
         self.max_entries = maxe.value
         self.pairs = pairs  # keep every buffer alive
+        self._scale_ptrs = {rec.scales.data_ptr() for _, rec in pairs}
         self._lib = lib
 
     def run(self, stream_ptr: int | None = None, finalize: bool = True):
@@ -356,7 +357,7 @@ class StepGlue:
 
         self._lib = L.load()
         self.inputs = inputs
-        self.fin = finalize
+        self.fin = None
         self.descs = (L.QuantDesc * max(1, len(inputs)))()
         for d, (x, rec) in zip(self.descs, inputs):
             d.x = x.data_ptr()
@@ -366,8 +367,15 @@ class StepGlue:
             d.ldq = rec.natural.stride(0) if rec.natural is not None else 0
             d.scale, d.rec, d.nonfinite_flag = rec.scales.data_ptr(), rec.buf.data_ptr(), None
         self._descs_ptr = C.cast(self.descs, C.c_void_p)
+        self.retarget(finalize)
 
     def retarget(self, finalize: "GemvBatch | None"):
+        # the finalize reads the batch's per-token scales while this launch's
+        # quantisation rows write theirs: they must be different buffers
+        if finalize is not None and any(rec.scales.data_ptr() in finalize._scale_ptrs
+                                        for _, rec in self.inputs):
+            raise ValueError("a glue cannot quantise into records whose batch it finalises "
+                             "(alternate two ActRecords sets)")
         self.fin = finalize
         return self
 

@@ -181,9 +181,14 @@ class LayerStack:
                                     for p, s in zip(plans, self.plan)], self.ks)
                           for plans in self.layers]
         else:
-            self.rec = [ActRecords(L.TL2 if fmt == "tl2" else L.I2S, tokens, k) for k in self.ks]
-            self.batches = [GemvBatch([(p, self.rec[s[3]]) for p, s in zip(plans, self.plan)])
-                            for plans in self.layers]
+            # two record sets, alternating by layer: the glue of layer l writes
+            # layer l's scales/records while (in the same launch) finalising
+            # layer l-1, whose outputs are scaled by layer l-1's a_scale
+            self.rec = [[ActRecords(L.TL2 if fmt == "tl2" else L.I2S, tokens, k)
+                         for k in self.ks] for _ in range(2)]
+            self.batches = [GemvBatch([(p, self.rec[li % 2][s[3]])
+                                       for p, s in zip(plans, self.plan)])
+                            for li, plans in enumerate(self.layers)]
             self.tail = StepGlue([])
         if self.rp:
             # what the reduction scales: per row-parallel projection
@@ -224,7 +229,7 @@ class LayerStack:
 
     def make_glues(self, XH, XI):
         """M > 1: one StepGlue per layer quantising rows of XH[l] / XI[l] ([M, K])."""
-        return [StepGlue([(XH[li], self.rec[0]), (XI[li], self.rec[1])])
+        return [StepGlue([(XH[li], self.rec[li % 2][0]), (XI[li], self.rec[li % 2][1])])
                 for li in range(self.nlayers)]
 
     def outputs(self, li: int) -> dict:

@@ -189,9 +189,11 @@ def small_fixtures():
     return out
 
 
-def large_fixtures():
+def large_fixtures(only=None):
     res = {}
     for cname, case in LARGE_CASES.items():
+        if only is not None and cname not in only:
+            continue
         t0 = time.time()
         mats, acts, entry = {}, {}, {"matrices": {}, "acts": {}, "gemv": {}}
         for name, n, k, seed in case["matrices"]:
@@ -231,11 +233,18 @@ def large_fixtures():
 
 
 def main():
+    """No arguments: every fixture.  ``--large cfgN ...``: regenerate only
+    those large cases and merge them into the existing large.json."""
     t0 = time.time()
-    small = small_fixtures()
-    np.savez_compressed(HERE / "small.npz", **small)
-    print(f"small.npz written ({time.time() - t0:.1f}s)", flush=True)
-    large = large_fixtures()
+    only = sys.argv[sys.argv.index("--large") + 1:] if "--large" in sys.argv else None
+    if only is None:
+        small = small_fixtures()
+        np.savez_compressed(HERE / "small.npz", **small)
+        print(f"small.npz written ({time.time() - t0:.1f}s)", flush=True)
+        large = large_fixtures()
+    else:
+        large = json.loads((HERE / "large.json").read_text())
+        large.update(large_fixtures(only))
     (HERE / "large.json").write_text(json.dumps(large, indent=1, sort_keys=True) + "\n")
     print(f"large.json written ({time.time() - t0:.1f}s)")
 

@@ -51,10 +51,13 @@ LARGE_CASES = {
         "gemv": [("q", "xh"), ("k", "xh"), ("v", "xh"), ("o", "xh"),
                  ("gate", "xh"), ("up", "xh"), ("down", "xi")],
     },
-    "cfg3": {
-        "matrices": [("q", 4096, 4096, 30)],
-        "acts": [("x", 512, 4096, 31)],
-        "gemv": [("q", "x")],
+    "cfg3": {  # the whole prefill layer the bench times (q ... down, K up to 14336)
+        "matrices": [("q", 4096, 4096, 30), ("k", 1024, 4096, 32), ("v", 1024, 4096, 33),
+                     ("o", 4096, 4096, 34), ("gate", 14336, 4096, 35),
+                     ("up", 14336, 4096, 36), ("down", 4096, 14336, 37)],
+        "acts": [("x", 512, 4096, 31), ("xi", 512, 14336, 38)],
+        "gemv": [("q", "x"), ("k", "x"), ("v", "x"), ("o", "x"), ("gate", "x"),
+                 ("up", "x"), ("down", "xi")],
     },
     "cfg4": {
         "matrices": [("q", 10240, 10240, 40), ("k", 1280, 10240, 41),

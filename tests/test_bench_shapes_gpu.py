@@ -1,0 +1,257 @@
+"""Parity of every path bench.py times, at the shape it is timed at.
+
+* cfg3: the whole prefill layer (q/k/v/o/gate/up/down, M=512, K up to 14336)
+  through ONE grouped tb_gemm_batch launch -- once with int32 accumulators
+  (SHA-pinned to the reference, tests/golden/large.json) and once with the
+  bench's descriptor (fp32 outputs only, the 128-bit-store epilogue), within
+  the north star's 1e-5 relative of the oracle's float64 make_result.
+* cfg1: the TL1 FFN block exactly as the bench builds it (6 weight copies,
+  one fused GemvStep per token, chained with programmatic dependent launch
+  and captured in a CUDA graph); copy 0 holds the reference-pinned
+  matrices, every step's outputs are checked.
+* cfg2 (I2_S, TL2) and cfg4 (I2_S, M=1 and M=8): the full-size LayerStack the
+  bench builds (seed, shapes, layer count), layers 0 and L-1 checked after a
+  whole token pass against the C port of the reference kernels
+  (oracle/c, pinned by tests/test_c_oracle.py).
+"""
+
+import ctypes as C
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import c_oracle as CO
+from oracle import ternpack_oracle as O
+from workloads import LARGE_CASES, activations, latent_weights, sha
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).parent / "golden"
+LARGE = json.loads((GOLD / "large.json").read_text())
+STACK_SEED = 11  # bench.py
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def tb():
+    import paper_2410_16144_b200 as tb
+    CO.build()
+    return tb
+
+
+# --------------------------------------------------------------------- cfg3
+
+def test_cfg3_layer_gemm_batch(tb):
+    from paper_2410_16144_b200 import _lib as L
+    lib = L.load()
+    case, gold = LARGE_CASES["cfg3"], LARGE["cfg3"]
+    M = 512
+    acts = {}
+    for name, mm, k, seed in case["acts"]:
+        qa = tb.quantize_tokens(torch.from_numpy(activations(seed, mm, k)).cuda(), pad_to=4)
+        assert sha(host(qa.data)) == gold["acts"][name]["data_p4"]
+        assert [float(s).hex() for s in host(qa.scales)] == gold["acts"][name]["scales"]
+        til = torch.empty(lib.tb_gemm_act_bytes(M, k), dtype=torch.uint8, device="cuda")
+        L.check(lib.tb_gemm_tile_act(qa.data.data_ptr(), M, qa.data.stride(0), k,
+                                     til.data_ptr(), L.stream_ptr()), "tile")
+        acts[name] = (qa, til)
+    src = dict(case["gemv"])
+    jobs = []
+    for name, n, k, seed in case["matrices"]:
+        m = tb.ternarize_weights(torch.from_numpy(latent_weights(seed, n, k)).cuda(), n, k)
+        assert m.scale.hex() == gold["matrices"][name]["scale"]
+        p = tb.encode_i2s(m)
+        assert sha(host(p.data)) == gold["matrices"][name]["i2s"]
+        main, _ = p.tiled()
+        jobs.append((name, p, main, acts[src[name]]))
+
+    def launch(kind):
+        descs = (L.GemmDesc * len(jobs))()
+        outs = []
+        for d, (name, p, main, (qa, til)) in zip(descs, jobs):
+            d.tiled, d.rows, d.cols, d.act_tiled = main.data_ptr(), p.rows, p.cols, til.data_ptr()
+            d.a_scale, d.w_scale = qa.scales.data_ptr(), float(p.scale)
+            dt = {"acc": torch.int32, "out32": torch.float32, "out64": torch.float64}[kind]
+            o = torch.empty((M, p.rows), dtype=dt, device="cuda")
+            setattr(d, {"acc": "acc_out"}.get(kind, kind), o.data_ptr())
+            outs.append(o)
+        L.check(lib.tb_gemm_batch(L.I2S, len(jobs), C.cast(descs, C.c_void_p), M,
+                                  L.stream_ptr()), "gemm_batch")
+        torch.cuda.synchronize()
+        return [host(o) for o in outs]
+
+    accs = launch("acc")
+    for (name, *_), acc in zip(jobs, accs):
+        assert sha(acc) == gold["gemv"][f"{name}:{src[name]}"]["acc"], name
+    out64 = launch("out64")  # the exact float64 chain (core.py:99-101)
+    for (name, *_), o in zip(jobs, out64):
+        assert sha(o) == gold["gemv"][f"{name}:{src[name]}"]["out"], name
+    out32 = launch("out32")  # the bench's descriptor: fp32 outputs only
+    for (name, p, main, (qa, til)), acc, o in zip(jobs, accs, out32):
+        want = acc.astype(np.float64) * float(p.scale) * host(qa.scales)[:, None]
+        np.testing.assert_allclose(o, want, rtol=1e-5, atol=0, err_msg=name)
+
+
+def test_cfg3_fused_quantize_tile(tb):
+    """The bench's per-layer activation path (quantise straight into the GEMM
+    operand layout, one launch per input) writes the same bytes, scales and
+    row sums as quantize_tokens + tb_gemm_tile_act."""
+    from paper_2410_16144_b200 import _lib as L
+    lib = L.load()
+    if not hasattr(lib, "tb_gemm_quantize_act"):
+        pytest.skip("no fused quantise-tile entry point")
+    rng = np.random.default_rng(3)
+    for M, K in ((512, 4096), (512, 14336), (200, 1000), (1, 64), (130, 4100)):
+        x = torch.from_numpy(rng.standard_normal((M, K)).astype(np.float32)).cuda()
+        x[0, 5] = 0.0
+        if M > 3:
+            x[3] = 0.0
+        qa = tb.quantize_tokens(x, pad_to=4)
+        want = torch.empty(lib.tb_gemm_act_bytes(M, K), dtype=torch.uint8, device="cuda")
+        L.check(lib.tb_gemm_tile_act(qa.data.data_ptr(), M, qa.data.stride(0), K,
+                                     want.data_ptr(), L.stream_ptr()), "tile")
+        got = torch.full_like(want, 0xAB)
+        sc = torch.empty(M, dtype=torch.float64, device="cuda")
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        L.check(lib.tb_gemm_quantize_act(x.data_ptr(), M, K, K, sc.data_ptr(), flag.data_ptr(),
+                                         got.data_ptr(), L.stream_ptr()), "quantize_act")
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), (M, K)
+        assert torch.equal(sc, qa.scales) and int(flag.item()) == 0
+    x[1, 2] = float("inf")
+    L.check(lib.tb_gemm_quantize_act(x.data_ptr(), M, K, K, sc.data_ptr(), flag.data_ptr(),
+                                     got.data_ptr(), L.stream_ptr()), "quantize_act")
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 1
+
+
+# --------------------------------------------------------------------- cfg1
+
+def test_cfg1_step_chain(tb):
+    H, I = 4096, 14336
+    gold = LARGE["cfg1"]
+    ncopy, nx = 6, 8
+    copies = []
+    for c in range(ncopy):
+        mats = {}
+        for name, rows, cols, seed in LARGE_CASES["cfg1"]["matrices"]:
+            if c == 0:  # the reference-pinned matrices
+                w = torch.from_numpy(latent_weights(seed, rows, cols)).cuda()
+            else:       # the bench's generator
+                g = torch.Generator(device="cuda").manual_seed(1000 + c * 7 + len(mats))
+                w = torch.randn(rows, cols, generator=g, device="cuda") * 0.02
+            m = tb.ternarize_weights(w, rows, cols)
+            del w
+            mats[name] = tb.encode_tl1(m)
+            if c == 0:
+                assert sha(host(mats[name].data)) == gold["matrices"][name]["tl1"]
+        pl = {k: tb.GemvPlan(v, out_dtype=torch.float32) for k, v in mats.items()}
+        step = tb.GemvStep([(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)], [H, I])
+        copies.append((mats, pl, step))
+    xs = [torch.from_numpy(activations(13, 1, H)[0]).cuda(),
+          torch.from_numpy(activations(14, 1, I)[0]).cuda()]
+    g = torch.Generator(device="cuda").manual_seed(77)
+    XH = torch.randn(nx, H, generator=g, device="cuda")
+    XI = torch.randn(nx, I, generator=g, device="cuda")
+    XH[0], XI[0] = xs  # step 0 sees the reference-pinned activations
+
+    def run(j0, n):
+        prev = None
+        for j in range(j0, j0 + n):
+            st = copies[j % ncopy][2]
+            st.run([XH[j % nx], XI[j % nx]], prev=prev)
+            prev = st
+        prev.finalize()
+
+    # eager, then the bench's form: a CUDA graph of the chain
+    for form in ("eager", "graph"):
+        if form == "eager":
+            run(0, ncopy)
+        else:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s), torch.cuda.graph(graph, stream=s):
+                run(ncopy, ncopy)
+            graph.replay()
+        torch.cuda.synchronize()
+        j0 = 0 if form == "eager" else ncopy
+        for j in range(j0, j0 + ncopy):
+            mats, pl, _ = copies[j % ncopy]
+            xh, xi = host(XH[j % nx]), host(XI[j % nx])
+            qh, sh = CO.quantize(xh, 2)
+            qi, si = CO.quantize(xi, 2)
+            for name, q, s_ in (("gate", qh, sh), ("up", qh, sh), ("down", qi, si)):
+                acc = CO.gemv_tl1(host(mats[name].data), CO.lut_tl1(q, q.size // 2), 0)
+                if j == 0:
+                    src = "xh" if name != "down" else "xi"
+                    assert sha(acc[None]) == gold["gemv"][f"{name}:{src}"]["acc"]
+                want = O.make_output(acc, mats[name].scale, s_).astype(np.float32)
+                assert np.array_equal(host(pl[name].out32[0]), want), (form, j, name)
+
+
+# ---------------------------------------------------------- cfg2 / cfg4 stacks
+
+def _planes(p, fmt):
+    if fmt == "tl2":
+        return host(p.index_data), host(p.sign_data)
+    return (host(p.data),)
+
+
+def _c_acc(fmt, planes, x, cols):
+    if fmt == "i2s":
+        q, s = CO.quantize(x, 4)
+        return CO.gemv_i2s(planes[0], q, 0), s
+    q, s = CO.quantize(x, 3)
+    return CO.gemv_tl2(planes[0], planes[1], CO.lut_tl2(q, -(-cols // 6) * 2), 0), s
+
+
+@pytest.mark.parametrize("name,fmt,tokens", [("cfg2", "i2s", 1), ("cfg2", "tl2", 1),
+                                             ("cfg4", "i2s", 1), ("cfg4", "i2s", 8)])
+def test_full_stack_layers(tb, name, fmt, tokens):
+    from paper_2410_16144_b200.stack import STACKS, LayerStack
+    cfg = STACKS[name]
+    st = LayerStack(cfg, fmt=fmt, seed=STACK_SEED, tokens=tokens)
+    L, h, i = st.nlayers, cfg["hidden"], cfg["inter"]
+    g = torch.Generator(device="cuda").manual_seed(99)
+    if tokens == 1:
+        XH = torch.randn(L, h, generator=g, device="cuda")
+        XI = torch.randn(L, i, generator=g, device="cuda")
+        st.token_pass(list(XH), list(XI))
+    else:
+        XH = torch.randn(L, tokens, h, generator=g, device="cuda")
+        XI = torch.randn(L, tokens, i, generator=g, device="cuda")
+        st.token_pass(None, None, st.make_glues(XH, XI))
+    torch.cuda.synchronize()
+    for li in (0, L - 1):
+        xs = [host(XH[li]).reshape(tokens, h), host(XI[li]).reshape(tokens, i)]
+        for plan, (pname, rows, cols, src) in zip(st.layers[li], st.shapes):
+            planes = _planes(plan.p, fmt)
+            got = host(plan.out32)
+            for t in range(tokens):
+                acc, s = _c_acc(fmt, planes, xs[src][t], cols)
+                want = O.make_output(acc, plan.p.scale, s).astype(np.float32)
+                assert np.array_equal(got[t], want), (name, fmt, tokens, li, pname, t)
+    del st
+    torch.cuda.empty_cache()
+
+
+def test_glue_refuses_scale_hazard(tb):
+    """A glue that finalises a batch may not quantise into that batch's
+    records: its finalize rows read the per-token scales the quantise rows
+    overwrite (the M>1 stack alternates two record sets)."""
+    from paper_2410_16144_b200 import _lib as L
+    v = np.ones((64, 128), np.int8)
+    plan = tb.GemvPlan(tb.encode_i2s(tb.TernaryMatrix(64, 128, v, 1.0)), max_tokens=2)
+    rec, rec2 = tb.ActRecords(L.I2S, 2, 128), tb.ActRecords(L.I2S, 2, 128)
+    batch = tb.GemvBatch([(plan, rec)])
+    x = torch.ones(2, 128, device="cuda")
+    with pytest.raises(ValueError, match="alternate two ActRecords sets"):
+        tb.StepGlue([(x, rec)], finalize=batch)
+    tb.StepGlue([(x, rec2)], finalize=batch)  # a different set is fine

@@ -65,13 +65,16 @@ def main():
     gen = torch.Generator(device="cuda").manual_seed(77)
     XH = torch.randn(NX, H, generator=gen, device="cuda")
     XI = torch.randn(NX, I, generator=gen, device="cuda")
-    rec_h = tb.ActRecords(L.TL1, 1, H)
-    rec_i = tb.ActRecords(L.TL1, 1, I)
-    for pl in plans:
+    # two record sets: a glue never quantises into the records of the batch it
+    # finalises (copies alternate sets; NCOPY and NX are even)
+    recs = [(tb.ActRecords(L.TL1, 1, H), tb.ActRecords(L.TL1, 1, I)) for _ in range(2)]
+    for c, pl in enumerate(plans):
+        rec_h, rec_i = recs[c % 2]
         pl["batch"] = tb.GemvBatch([(pl["gate"], rec_h), (pl["up"], rec_h), (pl["down"], rec_i)])
     for pl in plans:
         pl["step"] = tb.GemvStep([(pl["gate"], 0), (pl["up"], 0), (pl["down"], 1)], [H, I])
-    glues = [tb.StepGlue([(XH[j:j + 1], rec_h), (XI[j:j + 1], rec_i)]) for j in range(NX)]
+    glues = [tb.StepGlue([(XH[j:j + 1], recs[j % 2][0]), (XI[j:j + 1], recs[j % 2][1])])
+             for j in range(NX)]
     fin_only = tb.StepGlue([])
 
     def gemv_nofin(i):
