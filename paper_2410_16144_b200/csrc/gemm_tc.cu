@@ -617,6 +617,39 @@ __device__ __forceinline__ uint32_t qa_cluster_size() {
   return r;
 }
 
+// 16 floats of a unit (zero beyond K)
+__device__ __forceinline__ void qa_load16(const float *row, int64_t k, int K, bool vec, float *f) {
+  if (vec && k + 16 <= K) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(row + k) + i);
+      f[4 * i] = v.x, f[4 * i + 1] = v.y, f[4 * i + 2] = v.z, f[4 * i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) f[i] = k + i < K ? row[k + i] : 0.0f;
+  }
+}
+// 16 codes in code-plane order (word s = (a[s], a[4+s], a[8+s], a[12+s]))
+__device__ __forceinline__ uint4 qa_codes16(const float *f, float inv_sf, double sc, double inv_s,
+                                            int32_t &sum) {
+  uint32_t wd[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int q = quantize_fast(f[i], inv_sf, sc, inv_s);
+    sum += q;
+    wd[i >> 2] |= (uint32_t)(uint8_t)(int8_t)q << (8 * (i & 3));
+  }
+  const uint32_t t0 = prmt(wd[0], wd[1], 0x5140u), t1 = prmt(wd[0], wd[1], 0x7362u);
+  const uint32_t t2 = prmt(wd[2], wd[3], 0x5140u), t3 = prmt(wd[2], wd[3], 0x7362u);
+  return make_uint4(prmt(t0, t2, 0x5410u), prmt(t0, t2, 0x7632u), prmt(t1, t3, 0x5410u),
+                    prmt(t1, t3, 0x7632u));
+}
+
+// UPL > 0: each lane keeps its (at most UPL) units' floats in registers from
+// the absmax pass to the quantise pass (x read once, every load in flight at
+// entry); UPL == 0: any slice length, the quantise pass re-reads x (L2).
+template <int UPL>
 __global__ void __launch_bounds__(256) gemm_quantize_act_kernel(
     const float *__restrict__ x, int M, int K, int64_t ldx, int Mpad, int ks, int kps,
     double *__restrict__ scale, int32_t *flag, uint8_t *__restrict__ out) {
@@ -631,12 +664,29 @@ __global__ void __launch_bounds__(256) gemm_quantize_act_kernel(
   const int ks0 = rank * kps;
   const int nks = max(0, min(ks, ks0 + kps) - ks0);
   const int64_t k0 = (int64_t)ks0 * kGemmBK;
-  const int64_t k1 = std::min<int64_t>((int64_t)(ks0 + nks) * kGemmBK, (int64_t)K);
+  const int units = nks * kGemmKC;  // 16-column units of this CTA's slice
   const float *row = x + (int64_t)m * ldx;
   const bool vec = ((reinterpret_cast<uintptr_t>(x) | (uintptr_t)(ldx * 4)) & 15) == 0;
-  // ---- 1. absmax
+  // ---- 1. absmax (integer max of |x| bits: exact, float32 -> float64 is monotonic)
   uint32_t amax = 0;
-  if (m < M) {
+  float f[UPL > 0 ? UPL : 1][16];
+  if constexpr (UPL > 0) {
+#pragma unroll
+    for (int i = 0; i < UPL; ++i) {
+      const int u = lane + 32 * i;
+      if (m < M && u < units && k0 + u * 16 < K) {
+        qa_load16(row, k0 + (int64_t)u * 16, K, vec, f[i]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) f[i][e] = 0.0f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < UPL; ++i)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) amax = max(amax, __float_as_uint(f[i][e]) & 0x7fffffffu);
+  } else if (m < M) {
+    const int64_t k1 = std::min<int64_t>(k0 + (int64_t)nks * kGemmBK, (int64_t)K);
     int64_t k = k0 + lane * 4;
     if (vec)
       for (; k + 3 < k1; k += 128) {
@@ -651,8 +701,7 @@ __global__ void __launch_bounds__(256) gemm_quantize_act_kernel(
   amax = __reduce_max_sync(0xffffffffu, amax);
   if (lane == 0) s_amax[w] = amax;
   cluster_sync_all();
-  if (lane < S) amax = ld_cluster_u32(qa_mapa(smem_u32(&s_amax[w]), lane));
-  else amax = 0;
+  amax = lane < S ? ld_cluster_u32(qa_mapa(smem_u32(&s_amax[w]), lane)) : 0u;
   amax = __reduce_max_sync(0xffffffffu, amax);
   const double a = (double)__uint_as_float(amax);
   const double sc = a > 0.0 ? a / 127.0 : 1.0;
@@ -664,37 +713,30 @@ __global__ void __launch_bounds__(256) gemm_quantize_act_kernel(
   }
   // ---- 2. codes, staged per CTA
   int32_t sum = 0;
-  const int units = nks * kGemmKC;  // 16-column units of this CTA's slice
-  for (int u = lane; u < units; u += 32) {
-    const int64_t k = k0 + (int64_t)u * 16;
-    uint32_t wd[4] = {0, 0, 0, 0};
-    if (m < M && k < K) {
-      float f[16];
-      if (vec && k + 16 <= K) {
+  if constexpr (UPL > 0) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 v = __ldg(reinterpret_cast<const float4 *>(row + k) + i);
-          f[4 * i] = v.x, f[4 * i + 1] = v.y, f[4 * i + 2] = v.z, f[4 * i + 3] = v.w;
-        }
+    for (int i = 0; i < UPL; ++i) {
+      const int u = lane + 32 * i;
+      if (u < units) qa_stage[u * 8 + w] = qa_codes16(f[i], inv_sf, sc, inv_s, sum);
+    }
+  } else {
+    for (int u = lane; u < units; u += 32) {
+      const int64_t k = k0 + (int64_t)u * 16;
+      float g16[16];
+      if (m < M && k < K) {
+        qa_load16(row, k, K, vec, g16);
       } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) f[i] = k + i < K ? row[k + i] : 0.0f;
+        for (int e = 0; e < 16; ++e) g16[e] = 0.0f;
       }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int q = quantize_fast(f[i], inv_sf, sc, inv_s);
-        sum += q;
-        wd[i >> 2] |= (uint32_t)(uint8_t)(int8_t)q << (8 * (i & 3));
-      }
+      qa_stage[u * 8 + w] = qa_codes16(g16, inv_sf, sc, inv_s, sum);
     }
-    // 4x4 byte transpose: word s = (a[s], a[4+s], a[8+s], a[12+s])
-    const uint32_t t0 = prmt(wd[0], wd[1], 0x5140u), t1 = prmt(wd[0], wd[1], 0x7362u);
-    const uint32_t t2 = prmt(wd[2], wd[3], 0x5140u), t3 = prmt(wd[2], wd[3], 0x7362u);
-    qa_stage[u * 8 + w] = make_uint4(prmt(t0, t2, 0x5410u), prmt(t0, t2, 0x7632u),
-                                     prmt(t1, t3, 0x5410u), prmt(t1, t3, 0x7632u));
   }
   sum = __reduce_add_sync(0xffffffffu, sum);
   if (lane == 0) s_sum[w] = sum;
+  // publish the sums to the cluster BEFORE the global stores (a release
+  // arrive after them would wait for every store to be performed)
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   __syncthreads();
   // whole (stage, row group) blocks: kGemmKC x 8 rows x 16 B = 1 KB contiguous
   const int G = Mpad / 8;
@@ -703,14 +745,17 @@ __global__ void __launch_bounds__(256) gemm_quantize_act_kernel(
     const int ksl = i / (kGemmKC * 8), j = i % (kGemmKC * 8);
     o4[((int64_t)(ks0 + ksl) * G + g) * (kGemmKC * 8) + j] = qa_stage[i];
   }
-  cluster_sync_all();
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   // ---- 3. per-token sums (rank 0), after every rank published its part
   if (rank == 0 && threadIdx.x < 8) {
     int32_t t = 0;
-    for (int r = 0; r < S; ++r) t += (int32_t)ld_cluster_u32(qa_mapa(smem_u32(&s_sum[threadIdx.x]), r));
+    for (int r = 0; r < S; ++r)
+      t += (int32_t)ld_cluster_u32(qa_mapa(smem_u32(&s_sum[threadIdx.x]), r));
     reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK)[g * 8 + threadIdx.x] = t;
   }
-  cluster_sync_all();  // peers' shared memory stays alive until rank 0 has read it
+  // peers' shared memory stays alive until rank 0 has read it (no ordering
+  // of global memory needed: relaxed)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -860,13 +905,13 @@ extern "C" int tb_gemm_quantize_act(const float *x, int64_t M, int64_t cols, int
   S = (int)ceil_div(ks, kps);  // no empty ranks
   const int smem = kps * kGemmKC * 8 * 16;
   if (smem > 160 * 1024) return TB_ERR_UNSUPPORTED;  // K > 163840: tb_quantize + tb_gemm_tile_act
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_quantize_act_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             160 * 1024) != cudaSuccess)
-      return TB_ERR_CUDA;
-    attr_set = true;
-  }
+  const int upl = (int)ceil_div((int64_t)kps * kGemmKC, 32);  // units per lane
+  auto kern = upl <= 1 ? gemm_quantize_act_kernel<1>
+              : upl <= 2 ? gemm_quantize_act_kernel<2>
+                         : gemm_quantize_act_kernel<0>;  // (UPL 4: 104 registers, two waves: slower)
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return TB_ERR_CUDA;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(Mpad / 8 * S));
   cfg.blockDim = dim3(256);
@@ -879,7 +924,7 @@ extern "C" int tb_gemm_quantize_act(const float *x, int64_t M, int64_t cols, int
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_quantize_act_kernel, x, (int)M, (int)cols, ldx, Mpad, ks,
+  return cudaLaunchKernelEx(&cfg, kern, x, (int)M, (int)cols, ldx, Mpad, ks,
                             kps, scale, nonfinite_flag, out) == cudaSuccess
              ? TB_OK
              : TB_ERR_CUDA;
