@@ -76,8 +76,10 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 #define TL_LMARK(i) TL_MARK(i)
 #endif
 
-// FU: 0 = records path; 1 = fused step, small CTAs, several per SM; 2 = fused
-// step, 16 warps, one CTA per SM (record tables too large for two CTAs)
+// FU: 0 = records path; 1 = fused step, small CTAs, several per SM; 3 = fused
+// step, 8-warp CTAs, two per SM (record tables up to 56 KB: the ~100B stack's
+// 43K-element inputs); 2 = fused step, 16 warps, one CTA per SM (larger tables
+// or an isolated launch)
 template <int FMT, int MT, int FU = 0>
 struct Cfg {
   static constexpr bool kFused = FU != 0;
@@ -106,9 +108,20 @@ struct Cfg {
 #ifndef TB_TL2_RING
 #define TB_TL2_RING 4
 #endif
+#ifndef TB_MED_WARPS
+#define TB_MED_WARPS 8
+#endif
+#ifndef TB_MED_RING
+#define TB_MED_RING 3
+#endif
+#ifndef TB_MED_RECTAB_KB
+#define TB_MED_RECTAB_KB 56
+#endif
   static constexpr int kWarps = FU == 1 ? (FMT == TB_TL2 ? TB_TL2_WARPS : TB_FUSED_WARPS)
-                                       : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
-  static constexpr int kMinBlocks = FU == 1 ? (FMT == TB_TL2 ? TB_TL2_MINB : TB_FUSED_MINB) : 1;
+                                : FU == 3 ? TB_MED_WARPS
+                                          : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
+  static constexpr int kMinBlocks =
+      FU == 1 ? (FMT == TB_TL2 ? TB_TL2_MINB : TB_FUSED_MINB) : FU == 3 ? 2 : 1;
 #ifndef TB_MT1_RING
 #define TB_MT1_RING (TB_MT1_WARPS > 16 ? 3 : 4)
 #endif
@@ -117,6 +130,7 @@ struct Cfg {
       kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + MT * Fmt<FMT>::kRecBytes);
   static constexpr int kFit = (225 * 1024) / (kWarps * kStageBytesAll);
   static constexpr int kRing = FU == 1 ? (FMT == TB_TL2 ? TB_TL2_RING : TB_FUSED_RING)
+                               : FU == 3 ? TB_MED_RING
                                : (MT == 1 ? TB_MT1_RING : (kFit >= 4 ? 4 : (kFit >= 2 ? kFit : 2)));
   static constexpr int kThreads = 32 * kWarps;
   // fused step: records live in a CTA-wide table after the ring, not per stage
@@ -126,7 +140,8 @@ struct Cfg {
 #ifndef TB_SMALL_RECTAB_KB
 #define TB_SMALL_RECTAB_KB 40
 #endif
-  static constexpr int kRecTabBytes = kFused ? (kMinBlocks >= 2 ? TB_SMALL_RECTAB_KB : 64) * 1024 : 0;  // records of all inputs
+  static constexpr int kRecTabBytes =
+      !kFused ? 0 : (FU == 3 ? TB_MED_RECTAB_KB : kMinBlocks >= 2 ? TB_SMALL_RECTAB_KB : 64) * 1024;  // records of all inputs
   static constexpr int kSmem = kRingBytes + kRecTabBytes;
   static_assert(kSmem <= 227 * 1024 - 512, "ring does not fit in shared memory");
 };
@@ -643,7 +658,8 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // CTA's input mask, while the warp-range and job lookups below are chains of
   // constant-bank loads that are cold at launch (~1.4 us measured before the
   // loads were issued when they came after them).
-  constexpr int kMaxG = CQ >= 2 ? (CF::kThreads <= 128 ? 4 : CF::kThreads <= 192 ? 3 : 2) : (FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4);
+  // register groups of 16 inputs per thread (medium CTAs: 4, so a CTA pair holds a 32K input)
+  constexpr int kMaxG = FU == 3 ? 4 : CQ >= 2 ? (CF::kThreads <= 128 ? 4 : CF::kThreads <= 192 ? 3 : 2) : (FMT == TB_TL2 ? (CF::kThreads >= 384 ? 2 : 3) : 4);
   RegQuant<FMT, CF::kThreads, kMaxG> rq;
   constexpr int cq = CQ;
   int crank = 0, need = 0;
@@ -796,11 +812,13 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // stores happen at the end, so no load latency sits in the CTA's tail.
   // Two entries per thread (a 148 x 160-thread grid covers 23,680 of the
   // cfg1 step's 32,768): both read-and-resets go out together at the wait.
-  constexpr int kFinPer = 2;
-  int fin_j[kFinPer] = {-1, -1};
-  int64_t fin_k[kFinPer] = {0, 0};
-  int32_t fin_v[kFinPer] = {0, 0};
-  double fin_as[kFinPer] = {0.0, 0.0};
+  constexpr int kFinPer = FU == 3 ? 3 : 2;  // medium CTAs: 148 x 256 x 3 >= the 98,304 cfg4 rows
+  int fin_j[kFinPer];
+  int64_t fin_k[kFinPer];
+  int32_t fin_v[kFinPer];
+  double fin_as[kFinPer];
+#pragma unroll
+  for (int e = 0; e < kFinPer; ++e) fin_j[e] = -1, fin_k[e] = 0, fin_v[e] = 0, fin_as[e] = 0.0;
   auto fin_load = [&]() {
     if constexpr (kFused) {
       if (!b.in.prev_inline) return;
@@ -1198,9 +1216,11 @@ static int launch_step(int fmt, GemvBatch &b, int rec_tab_bytes, bool isolated, 
   // small CTAs, several per SM (chained steps overlap) when the record tables
   // allow it; one 16-warp CTA per SM for big tables or an isolated launch
   const bool small = !isolated && rec_tab_bytes <= Cfg<TB_I2S, 1, 1>::kRecTabBytes;  // 40 KB
+  const bool medium = !isolated && rec_tab_bytes <= Cfg<TB_I2S, 1, 3>::kRecTabBytes;  // 56 KB
   if (fmt == TB_I2S || fmt == TB_TL1)  // TL1 tiles hold I2_S codes
-    return small ? launch_tgemv<TB_I2S, 1, 1>(b, s, rec_tab_bytes)
-                 : launch_tgemv<TB_I2S, 1, 2>(b, s, rec_tab_bytes);
+    return small    ? launch_tgemv<TB_I2S, 1, 1>(b, s, rec_tab_bytes)
+           : medium ? launch_tgemv<TB_I2S, 1, 3>(b, s, rec_tab_bytes)
+                    : launch_tgemv<TB_I2S, 1, 2>(b, s, rec_tab_bytes);
   if (fmt == TB_TL2)
     return small ? launch_tgemv<TB_TL2, 1, 1>(b, s, rec_tab_bytes)
                  : launch_tgemv<TB_TL2, 1, 2>(b, s, rec_tab_bytes);
