@@ -84,8 +84,7 @@ class _TiledMixin:
         return t
 
     def workspace(self, stream=None):
-        s = stream if stream is not None else torch.cuda.current_stream()
-        key = ("ws", s.cuda_stream)
+        key = ("ws", L.stream_ptr(stream))
         w = self._cache.get(key)
         if w is None:
             nbytes = L.load().tb_gemv_workspace_bytes(self.FMT, self.rows, self.cols)
