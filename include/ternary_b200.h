@@ -190,6 +190,29 @@ int tb_gemv_batch_prepare(int fmt, int64_t njobs, const tb_gemv_desc *descs,
 int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t njobs,
                          int64_t total_chunks, int32_t max_m, int64_t max_entries,
                          int32_t finalize, void *stream);
+/* As tb_gemv_batch_prepare, plus K-windows: job j contracts record columns
+ * [col0[j], col0[j] + descs[j].cols) of a records buffer built for
+ * rec_cols[j] columns (col0 a multiple of one record chunk: 64 weights, 96
+ * for TL2; NULL arrays = whole records).  A job with acc_out, out64 and out32
+ * all NULL is not finalised: its partial sums accumulate in its workspace,
+ * which another job of the batch with the same workspace finalises (the
+ * K-windows of one matrix).  Replaces nothing in the reference (its thread
+ * pool splits rows only, kernels.py:181-186).                              */
+int tb_gemv_batch_prepare_cols(int fmt, int64_t njobs, const tb_gemv_desc *descs,
+                               const int64_t *col0, const int64_t *rec_cols, void *table_host,
+                               int64_t *total_chunks, int32_t *max_m, int64_t *max_entries);
+/* As tb_gemv_batch_launch, also given the host copy of a job table of <= 10
+ * jobs: the jobs ride in the kernel parameters and, for 2 <= M <= 8 tokens
+ * (I2_S / TL1), every CTA keeps its segment's records in one shared-memory
+ * table (no per-warp record staging); larger tables fall back to the
+ * records path.  prev_table_host / prev_njobs (optional): the host job table
+ * of the batch launched before this one (completed before this launch's
+ * inputs were produced); this launch finalises it in its tail (table mode
+ * only: TB_ERR_UNSUPPORTED otherwise, and the caller finalises it).       */
+int tb_gemv_batch_launch_inline(int fmt, const void *table_device, const void *table_host,
+                                int64_t njobs, int64_t total_chunks, int32_t max_m,
+                                int64_t max_entries, int32_t finalize,
+                                const void *prev_table_host, int64_t prev_njobs, void *stream);
 
 /* Decode-step glue in ONE launch: finalise a prepared GEMV batch (may be
  * empty: fin_njobs = 0) and quantise up to 4 activation matrices into

@@ -32,8 +32,8 @@
 
 namespace tb {
 
-constexpr int kMaxInlineJobs = 8;
-constexpr int kMaxSegs = 4;
+constexpr int kMaxInlineJobs = 10;  // a layer: 6 projections on x_h + 3 K-windows of down (M > 1)
+constexpr int kMaxSegs = 8;
 constexpr int kMaxStepCluster = 4;  // fused step: CTAs sharing one quantisation
 #ifndef TB_STEP_CLUSTER
 #define TB_STEP_CLUSTER 2
@@ -82,7 +82,11 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // or an isolated launch)
 template <int FMT, int MT, int FU = 0>
 struct Cfg {
-  static constexpr bool kFused = FU != 0;
+  static constexpr bool kFused = FU >= 1 && FU <= 3;
+  // FU = 4: the records path (M > 1 tokens, records built by a glue kernel)
+  // with the CTA's records in ONE shared-memory table filled at entry instead
+  // of staged per warp and ring stage: the ring carries weights only.
+  static constexpr bool kTable = FU == 4;
 #ifndef TB_MT1_WARPS
 #define TB_MT1_WARPS 16
 #endif
@@ -117,8 +121,18 @@ struct Cfg {
 #ifndef TB_MED_RECTAB_KB
 #define TB_MED_RECTAB_KB 56
 #endif
+#ifndef TB_TABLE_WARPS
+#define TB_TABLE_WARPS 16
+#endif
+#ifndef TB_TABLE_RING
+#define TB_TABLE_RING 3
+#endif
+#ifndef TB_TABLE_KB
+#define TB_TABLE_KB 124
+#endif
   static constexpr int kWarps = FU == 1 ? (FMT == TB_TL2 ? TB_TL2_WARPS : TB_FUSED_WARPS)
                                 : FU == 3 ? TB_MED_WARPS
+                                : FU == 4 ? TB_TABLE_WARPS
                                           : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
   static constexpr int kMinBlocks =
       FU == 1 ? (FMT == TB_TL2 ? TB_TL2_MINB : TB_FUSED_MINB) : FU == 3 ? 2 : 1;
@@ -131,17 +145,19 @@ struct Cfg {
   static constexpr int kFit = (225 * 1024) / (kWarps * kStageBytesAll);
   static constexpr int kRing = FU == 1 ? (FMT == TB_TL2 ? TB_TL2_RING : TB_FUSED_RING)
                                : FU == 3 ? TB_MED_RING
+                               : FU == 4 ? TB_TABLE_RING
                                : (MT == 1 ? TB_MT1_RING : (kFit >= 4 ? 4 : (kFit >= 2 ? kFit : 2)));
   static constexpr int kThreads = 32 * kWarps;
   // fused step: records live in a CTA-wide table after the ring, not per stage
   static constexpr int kStageBytes =
-      kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + (kFused ? 0 : MT) * Fmt<FMT>::kRecBytes);
+      kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + (kFused || kTable ? 0 : MT) * Fmt<FMT>::kRecBytes);
   static constexpr int kRingBytes = kWarps * kRing * kStageBytes;
 #ifndef TB_SMALL_RECTAB_KB
 #define TB_SMALL_RECTAB_KB 40
 #endif
   static constexpr int kRecTabBytes =
-      !kFused ? 0 : (FU == 3 ? TB_MED_RECTAB_KB : kMinBlocks >= 2 ? TB_SMALL_RECTAB_KB : 64) * 1024;  // records of all inputs
+      kTable ? TB_TABLE_KB * 1024
+      : !kFused ? 0 : (FU == 3 ? TB_MED_RECTAB_KB : kMinBlocks >= 2 ? TB_SMALL_RECTAB_KB : 64) * 1024;  // records of all inputs
   static constexpr int kSmem = kRingBytes + kRecTabBytes;
   static_assert(kSmem <= 227 * 1024 - 512, "ring does not fit in shared memory");
 };
@@ -161,8 +177,11 @@ struct GemvJob {
   int start;  // first flat chunk of this job
   int end;    // one past its last flat chunk (start + T * C)
   int src;    // fused step: index of the input vector this job contracts
-  int c0;     // fused step: first record chunk of that input (a row-parallel
-              // K-shard contracts input columns [64 c0, ...) -- 96 c0 for TL2)
+  int c0;     // first record chunk of that input (a K-window job contracts
+              // input columns [64 c0, ...) -- 96 c0 for TL2)
+  int cin;    // records path: chunks per token row of the global records (>= c0 + C)
+  int fin_m;  // tokens the finalize covers: M, or 0 for a job with no outputs
+              // (a K-window whose sums land in a workspace another job finalises)
 };
 
 // Fused decode step (tgemv_kernel<FMT, 1, true>): the launch quantises its own
@@ -274,12 +293,11 @@ __device__ __forceinline__ void flush_tile(const GemvBatch &b, int j, int t,
 // until the GEMV grid has completed and its memory operations are visible.
 // Finalize job j with CTAs `part` of `nparts` (every thread of the CTA).
 __device__ __forceinline__ void finalize_one(const GemvJob &J, int part, int nparts) {
-  const int64_t total = (int64_t)J.M * J.Npad;
+  const int64_t total = (int64_t)J.fin_m * J.Npad;
   for (int64_t i = part * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)nparts * blockDim.x) {
     const int m = (int)(i / J.Npad), row = (int)(i - (int64_t)m * J.Npad);
-    const int32_t v = J.ws_acc[i];
-    J.ws_acc[i] = 0;
+    const int32_t v = atomicExch(J.ws_acc + i, 0);  // read and reset: one L2 operation
     if (row < J.N) {
       const int64_t o = (int64_t)m * J.N + row;
       if (J.acc_out) J.acc_out[o] = v;
@@ -309,8 +327,7 @@ __device__ __forceinline__ void finalize_fin_all(const FinJob *fin, int njobs, i
     }
     const FinJob &J = fin[j];
     const int m = (int)(k / J.Npad), row = (int)(k - (int64_t)m * J.Npad);
-    const int32_t v = J.ws_acc[k];
-    J.ws_acc[k] = 0;
+    const int32_t v = atomicExch(J.ws_acc + k, 0);  // read and reset: one L2 operation
     if (row < J.N) {
       const int64_t o = (int64_t)m * J.N + row;
       if (J.acc_out) J.acc_out[o] = v;
@@ -337,8 +354,7 @@ __device__ __forceinline__ void finalize_fin_range(const FinJob *fin, int njobs,
     }
     const FinJob &J = fin[j];
     const int m = (int)(k / J.Npad), row = (int)(k - (int64_t)m * J.Npad);
-    const int32_t v = J.ws_acc[k];
-    J.ws_acc[k] = 0;
+    const int32_t v = atomicExch(J.ws_acc + k, 0);  // read and reset: one L2 operation
     if (row < J.N) {
       const int64_t o = (int64_t)m * J.N + row;
       if (J.acc_out) J.acc_out[o] = v;
@@ -406,7 +422,7 @@ __device__ __forceinline__ void glue_finalize_flat(const GemvBatch &b, int part,
   if ((int)threadIdx.x < b.njobs) {
     const GemvJob J = job_at(b, threadIdx.x);
     fj[threadIdx.x] = FinJob{J.ws_acc, J.acc_out, J.out64, J.out32, J.a_scale, J.w_scale,
-                             J.N, J.Npad, J.M};
+                             J.N, J.Npad, J.fin_m};
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -430,9 +446,12 @@ __device__ __forceinline__ void glue_finalize_flat(const GemvBatch &b, int part,
         while (j + 1 < b.njobs && pre[j + 1] <= e) ++j;
         jj[q] = j;
         kk[q] = e - pre[j];
-        int4 *ws = reinterpret_cast<int4 *>(fj[j].ws_acc + kk[q]);
-        v[q] = __ldcg(ws);
-        __stcg(ws, make_int4(0, 0, 0, 0));
+        // read and reset with atomics: a store after a load of the same
+        // address waits for the load's data, serialising the ILP (measured:
+        // the M = 8 finalize of a cfg4 layer 16 us -> ...)
+        int32_t *ws = fj[j].ws_acc + kk[q];
+        v[q] = make_int4(atomicExch(ws, 0), atomicExch(ws + 1, 0), atomicExch(ws + 2, 0),
+                         atomicExch(ws + 3, 0));
       }
     }
 #pragma unroll
@@ -542,7 +561,7 @@ __device__ void issue_chunks(const GemvBatch &b, Cursor cur, int cnt, uint8_t *s
       const int d = rem / RU, q = rem - d * RU;
       const int c = (cur.c + d) % C;
       cp_async16_ca(act_slot + (m * kStageChunks + done + d) * F::kRecBytes + q * 16,
-                    J.rec + ((int64_t)m * C + c) * F::kRecBytes + q * 16);
+                    J.rec + ((int64_t)m * J.cin + J.c0 + c) * F::kRecBytes + q * 16);
     }
     done += run;
     // advance the cursor
@@ -579,18 +598,20 @@ struct IssueState {
   const uint8_t *w;    // weights of chunk `cur` in the job's tiled layout
   const uint8_t *sgn;  // TL2 sign bits of chunk `cur`
   const uint8_t *rec;  // the job's record base
-  int C, T, M;
+  int C, T, M, CI, C0;  // CI: record chunks per token row; C0: the window's first
 
   __device__ __forceinline__ void reset(const GemvBatch &b, Cursor c) {
     cur = c;
     const GemvJob J = job_at(b, c.j);
     C = J.C;
     M = J.M;
+    CI = J.cin;
     T = (J.end - J.start) / J.C;
     const int64_t g = (int64_t)c.t * C + c.c;
     w = J.wmain + g * kTileChunkBytes;
     sgn = J.wsign + g * kTileSignBytes;
     rec = J.rec;
+    C0 = J.c0;
   }
 
   template <int FMT, int kWhat = kIssueAll>
@@ -615,7 +636,7 @@ struct IssueState {
       if ((kWhat & kIssueRecords) && lane < kStageChunks * F::kRecBytes / 16)
         for (int m = 0; m < M; ++m)  // the stage's 4 records are contiguous
           cp_async16_ca(act_slot + m * kStageChunks * F::kRecBytes + lane * 16,
-                        rec + ((int64_t)m * C + cur.c) * F::kRecBytes + lane * 16);
+                        rec + ((int64_t)m * CI + C0 + cur.c) * F::kRecBytes + lane * 16);
 #endif
       w += kStageChunks * kTileChunkBytes;
       sgn += kStageChunks * kTileSignBytes;
@@ -642,9 +663,10 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   using F = Fmt<FMT>;
   using CF = Cfg<FMT, MT, FU>;
   constexpr bool kFused = CF::kFused;
+  constexpr bool kTable = CF::kTable;
   static_assert(!kFused || MT == 1, "the fused step is a one-token decode step");
   constexpr int kRing = CF::kRing;
-  constexpr int kIssueMain = kFused ? kIssueWeights : kIssueAll;
+  constexpr int kIssueMain = (kFused || kTable) ? kIssueWeights : kIssueAll;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t *ring = smem + warp * kRing * CF::kStageBytes;
@@ -692,7 +714,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   bool waited = false;
   __shared__ double s_scale[kMaxStepInputs];
   int s_badm = 0;  // fused: non-finite inputs (bit v), identical in every thread
-  if constexpr (!kFused) {
+  if constexpr (!kFused && !kTable) {
     if (n <= 0) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       return;
@@ -787,6 +809,36 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       cp_async_commit();
     }
     __syncthreads();
+  } else if constexpr (kTable) {
+    // weights of the first ring stages first (no dependence on the glue),
+    // then -- once the glue that built the records has completed -- the
+    // CTA's records into the table: [C/4][M][4 chunks][record] (a ring
+    // stage's token stride), the window [c0, c0 + C) of the segment's input
+#pragma unroll 1
+    for (int k = 0; k < kRing && k < nst; ++k)
+      is.issue<FMT, kIssueWeights>(b, min(kStageChunks, n - k * kStageChunks),
+                                   ring + k * CF::kStageBytes, lane);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    {
+      int sj = 0;
+      const int sc = b.seg_chunk[seg];
+      for (int j = 1; j < b.njobs; ++j)
+        if (job_at(b, j).start <= sc) sj = j;
+      const GemvJob J = job_at(b, sj);
+      constexpr int RU = F::kRecBytes / 16;
+      const int units = J.M * J.C * RU;
+      for (int u = threadIdx.x; u < units; u += CF::kThreads) {
+        const int m = u / (J.C * RU), rem = u - m * J.C * RU;
+        const int c = rem / RU, q = rem - c * RU;
+        cp_async16_cg(rtab_base + (((c >> 2) * J.M + m) * kStageChunks + (c & 3)) * F::kRecBytes + q * 16,
+                      J.rec + ((int64_t)m * J.cin + J.c0 + c) * F::kRecBytes + q * 16);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 1; k < kRing; ++k) cp_async_commit();  // the ring's group arithmetic
   } else {
     IssueState wis = is;
 #pragma unroll 1
@@ -894,6 +946,11 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       M = J.M;
       T = (J.end - J.start) / J.C;
       if constexpr (kFused) rtab = rtab_base + b.in.off[J.src] + J.c0 * F::kRecBytes;
+      if constexpr (kTable) rtab = rtab_base;  // the segment's window
+    };
+    // table mode: chunk c's records (token stride = a ring stage's, kStageChunks records)
+    auto tab_rec = [&](int c) -> const uint8_t * {
+      return rtab + ((c >> 2) * M * kStageChunks + (c & 3)) * F::kRecBytes;
     };
     load_shape();
     Acc<FMT, MT> acc;
@@ -917,7 +974,8 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
           uint32_t sg = 0;
           if (FMT == TB_TL2)
             sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
-          process_chunk<FMT, MT>(w4, sg, act + j * F::kRecBytes, M, acc, j);
+          process_chunk<FMT, MT>(w4, sg, kTable ? tab_rec(cur.c + j) : act + j * F::kRecBytes, M,
+                                 acc, j);
         }
         nch += kStageChunks;
         cur.c += kStageChunks;
@@ -938,7 +996,8 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
           uint32_t sg = 0;
           if (FMT == TB_TL2)
             sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
-          const uint8_t *act = kFused ? rtab + cur.c * F::kRecBytes : slot_act + j * F::kRecBytes;
+          const uint8_t *act = kTable ? tab_rec(cur.c)
+                               : kFused ? rtab + cur.c * F::kRecBytes : slot_act + j * F::kRecBytes;
           process_chunk<FMT, MT>(w4, sg, act, M, acc);
           ++nch;
           ++cur.c;
@@ -964,6 +1023,69 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     if (nch > 0) flush(acc, M);
   }
   TL_MARK(4);
+  if constexpr (kTable) {
+    // the previous batch's finalize (its grid completed before the glue this
+    // launch waited on): every thread of the grid takes a strided share of
+    // the flat (job, token, row) space, off the critical path of the next
+    // launch's weight stream
+    if (b.in.prev_inline) {
+      // the jobs staged in shared memory (kernel-parameter loads with a
+      // per-lane index serialise); 8 entries per thread per round, every
+      // load issued before any use
+      __shared__ FinJob s_fin[kMaxInlineFin];
+      __shared__ int64_t s_pre[kMaxInlineFin + 1];
+      if ((int)threadIdx.x < b.in.prev_njobs) s_fin[threadIdx.x] = b.in.fin[threadIdx.x];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_pre[0] = 0;
+        for (int j = 0; j < b.in.prev_njobs; ++j)
+          s_pre[j + 1] = s_pre[j] + (int64_t)s_fin[j].M * s_fin[j].Npad;
+      }
+      __syncthreads();
+      const int nj = b.in.prev_njobs;
+      // warp-uniform runs of 32 entries (Npad is a multiple of 32: a run never
+      // straddles a token row), lane = row: the job search and the token
+      // index are uniform, 4 runs' loads in flight per warp
+      const int64_t nruns = s_pre[nj] / 32;
+      const int64_t nwarps = (int64_t)gridDim.x * CF::kWarps;
+      for (int64_t r0 = gw; r0 < nruns; r0 += 4 * nwarps) {
+        int32_t v[4];
+        int jj[4], mm[4], rw[4];
+        double as[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t r = r0 + u * nwarps;
+          jj[u] = -1;
+          if (r < nruns) {
+            const int64_t e = r * 32;
+            int j = 0;
+            while (j + 1 < nj && s_pre[j + 1] <= e) ++j;
+            const FinJob &J = s_fin[j];
+            const int k = (int)(e - s_pre[j]);  // < 2^31: M * Npad of one job
+            const int m = k / J.Npad;
+            jj[u] = j;
+            mm[u] = m;
+            rw[u] = k - m * J.Npad + lane;
+            int32_t *w = J.ws_acc + k + lane;
+            v[u] = atomicExch(w, 0);  // read and reset (a plain store would wait for the load)
+            as[u] = J.a_scale ? __ldg(J.a_scale + m) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (jj[u] < 0) continue;
+          const FinJob &J = s_fin[jj[u]];
+          if (rw[u] < J.N) {
+            const int64_t o = (int64_t)mm[u] * J.N + rw[u];
+            if (J.acc_out) J.acc_out[o] = v[u];
+            const double y = static_cast<double>(v[u]) * J.w_scale * as[u];  // core.py:99-101
+            if (J.out64) J.out64[o] = y;
+            if (J.out32) J.out32[o] = static_cast<float>(y);
+          }
+        }
+      }
+    }
+  }
   if constexpr (kFused) {
     if (!waited) {
 #ifndef TB_NO_TAILWAIT  // profiling variant (results invalid): no chain serialisation
@@ -1072,10 +1194,16 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
   // proportion to their chunks; otherwise one segment
   b.nseg = 1;
   b.seg_chunk[0] = 0;
-  if (kFused && b.table == nullptr) {
+  if (CF::kTable && (b.table != nullptr || rec_tab_bytes <= 0)) return TB_ERR_ARGUMENT;
+  if ((kFused || CF::kTable) && b.table == nullptr) {
+    // fused step: runs of jobs on the same input vector; table mode: runs of
+    // jobs on the same records AND K-window (one table per CTA)
     int ns = 0, starts[kMaxInlineJobs + 1];
     for (int j = 0; j < b.njobs; ++j)
-      if (j == 0 || b.jobs[j].src != b.jobs[j - 1].src) starts[ns++] = b.jobs[j].start;
+      if (j == 0 || b.jobs[j].src != b.jobs[j - 1].src ||
+          (CF::kTable && (b.jobs[j].rec != b.jobs[j - 1].rec || b.jobs[j].c0 != b.jobs[j - 1].c0)))
+        starts[ns++] = b.jobs[j].start;
+    if (CF::kTable && (ns > kMaxSegs || ns > grid)) return TB_ERR_UNSUPPORTED;
     if (ns <= kMaxSegs && ns <= grid && ns > 1) {
       b.nseg = ns;
       for (int q = 0; q < ns; ++q) b.seg_chunk[q] = starts[q];
@@ -1137,7 +1265,7 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(CF::kThreads);
-  cfg.dynamicSmemBytes = kFused ? CF::kRingBytes + rec_tab_bytes : CF::kSmem;
+  cfg.dynamicSmemBytes = (kFused || CF::kTable) ? CF::kRingBytes + rec_tab_bytes : CF::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1202,6 +1330,8 @@ static int make_job(int fmt, const uint8_t *tiled, const uint8_t *tiled_sign, in
   J.end = (int)(start + T * C);
   J.src = 0;
   J.c0 = 0;
+  J.cin = (int)C;
+  J.fin_m = (acc_out || out64 || out32) ? (int)M : 0;
   return TB_OK;
 }
 
@@ -1370,6 +1500,111 @@ extern "C" int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t n
   return launch_batch(fmt, b, max_m, static_cast<cudaStream_t>(stream));
 }
 
+// As tb_gemv_batch_prepare, plus K-windows: job j contracts record columns
+// [col0[j], col0[j] + descs[j].cols) of records built for rec_cols[j] columns
+// (col0 a multiple of one record chunk; NULL arrays = whole records).
+extern "C" int tb_gemv_batch_prepare_cols(int fmt, int64_t njobs, const tb_gemv_desc *descs,
+                                          const int64_t *col0, const int64_t *rec_cols,
+                                          void *table_host, int64_t *total_chunks,
+                                          int32_t *max_m, int64_t *max_entries) {
+  int st = tb_gemv_batch_prepare(fmt, njobs, descs, table_host, total_chunks, max_m, max_entries);
+  if (st != TB_OK || (!col0 && !rec_cols)) return st;
+  const int64_t chunk_w = fmt == TB_TL2 ? 96 : 64;
+  GemvJob *host = static_cast<GemvJob *>(table_host);
+  for (int64_t j = 0; j < njobs; ++j) {
+    const int64_t c0 = col0 ? col0[j] : 0;
+    const int64_t rc = rec_cols ? rec_cols[j] : descs[j].cols;
+    if (c0 < 0 || c0 % chunk_w || c0 + descs[j].cols > rc) return TB_ERR_ARGUMENT;
+    host[j].c0 = (int)(c0 / chunk_w);
+    host[j].cin = (int)ceil_div(ref_row_bytes(fmt, rc), kChunkBytes);
+  }
+  return TB_OK;
+}
+
+// As tb_gemv_batch_launch, with the host copy of a small job table (<= 10
+// jobs): the jobs ride in the kernel parameters, and for 2 <= M tokens each
+// CTA keeps its segment's records (one records buffer and K-window) in one
+// shared-memory table instead of staging them per warp and ring stage.
+extern "C" int tb_gemv_batch_launch_inline(int fmt, const void *table_device,
+                                           const void *table_host, int64_t njobs,
+                                           int64_t total_chunks, int32_t max_m,
+                                           int64_t max_entries, int32_t finalize,
+                                           const void *prev_table_host, int64_t prev_njobs,
+                                           void *stream) {
+  if (!table_host || njobs > kMaxInlineJobs || max_m < 2) {
+    if (prev_njobs > 0) return TB_ERR_UNSUPPORTED;  // the caller finalises the previous batch
+    return tb_gemv_batch_launch(fmt, table_device, njobs, total_chunks, max_m, max_entries,
+                                finalize, stream);
+  }
+  if (prev_njobs > kMaxInlineJobs) return TB_ERR_UNSUPPORTED;
+  if (fmt < TB_I2S || fmt > TB_TL2 || njobs < 1 || !table_device || total_chunks < 1 ||
+      total_chunks >= ((int64_t)1 << 31) || max_m > 16 || max_entries < 1 ||
+      max_entries >= ((int64_t)1 << 31))
+    return TB_ERR_ARGUMENT;
+  GemvBatch b{};
+  const GemvJob *h = static_cast<const GemvJob *>(table_host);
+  int64_t tab = 0;
+  for (int j = 0; j < njobs; ++j) {
+    b.jobs[j] = h[j];
+    tab = std::max<int64_t>(tab, (int64_t)h[j].M * pad_up(h[j].C, kStageChunks) * rec_bytes_of(fmt));
+  }
+  b.table = nullptr;
+  b.njobs = (int)njobs;
+  b.total = (int)total_chunks;
+  b.defer_finalize = finalize ? 0 : 1;
+  b.max_entries = (int)max_entries;
+  if (prev_njobs > 0) {  // finalise the previous batch in this launch's tail
+    if (!prev_table_host) return TB_ERR_ARGUMENT;
+    const GemvJob *ph = static_cast<const GemvJob *>(prev_table_host);
+    int nf = 0;
+    for (int j = 0; j < prev_njobs; ++j) {
+      if (ph[j].fin_m == 0) continue;  // K-windows finalised through another job
+      if (nf == kMaxInlineFin) return TB_ERR_UNSUPPORTED;
+      FinJob &F = b.in.fin[nf++];
+      F.ws_acc = ph[j].ws_acc;
+      F.acc_out = ph[j].acc_out;
+      F.out64 = ph[j].out64;
+      F.out32 = ph[j].out32;
+      F.a_scale = ph[j].a_scale;
+      F.w_scale = ph[j].w_scale;
+      F.N = ph[j].N;
+      F.Npad = ph[j].Npad;
+      F.M = ph[j].fin_m;
+    }
+    b.in.prev_njobs = nf;
+    b.in.prev_inline = nf > 0 ? 1 : 0;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int st = TB_ERR_UNSUPPORTED;
+  if (tab <= Cfg<TB_I2S, 8, 4>::kRecTabBytes && max_m <= 8) {
+    if (fmt == TB_I2S || fmt == TB_TL1)
+      st = max_m <= 2 ? launch_tgemv<TB_I2S, 2, 4>(b, s, (int)tab)
+           : max_m <= 4 ? launch_tgemv<TB_I2S, 4, 4>(b, s, (int)tab)
+                        : launch_tgemv<TB_I2S, 8, 4>(b, s, (int)tab);
+    if (st == TB_OK || st == TB_ERR_CUDA) return st;
+  }
+  // too large a table or too many segments: the records path, after a
+  // separate finalize launch of the previous batch
+  if (prev_njobs > 0) {
+    GemvBatch pb{};
+    const GemvJob *ph = static_cast<const GemvJob *>(prev_table_host);
+    if (prev_njobs > kMaxInlineJobs) return TB_ERR_UNSUPPORTED;
+    int64_t pe = 1;
+    for (int j = 0; j < prev_njobs; ++j) {
+      pb.jobs[j] = ph[j];
+      pe = std::max<int64_t>(pe, (int64_t)ph[j].fin_m * ph[j].Npad);
+    }
+    pb.table = nullptr;
+    pb.njobs = (int)prev_njobs;
+    pb.max_entries = (int)pe;
+    st = launch_finalize(pb, s);
+    if (st != TB_OK) return st;
+  }
+  b.in = StepInputs{};
+  b.table = static_cast<const GemvJob *>(table_device);
+  return launch_batch(fmt, b, max_m, s);
+}
+
 extern "C" int tb_gemv_step_prepare_cols(int fmt, int64_t njobs, const tb_gemv_desc *descs,
                                          const int32_t *src, const int64_t *col0,
                                          int64_t ninputs, const int64_t *input_k,
@@ -1459,7 +1694,7 @@ extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t nj
       F.w_scale = h[j].w_scale;
       F.N = h[j].N;
       F.Npad = h[j].Npad;
-      F.M = h[j].M;
+      F.M = h[j].fin_m;
     }
     b.in.prev_inline = 1;
   }

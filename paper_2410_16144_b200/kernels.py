@@ -299,12 +299,18 @@ class GemvBatch:
         import numpy as np
 
         lib = L.load()
-        fmts = {p.p.FMT for p, _ in pairs}
+        # (plan, records) or (plan, records, col0): a K-window of the records
+        # (columns [col0, col0 + plan cols); e.g. one of several column shards
+        # of a matrix that share one workspace, only one of them with outputs)
+        pairs = [tuple(pr) if len(pr) == 3 else (pr[0], pr[1], 0) for pr in pairs]
+        fmts = {p.p.FMT for p, _, _ in pairs}
         if len(fmts) != 1:
             raise ValueError("one format per batch")
         self.fmt = fmts.pop()
         descs = (L.GemvDesc * len(pairs))()
-        for d, (plan, rec) in zip(descs, pairs):
+        col0 = (C.c_int64 * len(pairs))(*[int(c) for _, _, c in pairs])
+        rec_cols = (C.c_int64 * len(pairs))(*[int(rec.K) for _, rec, _ in pairs])
+        for d, (plan, rec, _) in zip(descs, pairs):
             d.tiled = plan.main.data_ptr()
             d.tiled_sign = plan.sign.data_ptr() if plan.sign is not None else None
             d.rows, d.cols = plan.p.rows, plan.p.cols
@@ -319,9 +325,10 @@ class GemvBatch:
         total = C.c_int64()
         maxm = C.c_int32()
         maxe = C.c_int64()
-        L.check(lib.tb_gemv_batch_prepare(self.fmt, len(pairs), C.cast(descs, C.c_void_p),
-                                          host.ctypes.data_as(C.c_void_p), C.byref(total),
-                                          C.byref(maxm), C.byref(maxe)), "gemv_batch_prepare")
+        L.check(lib.tb_gemv_batch_prepare_cols(self.fmt, len(pairs), C.cast(descs, C.c_void_p),
+                                               C.cast(col0, C.c_void_p), C.cast(rec_cols, C.c_void_p),
+                                               host.ctypes.data_as(C.c_void_p), C.byref(total),
+                                               C.byref(maxm), C.byref(maxe)), "gemv_batch_prepare")
         dev = pairs[0][0].main.device
         self.table = torch.from_numpy(host).to(dev)
         self._host = host  # host copy of the job table (inline finalize by a later step)
@@ -329,17 +336,23 @@ class GemvBatch:
         self.njobs, self.total, self.max_m = len(pairs), total.value, maxm.value
         self.max_entries = maxe.value
         self.pairs = pairs  # keep every buffer alive
-        self._scale_ptrs = {rec.scales.data_ptr() for _, rec in pairs}
+        self._scale_ptrs = {rec.scales.data_ptr() for _, rec, _ in pairs}
         self._lib = lib
 
-    def run(self, stream_ptr: int | None = None, finalize: bool = True):
+    def run(self, stream_ptr: int | None = None, finalize: bool = True,
+            prev: "GemvBatch | None" = None):
         """One grouped GEMV launch (+ the finalize pass unless ``finalize`` is
-        False, in which case a later StepGlue must finalise this batch)."""
-        st = self._lib.tb_gemv_batch_launch(self.fmt, self.table.data_ptr(), self.njobs,
-                                            self.total, self.max_m, self.max_entries,
-                                            1 if finalize else 0,
-                                            stream_ptr if stream_ptr is not None
-                                            else L.stream_ptr())
+        False, in which case a later launch must finalise this batch).
+        ``prev``: the batch launched before this one (M > 1, I2_S / TL1, <= 10
+        jobs: records-table mode), finalised in this launch's tail."""
+        st = self._lib.tb_gemv_batch_launch_inline(self.fmt, self.table.data_ptr(),
+                                                   self._host_ptr, self.njobs, self.total,
+                                                   self.max_m, self.max_entries,
+                                                   1 if finalize else 0,
+                                                   prev._host_ptr if prev is not None else None,
+                                                   prev.njobs if prev is not None else 0,
+                                                   stream_ptr if stream_ptr is not None
+                                                   else L.stream_ptr())
         if st:
             L.check(st, "gemv_batch_launch")
 

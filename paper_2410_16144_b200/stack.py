@@ -119,6 +119,53 @@ def _slice(p, fmt: str, kind: str, lo: int, hi: int):
                      scale=p.scale, trusted=True)
 
 
+# one M-token records table per CTA (TB_TABLE_KB in csrc/gemv.cu, 124 KB):
+# the longest K-window, in record chunks, whose M-token records fit
+_TABLE_BYTES = 124 * 1024
+
+
+def window_chunks(fmt: str, tokens: int) -> int:
+    rec = 112 if fmt == "tl2" else 80
+    return (_TABLE_BYTES // (tokens * rec)) // 4 * 4
+
+
+class _WindowedView:
+    """A matrix contracted as K-window column shards (one GemvPlan each, one
+    shared workspace, outputs on the first): the packed matrix and its output
+    buffer, as a GemvPlan would hold them."""
+
+    def __init__(self, p, first):
+        self.p = p
+        self.out32, self.out64, self.acc = first.out32, first.out64, first.acc
+        self.ws = first.ws
+        self.windows = []
+
+
+def _windowed(p, fmt: str, tokens: int, src: int, kw: int):
+    """(view, [(plan, input, col0)]): p's columns in windows of <= kw record
+    chunks (near-even, whole 4-chunk groups)."""
+    cw = CHUNK_W[fmt]
+    nchunk = -(-p.cols // cw)
+    nwin = -(-nchunk // kw)
+    per = -(-(-(-nchunk // nwin)) // 4) * 4
+    jobs, first = [], None
+    for w in range(nwin):
+        lo, hi = w * per * cw, min(p.cols, (w + 1) * per * cw)
+        if lo >= hi:
+            break
+        shard = _slice(p, fmt, "row", lo, hi)
+        plan = GemvPlan(shard, max_tokens=tokens,
+                        out_dtype=torch.float32 if first is None else None)
+        if first is None:
+            first = plan
+        else:
+            plan.ws = first.ws  # partial sums of every window accumulate here
+        jobs.append((plan, src, lo))
+    view = _WindowedView(p, first)
+    view.windows = [j[0] for j in jobs]
+    return view, jobs
+
+
 class LayerStack:
     """All layers of a config (this rank's shards) resident on one GPU, plus
     the per-layer launch objects."""
@@ -155,9 +202,16 @@ class LayerStack:
             self.rp_out = torch.empty((self.nlayers, self.part_len), dtype=torch.float32,
                                       device=dev)
         self.layers = []
+        # M > 1 (I2_S / TL1): every CTA of the grouped GEMV keeps its segment's
+        # records in one shared-memory table (tb_gemv_batch_launch_inline);
+        # an input too long for one table is contracted in K-windows, each a
+        # column shard of the matrix, all accumulating into one workspace
+        # that the first window's job finalises.  window_jobs[li]: (plan, input, col0)
+        self.window_jobs = []
+        kw = window_chunks(fmt, tokens) if 1 < tokens <= 8 and fmt != "tl2" else 0
         gen = torch.Generator(device=dev)
         for li in range(self.nlayers):
-            plans = []
+            plans, jobs = [], []
             for mi, (name, rows, cols, src, kind, lo, hi) in enumerate(self.plan):
                 gen.manual_seed(seed * 1_000_003 + li * 131 + mi)
                 w = torch.randn(rows, cols, generator=gen, device=dev) * 0.02
@@ -165,13 +219,21 @@ class LayerStack:
                 del w
                 p = _slice(p, fmt, kind, lo, hi)
                 rowpar = kind == "row"
+                nchunk = -(-p.cols // CHUNK_W[fmt])
+                if kw and nchunk > kw:
+                    view, wjobs = _windowed(p, fmt, tokens, src, kw)
+                    plans.append(view)
+                    jobs += wjobs
+                    continue
                 plan = GemvPlan(p, max_tokens=tokens,
                                 out_dtype=None if rowpar else torch.float32)
                 if rowpar:  # partials land in the layer's slice of the symmetric buffer
                     off = sum(r for j, r in self.rp if j < mi)
                     plan.acc = self.parts[li, off:off + rows].view(1, rows)
                 plans.append(plan)
+                jobs.append((plan, src, 0))
             self.layers.append(plans)
+            self.window_jobs.append(jobs)
         # algorithmic bytes of THIS rank's shards: packed bytes
         # + M * (columns contracted) int8 activations + 4 * M * (rows written)
         self.algo_bytes = sum(packed_bytes(fmt, p.p.rows, p.p.cols) + tokens * p.p.cols
@@ -186,10 +248,12 @@ class LayerStack:
             # layer l-1, whose outputs are scaled by layer l-1's a_scale
             self.rec = [[ActRecords(L.TL2 if fmt == "tl2" else L.I2S, tokens, k)
                          for k in self.ks] for _ in range(2)]
-            self.batches = [GemvBatch([(p, self.rec[li % 2][s[3]])
-                                       for p, s in zip(plans, self.plan)])
-                            for li, plans in enumerate(self.layers)]
+            self.batches = [GemvBatch([(p, self.rec[li % 2][src], c0)
+                                       for p, src, c0 in self.window_jobs[li]])
+                            for li in range(self.nlayers)]
             self.tail = StepGlue([])
+            self.tail_fin = fmt != "tl2" and tokens <= 8 and all(
+                len(j) <= 10 for j in self.window_jobs)
         if self.rp:
             # what the reduction scales: per row-parallel projection
             # (rows, w_scale, the step's device scale of its input)
@@ -220,10 +284,12 @@ class LayerStack:
             if self.rp:
                 self.coll.reduce_layer(self, self.nlayers - 1)
         else:
+            # records-table mode: layer l's launch finalises layer l-1 in its
+            # tail, so the glue only quantises; otherwise the glue finalises
             prev = None
             for li, b in enumerate(self.batches):
-                glue_pool[li].retarget(prev).run()
-                b.run(finalize=False)
+                glue_pool[li].retarget(None if self.tail_fin else prev).run()
+                b.run(finalize=False, prev=prev if self.tail_fin else None)
                 prev = b
             self.tail.retarget(prev).run()
 

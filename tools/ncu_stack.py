@@ -16,6 +16,7 @@ if os.environ.get("TB_LIB"):
     L.load(os.environ["TB_LIB"])
 
 from paper_2410_16144_b200.stack import STACKS, LayerStack  # noqa: E402
+from paper_2410_16144_b200 import kernels as tb_kernels  # noqa: E402
 
 
 def main():
@@ -43,6 +44,51 @@ def main():
                 pool_[li].retarget(prev).run()
                 prev = b
         st.token_pass = glue_only
+    elif os.environ.get("ONLY") == "gq" and M > 1:  # timing only: the glues' quantisation
+        def gq(xh_, xi_, pool_):
+            for li in range(len(st.batches)):
+                pool_[li].retarget(None).run()
+        st.token_pass = gq
+    elif os.environ.get("ONLY") == "gf" and M > 1:  # timing only: the glues' finalize
+        fin = tb_kernels.StepGlue([])
+
+        def gf(xh_, xi_, pool_):
+            for b in st.batches:
+                fin.retarget(b).run()
+        st.token_pass = gf
+    elif os.environ.get("ONLY") == "gemvq" and M > 1:  # timing only: quantise + GEMV (no finalize)
+        def gemvq(xh_, xi_, pool_):
+            for li, b in enumerate(st.batches):
+                pool_[li].retarget(None).run()
+                b.run(finalize=False)
+        st.token_pass = gemvq
+    elif os.environ.get("ONLY") == "gemvf" and M > 1:  # timing only: finalize + GEMV (no quantise)
+        fin2 = tb_kernels.StepGlue([])
+
+        def gemvf(xh_, xi_, pool_):
+            prev = None
+            for b in st.batches:
+                fin2.retarget(prev).run() if prev is not None else None
+                b.run(finalize=False)
+                prev = b
+        st.token_pass = gemvf
+    if os.environ.get("ONLY") == "gemvp" and M > 1:  # timing only: GEMV + tail finalize (no glue)
+        def gemvp(xh_, xi_, pool_):
+            prev = None
+            for b in st.batches:
+                b.run(finalize=False, prev=prev)
+                prev = b
+        st.token_pass = gemvp
+    if os.environ.get("GRAPH"):
+        run1 = st.token_pass
+        run1(xh, xi, pool)
+        torch.cuda.synchronize()
+        s_ = torch.cuda.Stream()
+        s_.wait_stream(torch.cuda.current_stream())
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s_), torch.cuda.graph(gr, stream=s_):
+            run1(xh, xi, pool)
+        st.token_pass = lambda *a: gr.replay()
     for _ in range(4):
         st.token_pass(xh, xi, pool)
     torch.cuda.synchronize()
