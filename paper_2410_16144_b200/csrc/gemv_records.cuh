@@ -889,19 +889,19 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
       }
 #endif
     } else {
-      // TL2 (packing.py:63-74): d = 13 + idx (sign 0) or 13 - idx (sign 1) is
-      // the base-3 number of the triple's codes (c0 c1 c2).
-      const uint32_t S = (sgn >> (8 * i)) & 0xFFu;
+      // TL2 (packing.py:63-74): the tiled layout holds v = 13 + signed index =
+      // the base-3 number 9 c0 + 3 c1 + c2 of the triple's codes (c = w + 1),
+      // bits 0-3 in the index plane, bit 4 in the sign plane (pack.cu repack).
+      const uint32_t S = sgn >> (8 * i);
       const uint32_t lo = W & 0x0F0F0F0Fu, hi = (W >> 4) & 0x0F0F0F0Fu;
-      // byte-wide sign masks: even sign bits -> low-nibble triples, odd -> high
-      const uint32_t mlo = prmt((S & 0x55u) * 0x02082080u, 0u, 0xBA98u);
-      const uint32_t mhi = prmt((S & 0xAAu) * 0x01041040u, 0u, 0xBA98u);
+      // bit 4 of every byte: even plane bits -> low-nibble triples, odd -> high
+      // (the multiplies place bit 2b / 2b + 1 at bit 8b + 4, carry-free there)
+      const uint32_t vlo = lo | (((S & 0x55u) * 0x00410410u) & 0x10101010u);
+      const uint32_t vhi = hi | (((S & 0xAAu) * 0x00208208u) & 0x10101010u);
       uint32_t code[6];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const uint32_t x = h ? hi : lo;
-        const uint32_t msk = h ? mhi : mlo;
-        const uint32_t d = lop3_sel(x + 0x0D0D0D0Du, 0x0D0D0D0Du - x, msk);
+        const uint32_t d = h ? vhi : vlo;
         const uint32_t c0 = ((d * 7u + 0x07070707u) >> 6) & 0x03030303u;  // d / 9
         const uint32_t r = d - 9u * c0;                                      // d % 9
         const uint32_t c1 = __umulhi(r, 11u << 27) & 0x03030303u;           // r / 3

@@ -196,6 +196,37 @@ __device__ __forceinline__ uint8_t codes_to_tl1(uint32_t c) {
   return (uint8_t)(lo | (hi << 4));
 }
 
+// TL2 triples are re-encoded on the way to the tiled layout: (sign s, index
+// idx) -> v = 13 + (s ? -idx : idx) = 9 c0 + 3 c1 + c2 (c = w + 1, the
+// base-3 number of the triple, packing.py:63-74), low 4 bits in the index
+// plane and bit 4 in the sign plane: the same 5 bits per triple, a
+// bijection (zero is v = 13), and the decode needs no sign masks (the digits
+// come straight from v).  tb_unrepack inverts it.
+__device__ __forceinline__ void tl2_to_v(uint8_t *idx16, uint32_t &sgn32) {
+  uint32_t out = 0;
+#pragma unroll
+  for (int t = 0; t < 32; ++t) {
+    const uint32_t nib = (idx16[t >> 1] >> (4 * (t & 1))) & 15u;
+    const uint32_t s = (sgn32 >> t) & 1u;
+    const uint32_t v = s ? 13u - nib : 13u + nib;
+    idx16[t >> 1] = (uint8_t)((idx16[t >> 1] & (0xF0u >> (4 * (t & 1)))) | ((v & 15u) << (4 * (t & 1))));
+    out |= (v >> 4) << t;
+  }
+  sgn32 = out;
+}
+__device__ __forceinline__ void v_to_tl2(uint8_t *idx16, uint32_t &bits32) {
+  uint32_t out = 0;
+#pragma unroll
+  for (int t = 0; t < 32; ++t) {
+    const uint32_t v = ((idx16[t >> 1] >> (4 * (t & 1))) & 15u) | (((bits32 >> t) & 1u) << 4);
+    const uint32_t s = v < 13u ? 1u : 0u;
+    const uint32_t nib = s ? 13u - v : v - 13u;
+    idx16[t >> 1] = (uint8_t)((idx16[t >> 1] & (0xF0u >> (4 * (t & 1)))) | (nib << (4 * (t & 1))));
+    out |= s << t;
+  }
+  bits32 = out;
+}
+
 __global__ void repack_kernel(int fmt, const uint8_t *ref, const uint8_t *ref_sign, int64_t rows,
                               int64_t cols, uint8_t *tiled, uint8_t *tiled_sign, int64_t C,
                               int64_t T) {
@@ -216,9 +247,7 @@ __global__ void repack_kernel(int fmt, const uint8_t *ref, const uint8_t *ref_si
       buf[b] = (r < rows && j < rb) ? ref[r * rb + j] : zb;
       if (fmt == TB_TL1) buf[b] = tl1_to_codes(buf[b]);
     }
-    uint4 v;
-    memcpy(&v, buf, 16);
-    reinterpret_cast<uint4 *>(tiled)[i] = v;
+    uint32_t sv = 0;
     if (fmt == TB_TL2) {
       uint8_t sb[4];
 #pragma unroll
@@ -226,10 +255,13 @@ __global__ void repack_kernel(int fmt, const uint8_t *ref, const uint8_t *ref_si
         int64_t j = 4 * c + b;
         sb[b] = (r < rows && j < sbpr) ? ref_sign[r * sbpr + j] : 0;
       }
-      uint32_t sv;
       memcpy(&sv, sb, 4);
+      tl2_to_v(buf, sv);
       reinterpret_cast<uint32_t *>(tiled_sign)[i] = sv;
     }
+    uint4 v;
+    memcpy(&v, buf, 16);
+    reinterpret_cast<uint4 *>(tiled)[i] = v;
   }
 }
 
@@ -244,13 +276,27 @@ __global__ void unrepack_kernel(int fmt, const uint8_t *tiled, const uint8_t *ti
     if (i < rows * rb) {
       int64_t r = i / rb, j = i % rb;
       int64_t t = r / kRowTile, rin = r % kRowTile, c = j / 16, b = j % 16;
-      const uint8_t v = tiled[((t * C + c) * kRowTile + rin) * 16 + b];
-      ref[i] = fmt == TB_TL1 ? codes_to_tl1(v) : v;
+      const int64_t q = (t * C + c) * kRowTile + rin;
+      if (fmt == TB_TL2) {  // the chunk's triples back to (sign, index)
+        uint8_t idx16[16];
+        memcpy(idx16, tiled + q * 16, 16);
+        uint32_t bits = reinterpret_cast<const uint32_t *>(tiled_sign)[q];
+        v_to_tl2(idx16, bits);
+        ref[i] = idx16[b];
+      } else {
+        const uint8_t v = tiled[q * 16 + b];
+        ref[i] = fmt == TB_TL1 ? codes_to_tl1(v) : v;
+      }
     } else {
       int64_t k = i - rows * rb;
       int64_t r = k / sbpr, j = k % sbpr;
       int64_t t = r / kRowTile, rin = r % kRowTile, c = j / 4, b = j % 4;
-      ref_sign[k] = tiled_sign[((t * C + c) * kRowTile + rin) * 4 + b];
+      const int64_t q = (t * C + c) * kRowTile + rin;
+      uint8_t idx16[16];
+      memcpy(idx16, tiled + q * 16, 16);
+      uint32_t bits = reinterpret_cast<const uint32_t *>(tiled_sign)[q];
+      v_to_tl2(idx16, bits);
+      ref_sign[k] = (uint8_t)(bits >> (8 * b));
     }
   }
 }
