@@ -148,6 +148,8 @@ struct Cfg {
                                : FU == 4 ? TB_TABLE_RING
                                : (MT == 1 ? TB_MT1_RING : (kFit >= 4 ? 4 : (kFit >= 2 ? kFit : 2)));
   static constexpr int kThreads = 32 * kWarps;
+  // fused step: previous-step outputs finalised per thread at the wait point
+  static constexpr int kFinPer = FU == 3 ? 3 : 2;
   // fused step: records live in a CTA-wide table after the ring, not per stage
   static constexpr int kStageBytes =
       kStageChunks * (kTileChunkBytes + Fmt<FMT>::kSignBytes + (kFused || kTable ? 0 : MT) * Fmt<FMT>::kRecBytes);
@@ -864,7 +866,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
   // stores happen at the end, so no load latency sits in the CTA's tail.
   // Two entries per thread (a 148 x 160-thread grid covers 23,680 of the
   // cfg1 step's 32,768): both read-and-resets go out together at the wait.
-  constexpr int kFinPer = FU == 3 ? 3 : 2;  // medium CTAs: 148 x 256 x 3 >= the 98,304 cfg4 rows
+  constexpr int kFinPer = CF::kFinPer;  // medium CTAs: 148 x 256 x 3 >= the 98,304 cfg4 rows
   int fin_j[kFinPer];
   int64_t fin_k[kFinPer];
   int32_t fin_v[kFinPer];
@@ -1183,7 +1185,14 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
 #ifndef TB_MIN_WARP_CHUNKS
 #define TB_MIN_WARP_CHUNKS 32
 #endif
-  const int64_t want = ceil_div(b.total, (int64_t)CF::kWarps * TB_MIN_WARP_CHUNKS);
+  int64_t want = ceil_div(b.total, (int64_t)CF::kWarps * TB_MIN_WARP_CHUNKS);
+  if (kFused && b.in.prev_inline) {
+    // ... but enough threads that the previous step's outputs are finalised
+    // at kFinPer entries per thread, not in the serial tail loop
+    int64_t prev = 0;
+    for (int j = 0; j < b.in.prev_njobs; ++j) prev += (int64_t)b.in.fin[j].M * b.in.fin[j].Npad;
+    want = std::max<int64_t>(want, ceil_div(prev, (int64_t)CF::kThreads * CF::kFinPer));
+  }
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count_cached(), want));
   if (kFused && kStepCQ > 1 && grid > kStepCQ) grid -= grid % kStepCQ;  // whole CTA clusters
   const int nw = grid * CF::kWarps;

@@ -818,16 +818,3 @@ class ActRecords:
         if st:
             L.check(st, "prep_activations")
         return self
-
-    def chunk_slice(self, c0: int, c1: int) -> "ActRecords":
-        """Records of chunks [c0, c1) (one token): the input of a K-sharded
-        (row-parallel) GEMV whose shard starts at chunk c0."""
-        if self.M != 1:
-            raise ValueError("chunk_slice needs a single-token record buffer")
-        rb = 112 if self.fmt == L.TL2 else 80
-        v = object.__new__(ActRecords)
-        v.fmt, v.M, v._lib, v.natural = self.fmt, 1, self._lib, None
-        v.K = self.K
-        v.buf = self.buf[c0 * rb: c1 * rb]
-        v.scales = self.scales
-        return v

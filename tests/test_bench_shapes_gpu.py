@@ -255,3 +255,35 @@ def test_glue_refuses_scale_hazard(tb):
     with pytest.raises(ValueError, match="alternate two ActRecords sets"):
         tb.StepGlue([(x, rec)], finalize=batch)
     tb.StepGlue([(x, rec2)], finalize=batch)  # a different set is fine
+
+
+def test_small_step_after_large(tb):
+    """A small fused step (its grid sized down by the chunks-per-warp rule)
+    finalises a LARGE previous step: the grid must still cover the previous
+    outputs (the launch keeps enough threads), and both steps'
+    outputs are exact."""
+    rng = np.random.default_rng(12)
+    H, I = 4096, 14336
+    big = []
+    for rows, cols in ((I, H), (H, I)):
+        v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+        big.append((tb.GemvPlan(tb.encode_i2s(tb.TernaryMatrix(rows, cols, v, 0.5)),
+                                out_dtype=torch.float32), v))
+    vs = rng.integers(-1, 2, size=(40, 256), dtype=np.int8)
+    small = tb.GemvPlan(tb.encode_i2s(tb.TernaryMatrix(40, 256, vs, 0.25)), out_dtype=torch.float32)
+    s_big = tb.GemvStep([(big[0][0], 0), (big[1][0], 1)], [H, I])
+    s_small = tb.GemvStep([(small, 0)], [256])
+    xh = rng.standard_normal(H).astype(np.float32)
+    xi = rng.standard_normal(I).astype(np.float32)
+    xs = rng.standard_normal(256).astype(np.float32)
+    s_big.run([torch.from_numpy(xh).cuda(), torch.from_numpy(xi).cuda()])
+    s_small.run([torch.from_numpy(xs).cuda()], prev=s_big)  # finalises the big step
+    s_small.finalize()
+    torch.cuda.synchronize()
+    for (plan, v), x in zip(big, (xh, xi)):
+        q, s = CO.quantize(x, 4)
+        want = O.make_output(CO.gemv_i2s(O.encode_i2s(v), q, 0), 0.5, s).astype(np.float32)
+        assert np.array_equal(host(plan.out32[0]), want)
+    q, s = CO.quantize(xs, 4)
+    want = O.make_output(CO.gemv_i2s(O.encode_i2s(vs), q, 0), 0.25, s).astype(np.float32)
+    assert np.array_equal(host(small.out32[0]), want)
