@@ -233,6 +233,15 @@ typedef struct tb_quant_desc {
 int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
                  int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
                  void *stream);
+/* As tb_step_glue; flags & TB_GLUE_EARLY_QUANT: the quantisation runs
+ * before the programmatic-dependent-launch wait on the preceding kernel
+ * (overlapping it), the finalize after it, and every CTA waits before
+ * exiting.  The caller guarantees the inputs do not depend on the preceding
+ * kernel and that no kernel still in flight reads the records or scales
+ * being written (e.g. three record sets in rotation).                     */
+#define TB_GLUE_EARLY_QUANT 1
+int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs, int64_t fin_max_entries,
+                    int64_t nq, const tb_quant_desc *q, int32_t flags, void *stream);
 /* Fused one-token decode step in ONE launch (gemv.cu, tgemv_kernel<.,1,true>):
  * every CTA quantises the float32 input vectors itself (quantize_activations,
  * core.py:116-134, records kept in shared memory), streams the grouped GEMV

@@ -56,6 +56,7 @@ _SIGS = {
     "tb_gemv_batch_prepare": (_i32, [_i32, _i64, _p, _p, _p, _p, _p]),
     "tb_gemv_batch_launch": (_i32, [_i32, _p, _i64, _i64, _i32, _i64, _i32, _p]),
     "tb_step_glue": (_i32, [_p, _i64, _i64, _i64, _p, _p]),
+    "tb_step_glue_ex": (_i32, [_p, _i64, _i64, _i64, _p, _i32, _p]),
     "tb_gemv_step_prepare": (_i32, [_i32, _i64, _p, _p, _i64, _p, _p, _p, _p]),
     "tb_gemv_step_prepare_cols": (_i32, [_i32, _i64, _p, _p, _p, _i64, _p, _p, _p, _p]),
     "tb_gemv_step_launch": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _i32, _p, _i64, _p, _p, _p]),

@@ -400,6 +400,7 @@ struct GlueParams {
   GemvBatch fin;  // fin.njobs == 0: nothing to finalise
   QuantVec q[kMaxGlueVecs];
   int nq, q_tokens;
+  int early;      // quantise before griddepcontrol.wait (TB_GLUE_EARLY_QUANT)
 };
 
 template <int FMT>
@@ -479,7 +480,11 @@ __device__ __forceinline__ void glue_finalize_flat(const GemvBatch &b, int part,
 }
 
 __global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueParams g) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // early: the quantisation (inputs that do not depend on the preceding
+  // kernel, records that nothing in flight reads -- the caller's contract)
+  // overlaps the preceding kernel; every CTA still waits for it before
+  // exiting, so this grid's completion implies the predecessor's
+  if (!g.early) asm volatile("griddepcontrol.wait;" ::: "memory");
   // the next GEMV group may launch now: its prologue prefetches weights (no
   // dependence on us) and then waits for this grid before reading records
   asm volatile("griddepcontrol.launch_dependents;");
@@ -492,7 +497,11 @@ __global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueP
     }
     if (g.q[v].fmt == TB_TL2) glue_quant<TB_TL2>(g.q[v], m);
     else glue_quant<TB_I2S>(g.q[v], m);  // I2_S and TL1 share the record layout
-  } else if (g.fin.njobs <= kMaxGlueFin) {
+    if (g.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
+  if (g.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (g.fin.njobs <= kMaxGlueFin) {
     const int r = y - g.q_tokens;  // finalize rows: flat over every job's entries
     glue_finalize_flat(g.fin, r * gridDim.x + blockIdx.x, g.fin.fin_parts * gridDim.x);
   } else {
@@ -1727,9 +1736,18 @@ extern "C" int tb_gemv_batch_finalize(const void *table_device, int64_t njobs,
   return launch_finalize(b, static_cast<cudaStream_t>(stream));
 }
 
+extern "C" int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs,
+                               int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
+                               int32_t flags, void *stream);
 extern "C" int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
                             int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
                             void *stream) {
+  return tb_step_glue_ex(fin_table_device, fin_njobs, fin_max_entries, nq, q, 0, stream);
+}
+
+extern "C" int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs,
+                               int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
+                               int32_t flags, void *stream) {
   if (nq < 0 || nq > kMaxGlueVecs || (nq > 0 && !q) || fin_njobs < 0 ||
       (fin_njobs > 0 && (!fin_table_device || fin_max_entries < 1 ||
                          fin_max_entries >= ((int64_t)1 << 31))))
@@ -1738,6 +1756,7 @@ extern "C" int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
   g.fin.table = static_cast<const GemvJob *>(fin_table_device);
   g.fin.njobs = (int)fin_njobs;
   g.nq = (int)nq;
+  g.early = (flags & 1) ? 1 : 0;
   int tokens = 0;
   for (int64_t v = 0; v < nq; ++v) {
     const tb_quant_desc &d = q[v];

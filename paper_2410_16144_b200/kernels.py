@@ -365,11 +365,16 @@ class StepGlue:
     they must stay allocated (e.g. a fixed buffer refilled every step).
     """
 
-    def __init__(self, inputs, finalize: "GemvBatch | None" = None):
+    def __init__(self, inputs, finalize: "GemvBatch | None" = None, early: bool = False):
+        """``early``: quantise before waiting on the preceding kernel
+        (TB_GLUE_EARLY_QUANT) -- only when the inputs do not depend on it and
+        nothing in flight reads these records (e.g. three record sets in
+        rotation, the GEMV finalising its predecessor)."""
         import ctypes as C
 
         self._lib = L.load()
         self.inputs = inputs
+        self._flags = 1 if early else 0
         self.fin = None
         self.descs = (L.QuantDesc * max(1, len(inputs)))()
         for d, (x, rec) in zip(self.descs, inputs):
@@ -394,11 +399,11 @@ class StepGlue:
 
     def run(self, stream_ptr: int | None = None):
         fin = self.fin
-        st = self._lib.tb_step_glue(fin.table.data_ptr() if fin is not None else None,
-                                    fin.njobs if fin is not None else 0,
-                                    fin.max_entries if fin is not None else 0, len(self.inputs),
-                                    self._descs_ptr,
-                                    stream_ptr if stream_ptr is not None else L.stream_ptr())
+        st = self._lib.tb_step_glue_ex(fin.table.data_ptr() if fin is not None else None,
+                                       fin.njobs if fin is not None else 0,
+                                       fin.max_entries if fin is not None else 0,
+                                       len(self.inputs), self._descs_ptr, self._flags,
+                                       stream_ptr if stream_ptr is not None else L.stream_ptr())
         if st:
             L.check(st, "step_glue")
 

@@ -243,17 +243,22 @@ class LayerStack:
                                     for p, s in zip(plans, self.plan)], self.ks)
                           for plans in self.layers]
         else:
-            # two record sets, alternating by layer: the glue of layer l writes
-            # layer l's scales/records while (in the same launch) finalising
-            # layer l-1, whose outputs are scaled by layer l-1's a_scale
+            # record sets in rotation.  Glue finalise mode (the glue of layer
+            # l quantises layer l while finalising layer l-1, whose outputs are
+            # scaled by layer l-1's a_scale): two sets.  Tail finalise mode
+            # (records tables; GEMV l finalises layer l-1 in its tail; glue l
+            # quantises BEFORE waiting on GEMV l-1, overlapping it): three
+            # sets -- glue l writes set l % 3 while GEMV l-1 reads set (l-1) % 3
+            # and finalises with set (l-2) % 3's scales.
+            self.tail_fin = fmt != "tl2" and tokens <= 8 and all(
+                len(j) <= 10 for j in self.window_jobs)
+            self.nsets = 3 if self.tail_fin else 2
             self.rec = [[ActRecords(L.TL2 if fmt == "tl2" else L.I2S, tokens, k)
-                         for k in self.ks] for _ in range(2)]
-            self.batches = [GemvBatch([(p, self.rec[li % 2][src], c0)
+                         for k in self.ks] for _ in range(self.nsets)]
+            self.batches = [GemvBatch([(p, self.rec[li % self.nsets][src], c0)
                                        for p, src, c0 in self.window_jobs[li]])
                             for li in range(self.nlayers)]
             self.tail = StepGlue([])
-            self.tail_fin = fmt != "tl2" and tokens <= 8 and all(
-                len(j) <= 10 for j in self.window_jobs)
         if self.rp:
             # what the reduction scales: per row-parallel projection
             # (rows, w_scale, the step's device scale of its input)
@@ -295,7 +300,9 @@ class LayerStack:
 
     def make_glues(self, XH, XI):
         """M > 1: one StepGlue per layer quantising rows of XH[l] / XI[l] ([M, K])."""
-        return [StepGlue([(XH[li], self.rec[li % 2][0]), (XI[li], self.rec[li % 2][1])])
+        n = self.nsets
+        return [StepGlue([(XH[li], self.rec[li % n][0]), (XI[li], self.rec[li % n][1])],
+                         early=self.tail_fin)
                 for li in range(self.nlayers)]
 
     def outputs(self, li: int) -> dict:
