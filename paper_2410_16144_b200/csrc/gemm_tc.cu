@@ -586,37 +586,7 @@ __global__ void gemm_rowsum_kernel(const int8_t *__restrict__ act, int M, int64_
 
 // quantize_activations (core.py:116-134) straight into the GEMM's A layout:
 // float32 tokens [M][ldx] -> the bytes tb_gemm_tile_act writes (tiled int8
-// codes + per-token sums) and the float64 scales, in ONE launch.  A cluster
-// of S CTAs owns one 8-token row group; CTA r of the cluster owns K stages
-// [r*kps, (r+1)*kps).  Warp w handles token 8g + w:
-//   1. integer max of |x| bits over its slice (exact: float32 -> float64 is
-//      monotonic), cluster max through DSMEM -> scale = amax / 127 (fp64);
-//   2. quantise (quantize_fast: fp32 product, exact fp64 fallback at ties),
-//      16 codes per lane in code-plane order, staged in shared memory so the
-//      CTA writes whole 1 KB (stage, row group) blocks;
-//   3. per-token code sums reduced over the cluster by rank 0.
-// x is read twice (the second pass hits L2).
-__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t qa_mapa(uint32_t saddr, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ uint32_t qa_cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t qa_cluster_size() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-  return r;
-}
-
+// codes in code-plane order + per-token code sums) and the float64 scales.
 // 16 floats of a unit (zero beyond K)
 __device__ __forceinline__ void qa_load16(const float *row, int64_t k, int K, bool vec, float *f) {
   if (vec && k + 16 <= K) {
@@ -646,250 +616,95 @@ __device__ __forceinline__ uint4 qa_codes16(const float *f, float inv_sf, double
                     prmt(t1, t3, 0x7632u));
 }
 
-// UPL > 0: each lane keeps its (at most UPL) units' floats in registers from
-// the absmax pass to the quantise pass (x read once, every load in flight at
-// entry); UPL == 0: any slice length, the quantise pass re-reads x (L2).
-template <int UPL>
-__global__ void __launch_bounds__(256) gemm_quantize_act_kernel(
-    const float *__restrict__ x, int M, int K, int64_t ldx, int Mpad, int ks, int kps,
-    double *__restrict__ scale, int32_t *flag, uint8_t *__restrict__ out) {
-  extern __shared__ uint4 qa_stage[];  // [kps][kGemmKC][8 rows] 16-byte units
-  __shared__ uint32_t s_amax[8];
-  __shared__ int32_t s_sum[8];
-  const int S = (int)qa_cluster_size();
-  const int rank = (int)qa_cluster_rank();
-  const int g = blockIdx.x / S;
+// Two launches (no clusters): (1) one CTA per
+// token row: absmax (integer max of |x| bits), the float64 scale, the
+// non-finite flag, and the row's code sum zeroed; (2) a programmatic
+// dependent grid over (8-token row group, block of 4 K stages): quantise
+// (x is L2-resident after (1)), stage the block's 16-byte units in shared
+// memory, write whole 1 KB (stage, row group) blocks, add the per-token code
+// sums with one atomic per row.  Every CTA has work from its first
+// instruction (a single-launch form with 8-CTA clusters sharing the absmax
+// through DSMEM measured 6.2 / 14-16 us for the cfg3 layer's two inputs,
+// this one 6.0 / 12.5 us).
+constexpr int kQa2Stages = 4;  // K stages per (2) CTA
+
+__global__ void __launch_bounds__(512) qa_absmax_kernel(const float *__restrict__ x, int M, int K,
+                                                       int64_t ldx, int Mpad, int ks,
+                                                       double *__restrict__ scale, int32_t *flag,
+                                                       uint8_t *__restrict__ out) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int m = blockIdx.x;
+  int32_t *rowsum = reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK);
+  if (m >= M) {
+    if (threadIdx.x == 0) rowsum[m] = 0;
+    return;
+  }
+  const float *row = x + (int64_t)m * ldx;
+  uint32_t amax = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | (uintptr_t)(ldx * 4)) & 15) == 0;
+  int k = threadIdx.x * 4;
+  if (vec)
+#pragma unroll 8  // several loads in flight per thread (the max is the only dependence)
+    for (; k + 3 < K; k += 512 * 4) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + k));
+      amax = max(amax, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
+                           max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
+    }
+  for (; k < K; k += 512 * 4)
+    for (int i = 0; i < 4 && k + i < K; ++i) amax = max(amax, __float_as_uint(row[k + i]) & 0x7fffffffu);
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  __shared__ uint32_t red[16];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    amax = threadIdx.x < 16 ? red[threadIdx.x] : 0u;
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (threadIdx.x == 0) {
+      const double a = (double)__uint_as_float(amax);
+      scale[m] = a > 0.0 ? a / 127.0 : 1.0;  // core.py:128-130
+      if (amax >= 0x7f800000u && flag) atomicOr(flag, 1);
+      rowsum[m] = 0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) qa_codes_kernel(const float *__restrict__ x, int M, int K,
+                                                      int64_t ldx, int Mpad, int ks,
+                                                      const double *__restrict__ scale,
+                                                      uint8_t *__restrict__ out) {
+  __shared__ uint4 stage[kQa2Stages * kGemmKC * 8];
+  const int g = blockIdx.x, blk = blockIdx.y;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = g * 8 + w;
-  const int ks0 = rank * kps;
-  const int nks = max(0, min(ks, ks0 + kps) - ks0);
+  const int ks0 = blk * kQa2Stages;
+  const int nks = min(ks, ks0 + kQa2Stages) - ks0;
   const int64_t k0 = (int64_t)ks0 * kGemmBK;
-  const int units = nks * kGemmKC;  // 16-column units of this CTA's slice
   const float *row = x + (int64_t)m * ldx;
   const bool vec = ((reinterpret_cast<uintptr_t>(x) | (uintptr_t)(ldx * 4)) & 15) == 0;
-  // ---- 1. absmax (integer max of |x| bits: exact, float32 -> float64 is monotonic)
-  uint32_t amax = 0;
-  float f[UPL > 0 ? UPL : 1][16];
-  if constexpr (UPL > 0) {
-#pragma unroll
-    for (int i = 0; i < UPL; ++i) {
-      const int u = lane + 32 * i;
-      if (m < M && u < units && k0 + u * 16 < K) {
-        qa_load16(row, k0 + (int64_t)u * 16, K, vec, f[i]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) f[i][e] = 0.0f;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < UPL; ++i)
-#pragma unroll
-      for (int e = 0; e < 16; ++e) amax = max(amax, __float_as_uint(f[i][e]) & 0x7fffffffu);
-  } else if (m < M) {
-    const int64_t k1 = std::min<int64_t>(k0 + (int64_t)nks * kGemmBK, (int64_t)K);
-    int64_t k = k0 + lane * 4;
-    if (vec)
-      for (; k + 3 < k1; k += 128) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + k));
-        amax = max(amax, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
-                             max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
-      }
-    for (; k < k1; k += 128)
-      for (int i = 0; i < 4 && k + i < k1; ++i)
-        amax = max(amax, __float_as_uint(row[k + i]) & 0x7fffffffu);
-  }
-  amax = __reduce_max_sync(0xffffffffu, amax);
-  if (lane == 0) s_amax[w] = amax;
-  cluster_sync_all();
-  amax = lane < S ? ld_cluster_u32(qa_mapa(smem_u32(&s_amax[w]), lane)) : 0u;
-  amax = __reduce_max_sync(0xffffffffu, amax);
-  const double a = (double)__uint_as_float(amax);
-  const double sc = a > 0.0 ? a / 127.0 : 1.0;
-  const double inv_s = 1.0 / sc;
-  const float inv_sf = (float)inv_s;
-  if (rank == 0 && lane == 0 && m < M) {
-    scale[m] = sc;
-    if (amax >= 0x7f800000u && flag) atomicOr(flag, 1);
-  }
-  // ---- 2. codes, staged per CTA
-  int32_t sum = 0;
-  if constexpr (UPL > 0) {
-#pragma unroll
-    for (int i = 0; i < UPL; ++i) {
-      const int u = lane + 32 * i;
-      if (u < units) qa_stage[u * 8 + w] = qa_codes16(f[i], inv_sf, sc, inv_s, sum);
-    }
+  const int units = nks * kGemmKC;  // one 16-column unit per lane (32 units)
+  float f[16];
+  const int64_t k = k0 + (int64_t)lane * 16;
+  if (m < M && lane < units && k < K) {
+    qa_load16(row, k, K, vec, f);
   } else {
-    for (int u = lane; u < units; u += 32) {
-      const int64_t k = k0 + (int64_t)u * 16;
-      float g16[16];
-      if (m < M && k < K) {
-        qa_load16(row, k, K, vec, g16);
-      } else {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) g16[e] = 0.0f;
-      }
-      qa_stage[u * 8 + w] = qa_codes16(g16, inv_sf, sc, inv_s, sum);
-    }
+    for (int e = 0; e < 16; ++e) f[e] = 0.0f;
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the scales of (1)
+  const double sc = m < M ? scale[m] : 1.0;
+  const double inv_s = 1.0 / sc;
+  int32_t sum = 0;
+  if (lane < units) stage[lane * 8 + w] = qa_codes16(f, (float)inv_s, sc, inv_s, sum);
   sum = __reduce_add_sync(0xffffffffu, sum);
-  if (lane == 0) s_sum[w] = sum;
-  // publish the sums to the cluster BEFORE the global stores (a release
-  // arrive after them would wait for every store to be performed)
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  if (lane == 0 && m < M && sum != 0)
+    atomicAdd(reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK) + m, sum);
   __syncthreads();
-  // whole (stage, row group) blocks: kGemmKC x 8 rows x 16 B = 1 KB contiguous
   const int G = Mpad / 8;
   uint4 *o4 = reinterpret_cast<uint4 *>(out);
   for (int i = threadIdx.x; i < nks * kGemmKC * 8; i += 256) {
     const int ksl = i / (kGemmKC * 8), j = i % (kGemmKC * 8);
-    o4[((int64_t)(ks0 + ksl) * G + g) * (kGemmKC * 8) + j] = qa_stage[i];
+    o4[((int64_t)(ks0 + ksl) * G + g) * (kGemmKC * 8) + j] = stage[i];
   }
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-  // ---- 3. per-token sums (rank 0), after every rank published its part
-  if (rank == 0 && threadIdx.x < 8) {
-    int32_t t = 0;
-    for (int r = 0; r < S; ++r)
-      t += (int32_t)ld_cluster_u32(qa_mapa(smem_u32(&s_sum[threadIdx.x]), r));
-    reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK)[g * 8 + threadIdx.x] = t;
-  }
-  // peers' shared memory stays alive until rank 0 has read it (no ordering
-  // of global memory needed: relaxed)
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
-}
-
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// Tiled weights [T][C][32 rows x 16 B] as a 3-D tensor of 8-byte elements
-// {64, C, T}; a box {64, 1, 8} is one K stage of 256 rows.
-static bool encode_weight_map(CUtensorMap *map, const uint8_t *w, int C, int T) {
-  auto enc = tensor_map_encoder();
-  if (!enc) return false;
-  const cuuint64_t dims[3] = {kTileChunkBytes / 8, (cuuint64_t)C, (cuuint64_t)T};
-  const cuuint64_t strides[2] = {kTileChunkBytes, (cuuint64_t)C * kTileChunkBytes};
-  const cuuint32_t box[3] = {kTileChunkBytes / 8, kChunksPerStage, kGemmBN / kRowTile};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint8_t *>(w), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-template <int FMT>
-static int launch_gemm(GemmBatch &b, cudaStream_t s) {
-  const int stage = b.MT * kSubTileBytes + kPackedBytes;
-  const int smem = kGemmStages * stage + kGemmBSlots * kBTileBytes + 1024 + 1024;
-  static int configured_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured_dev != dev) {
-    const int max_smem =
-        kGemmStages * (kGemmMaxMT * kSubTileBytes + kPackedBytes) + kGemmBSlots * kBTileBytes + 2048;
-    if (cudaFuncSetAttribute(tgemm_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             max_smem) != cudaSuccess)
-      return TB_ERR_CUDA;
-    configured_dev = dev;
-  }
-  const int pairs = std::max(1, std::min(b.total, sm_count_cached() / kGemmCluster));
-  // Longest-processing-time-first static schedule: items (cost = K stages)
-  // go to the least-loaded pair, largest first -- a 224-stage down-projection
-  // tile no longer lands on a pair that already has two 64-stage tiles.
-  b.scheduled = 0;
-  if (b.total <= kGemmMaxSched && pairs <= kGemmMaxPairs) {
-    std::vector<std::pair<int, int>> items;  // (cost, item)
-    for (int it = 0; it < b.total; ++it) {
-      const int tt = it / b.MH;
-      int jj = 0;
-      while (jj + 1 < b.njobs && b.jobs[jj + 1].tile0 <= tt) ++jj;
-      items.push_back({b.jobs[jj].C, it});
-    }
-    std::stable_sort(items.begin(), items.end(),
-                     [](const std::pair<int, int> &x, const std::pair<int, int> &y) { return x.first > y.first; });
-    std::vector<long long> load(pairs, 0);
-    std::vector<std::vector<int>> lists(pairs);
-    for (const auto &ci : items) {
-      int best = 0;
-      for (int q = 1; q < pairs; ++q)
-        if (load[q] < load[best]) best = q;
-      load[best] += ci.first + 8;  // + a per-tile epilogue allowance
-      lists[best].push_back(ci.second);
-    }
-    int off = 0;
-    for (int q = 0; q < pairs; ++q) {
-      b.sched_off[q] = (uint16_t)off;
-      for (int it : lists[q]) b.sched[off++] = (uint16_t)it;
-    }
-    b.sched_off[pairs] = (uint16_t)off;
-    b.scheduled = 1;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(pairs * kGemmCluster);
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kGemmCluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, tgemm_kernel<FMT>, b) != cudaSuccess) return TB_ERR_CUDA;
-  return TB_OK;
-}
-
-static int64_t gemm_stages_of(int64_t cols) { return ceil_div(cols, kGemmBK); }
-
-}  // namespace tb
-
-using namespace tb;
-
-#ifdef TB_GEMM_TRACE_EPI
-extern "C" int tb_gemm_epi_trace_fetch(void *host, int64_t bytes) {
-  return cudaMemcpyFromSymbol(host, g_epi_trace, bytes) == cudaSuccess ? 0 : 2;
-}
-#endif
-#ifdef TB_GEMM_TRACE
-extern "C" int tb_gemm_trace_fetch(void *host, int64_t bytes) {
-  return cudaMemcpyFromSymbol(host, g_gemm_trace, bytes) == cudaSuccess ? 0 : 2;
-}
-#endif
-
-// token rows of the tiled A: one 128-row sub-tile, or whole 256-row halves
-static int64_t gemm_mpad(int64_t M) {
-  return M <= kGemmSubM ? kGemmSubM : pad_up(M, kGemmMaxMT * kGemmSubM);
-}
-
-extern "C" int64_t tb_gemm_act_bytes(int64_t M, int64_t cols) {
-  if (M < 1 || M > kGemmMaxM || cols < 1) return -1;
-  return gemm_stages_of(cols) * gemm_mpad(M) * kGemmBK + gemm_mpad(M) * (int64_t)sizeof(int32_t);
-}
-
-extern "C" int tb_gemm_tile_act(const int8_t *act, int64_t M, int64_t lda, int64_t cols,
-                                uint8_t *out, void *stream) {
-  if (!act || !out || M < 1 || M > kGemmMaxM || cols < 1 || lda < cols ||
-      (reinterpret_cast<uintptr_t>(out) & 15))
-    return TB_ERR_ARGUMENT;
-  const int Mpad = (int)gemm_mpad(M);
-  const int ks = (int)gemm_stages_of(cols);
-  const int64_t units = (int64_t)ks * Mpad * 4;
-  const int grid = (int)std::min<int64_t>(ceil_div(units, 256), (int64_t)sm_count_cached() * 8);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  gemm_tile_act_kernel<<<grid, 256, 0, s>>>(act, (int)M, lda, (int)cols, Mpad, ks, out);
-  gemm_rowsum_kernel<<<Mpad, 256, 0, s>>>(act, (int)M, lda, (int)cols, Mpad,
-                                          reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK));
-  TB_CHECK_LAUNCH();
-  return TB_OK;
 }
 
 extern "C" int tb_gemm_quantize_act(const float *x, int64_t M, int64_t cols, int64_t ldx,
@@ -900,32 +715,21 @@ extern "C" int tb_gemm_quantize_act(const float *x, int64_t M, int64_t cols, int
     return TB_ERR_ARGUMENT;
   const int Mpad = (int)gemm_mpad(M);
   const int ks = (int)gemm_stages_of(cols);
-  int S = std::min(8, ks);
-  const int kps = (int)ceil_div(ks, S);
-  S = (int)ceil_div(ks, kps);  // no empty ranks
-  const int smem = kps * kGemmKC * 8 * 16;
-  if (smem > 160 * 1024) return TB_ERR_UNSUPPORTED;  // K > 163840: tb_quantize + tb_gemm_tile_act
-  const int upl = (int)ceil_div((int64_t)kps * kGemmKC, 32);  // units per lane
-  auto kern = upl <= 1 ? gemm_quantize_act_kernel<1>
-              : upl <= 2 ? gemm_quantize_act_kernel<2>
-                         : gemm_quantize_act_kernel<0>;  // (UPL 4: 104 registers, two waves: slower)
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return TB_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  qa_absmax_kernel<<<Mpad, 512, 0, s>>>(x, (int)M, (int)cols, ldx, Mpad, ks, scale,
+                                        nonfinite_flag, out);
+  TB_CHECK_LAUNCH();
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(Mpad / 8 * S));
+  cfg.gridDim = dim3((unsigned)(Mpad / 8), (unsigned)ceil_div(ks, kQa2Stages));
   cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = static_cast<cudaStream_t>(stream);
+  cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = S;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, x, (int)M, (int)cols, ldx, Mpad, ks,
-                            kps, scale, nonfinite_flag, out) == cudaSuccess
+  return cudaLaunchKernelEx(&cfg, qa_codes_kernel, x, (int)M, (int)cols, ldx, Mpad, ks,
+                            (const double *)scale, out) == cudaSuccess
              ? TB_OK
              : TB_ERR_CUDA;
 }
