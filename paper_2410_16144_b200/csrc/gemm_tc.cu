@@ -616,6 +616,140 @@ __device__ __forceinline__ uint4 qa_codes16(const float *f, float inv_sf, double
                     prmt(t1, t3, 0x7632u));
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Tiled weights [T][C][32 rows x 16 B] as a 3-D tensor of 8-byte elements
+// {64, C, T}; a box {64, 1, 8} is one K stage of 256 rows.
+static bool encode_weight_map(CUtensorMap *map, const uint8_t *w, int C, int T) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {kTileChunkBytes / 8, (cuuint64_t)C, (cuuint64_t)T};
+  const cuuint64_t strides[2] = {kTileChunkBytes, (cuuint64_t)C * kTileChunkBytes};
+  const cuuint32_t box[3] = {kTileChunkBytes / 8, kChunksPerStage, kGemmBN / kRowTile};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint8_t *>(w), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int FMT>
+static int launch_gemm(GemmBatch &b, cudaStream_t s) {
+  const int stage = b.MT * kSubTileBytes + kPackedBytes;
+  const int smem = kGemmStages * stage + kGemmBSlots * kBTileBytes + 1024 + 1024;
+  static int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    const int max_smem =
+        kGemmStages * (kGemmMaxMT * kSubTileBytes + kPackedBytes) + kGemmBSlots * kBTileBytes + 2048;
+    if (cudaFuncSetAttribute(tgemm_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             max_smem) != cudaSuccess)
+      return TB_ERR_CUDA;
+    configured_dev = dev;
+  }
+  const int pairs = std::max(1, std::min(b.total, sm_count_cached() / kGemmCluster));
+  // Longest-processing-time-first static schedule: items (cost = K stages)
+  // go to the least-loaded pair, largest first -- a 224-stage down-projection
+  // tile no longer lands on a pair that already has two 64-stage tiles.
+  b.scheduled = 0;
+  if (b.total <= kGemmMaxSched && pairs <= kGemmMaxPairs) {
+    std::vector<std::pair<int, int>> items;  // (cost, item)
+    for (int it = 0; it < b.total; ++it) {
+      const int tt = it / b.MH;
+      int jj = 0;
+      while (jj + 1 < b.njobs && b.jobs[jj + 1].tile0 <= tt) ++jj;
+      items.push_back({b.jobs[jj].C, it});
+    }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const std::pair<int, int> &x, const std::pair<int, int> &y) { return x.first > y.first; });
+    std::vector<long long> load(pairs, 0);
+    std::vector<std::vector<int>> lists(pairs);
+    for (const auto &ci : items) {
+      int best = 0;
+      for (int q = 1; q < pairs; ++q)
+        if (load[q] < load[best]) best = q;
+      load[best] += ci.first + 8;  // + a per-tile epilogue allowance
+      lists[best].push_back(ci.second);
+    }
+    int off = 0;
+    for (int q = 0; q < pairs; ++q) {
+      b.sched_off[q] = (uint16_t)off;
+      for (int it : lists[q]) b.sched[off++] = (uint16_t)it;
+    }
+    b.sched_off[pairs] = (uint16_t)off;
+    b.scheduled = 1;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pairs * kGemmCluster);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kGemmCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, tgemm_kernel<FMT>, b) != cudaSuccess) return TB_ERR_CUDA;
+  return TB_OK;
+}
+
+static int64_t gemm_stages_of(int64_t cols) { return ceil_div(cols, kGemmBK); }
+
+}  // namespace tb
+
+using namespace tb;
+
+#ifdef TB_GEMM_TRACE_EPI
+extern "C" int tb_gemm_epi_trace_fetch(void *host, int64_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_epi_trace, bytes) == cudaSuccess ? 0 : 2;
+}
+#endif
+#ifdef TB_GEMM_TRACE
+extern "C" int tb_gemm_trace_fetch(void *host, int64_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_gemm_trace, bytes) == cudaSuccess ? 0 : 2;
+}
+#endif
+
+// token rows of the tiled A: one 128-row sub-tile, or whole 256-row halves
+static int64_t gemm_mpad(int64_t M) {
+  return M <= kGemmSubM ? kGemmSubM : pad_up(M, kGemmMaxMT * kGemmSubM);
+}
+
+extern "C" int64_t tb_gemm_act_bytes(int64_t M, int64_t cols) {
+  if (M < 1 || M > kGemmMaxM || cols < 1) return -1;
+  return gemm_stages_of(cols) * gemm_mpad(M) * kGemmBK + gemm_mpad(M) * (int64_t)sizeof(int32_t);
+}
+
+extern "C" int tb_gemm_tile_act(const int8_t *act, int64_t M, int64_t lda, int64_t cols,
+                                uint8_t *out, void *stream) {
+  if (!act || !out || M < 1 || M > kGemmMaxM || cols < 1 || lda < cols ||
+      (reinterpret_cast<uintptr_t>(out) & 15))
+    return TB_ERR_ARGUMENT;
+  const int Mpad = (int)gemm_mpad(M);
+  const int ks = (int)gemm_stages_of(cols);
+  const int64_t units = (int64_t)ks * Mpad * 4;
+  const int grid = (int)std::min<int64_t>(ceil_div(units, 256), (int64_t)sm_count_cached() * 8);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  gemm_tile_act_kernel<<<grid, 256, 0, s>>>(act, (int)M, lda, (int)cols, Mpad, ks, out);
+  gemm_rowsum_kernel<<<Mpad, 256, 0, s>>>(act, (int)M, lda, (int)cols, Mpad,
+                                          reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK));
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
 // Two launches (no clusters): (1) one CTA per
 // token row: absmax (integer max of |x| bits), the float64 scale, the
 // non-finite flag, and the row's code sum zeroed; (2) a programmatic
