@@ -209,6 +209,9 @@ int tb_gemv_batch_prepare_cols(int fmt, int64_t njobs, const tb_gemv_desc *descs
  * of the batch launched before this one (completed before this launch's
  * inputs were produced); this launch finalises it in its tail (table mode
  * only: TB_ERR_UNSUPPORTED otherwise, and the caller finalises it).       */
+/* Number of tb_gemv_batch_launch_inline calls that ran in records-table
+ * mode (introspection for tests: the fallback is silent by design).       */
+int64_t tb_gemv_table_launches(void);
 int tb_gemv_batch_launch_inline(int fmt, const void *table_device, const void *table_host,
                                 int64_t njobs, int64_t total_chunks, int32_t max_m,
                                 int64_t max_entries, int32_t finalize,

@@ -68,6 +68,7 @@ _SIGS = {
     "tb_gemm_i8": (_i32, [_i32, _p, _i64, _i64, _p, _i64, _i64, _p, _f64, _p, _p, _p, _p, _p]),
     "tb_gemm_act_bytes": (_i64, [_i64, _i64]),
     "tb_gemm_tile_act": (_i32, [_p, _i64, _i64, _i64, _p, _p]),
+    "tb_gemv_table_launches": (_i64, []),
     "tb_gemv_batch_prepare_cols": (_i32, [_i32, _i64, _p, _p, _p, _p, _p, _p, _p]),
     "tb_gemv_batch_launch_inline": (_i32, [_i32, _p, _p, _i64, _i64, _i32, _i64, _i32, _p, _i64,
                                             _p]),

@@ -27,6 +27,7 @@
 // warp that retires the tile's last chunk (acq_rel counter) applies the
 // scales (core.py:99-101), writes the outputs and resets the workspace.
 #include <algorithm>
+#include <atomic>
 
 #include "gemv_records.cuh"
 
@@ -1202,6 +1203,12 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
     for (int j = 0; j < b.in.prev_njobs; ++j) prev += (int64_t)b.in.fin[j].M * b.in.fin[j].Npad;
     want = std::max<int64_t>(want, ceil_div(prev, (int64_t)CF::kThreads * CF::kFinPer));
   }
+  if (CF::kTable && b.table == nullptr) {  // at least one CTA per table segment
+    int runs = 0;
+    for (int j = 0; j < b.njobs; ++j)
+      if (j == 0 || b.jobs[j].rec != b.jobs[j - 1].rec || b.jobs[j].c0 != b.jobs[j - 1].c0) ++runs;
+    want = std::max<int64_t>(want, runs);
+  }
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count_cached(), want));
   if (kFused && kStepCQ > 1 && grid > kStepCQ) grid -= grid % kStepCQ;  // whole CTA clusters
   const int nw = grid * CF::kWarps;
@@ -1539,6 +1546,9 @@ extern "C" int tb_gemv_batch_prepare_cols(int fmt, int64_t njobs, const tb_gemv_
   return TB_OK;
 }
 
+static std::atomic<int64_t> g_table_launches{0};
+extern "C" int64_t tb_gemv_table_launches(void) { return g_table_launches.load(); }
+
 // As tb_gemv_batch_launch, with the host copy of a small job table (<= 10
 // jobs): the jobs ride in the kernel parameters, and for 2 <= M tokens each
 // CTA keeps its segment's records (one records buffer and K-window) in one
@@ -1599,6 +1609,7 @@ extern "C" int tb_gemv_batch_launch_inline(int fmt, const void *table_device,
       st = max_m <= 2 ? launch_tgemv<TB_I2S, 2, 4>(b, s, (int)tab)
            : max_m <= 4 ? launch_tgemv<TB_I2S, 4, 4>(b, s, (int)tab)
                         : launch_tgemv<TB_I2S, 8, 4>(b, s, (int)tab);
+    if (st == TB_OK) g_table_launches.fetch_add(1, std::memory_order_relaxed);
     if (st == TB_OK || st == TB_ERR_CUDA) return st;
   }
   // too large a table or too many segments: the records path, after a

@@ -287,3 +287,51 @@ def test_small_step_after_large(tb):
     q, s = CO.quantize(xs, 4)
     want = O.make_output(CO.gemv_i2s(O.encode_i2s(vs), q, 0), 0.25, s).astype(np.float32)
     assert np.array_equal(host(small.out32[0]), want)
+
+
+@pytest.mark.parametrize("fmt,M", [("i2s", 2), ("i2s", 3), ("tl1", 5), ("i2s", 8)])
+def test_records_table_mode_windows(tb, fmt, M):
+    """The M > 1 records-table GEMV (tb_gemv_batch_launch_inline): jobs on two
+    record buffers, one matrix contracted as three ragged K-windows sharing a
+    workspace (outputs on the first), ragged rows and K, and the previous
+    batch finalised in the next launch's tail -- against the oracle."""
+    from paper_2410_16144_b200 import _lib as L
+    from paper_2410_16144_b200.stack import _windowed
+    rng = np.random.default_rng(40 + M)
+    enc = tb.encode_i2s if fmt == "i2s" else tb.encode_tl1
+    K0, K1 = 1000, 2900  # ragged: neither a multiple of 256
+    recs = [tb.ActRecords(L.I2S, M, K0), tb.ActRecords(L.I2S, M, K1)]
+    batches, truth = [], []
+    for b in range(2):
+        jobs, tr = [], []
+        for rows, src in ((70, 0), (33, 0), (300, 1)):
+            v = rng.integers(-1, 2, size=(rows, (K0, K1)[src]), dtype=np.int8)
+            p = enc(tb.TernaryMatrix(rows, v.shape[1], v, 0.5 + b))
+            if src == 1:  # three K-windows (~16 chunks each), one workspace
+                view, wj = _windowed(p, fmt, M, src, 16)
+                jobs += [(pl, recs[src], c0) for pl, _, c0 in wj]
+                tr.append((view, v, src))
+            else:
+                pl = tb.GemvPlan(p, max_tokens=M, out_dtype=torch.float32)
+                jobs.append((pl, recs[src], 0))
+                tr.append((pl, v, src))
+        batches.append(tb.GemvBatch(jobs))
+        truth.append(tr)
+    assert len(batches[0].pairs) == 5
+    xs = [torch.from_numpy(rng.standard_normal((M, k)).astype(np.float32)).cuda() for k in (K0, K1)]
+    for r, x in zip(recs, xs):
+        r.quantize(x)
+    n0 = L.load().tb_gemv_table_launches()
+    batches[0].run(finalize=False)
+    batches[1].run(finalize=False, prev=batches[0])  # finalises batch 0 in its tail
+    assert L.load().tb_gemv_table_launches() == n0 + 2  # the records-table kernel ran
+    tb.StepGlue([]).retarget(batches[1]).run()       # and batch 1
+    torch.cuda.synchronize()
+    xh = [host(x) for x in xs]
+    for b in range(2):
+        for plan, v, src in truth[b]:
+            got = host(plan.out32)
+            for t in range(M):
+                q, s, _ = O.quantize(xh[src][t], 1)
+                want = O.make_output(O.gemv_ref_int32(v, q), plan.p.scale, s).astype(np.float32)
+                assert np.array_equal(got[t], want), (fmt, M, b, v.shape, t)
