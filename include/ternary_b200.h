@@ -49,6 +49,8 @@ typedef enum tb_format { TB_I2S = 1, TB_TL1 = 2, TB_TL2 = 3 } tb_format;
 const char *tb_strerror(int status);
 int tb_abi_version(void);            /* bumps on any signature change          */
 int tb_device_sm_count(int device);  /* cached multiProcessorCount             */
+int tb_stream_synchronize(void *stream); /* cudaStreamSynchronize (host paths that
+                                            replay a graph on the caller's stream) */
 
 /* ---------------------------------------------------------------- core.py */
 
@@ -265,6 +267,22 @@ int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs, int64_t fin
                                   one 16-warp CTA per SM instead of four small ones */
 #define TB_STEP_STICKY_FLAGS 4 /* non-finite flags are only ever SET (the caller
                                   clears them): one flag can cover many steps     */
+#define TB_STEP_SELF_FINALIZE 8 /* the launch writes its OWN outputs: the warp
+                                  that completes a row tile's partial sums (a
+                                  per-tile chunk counter in the workspace)
+                                  applies the scales -- no finalize launch and
+                                  no next step needed (one-token latency path,
+                                  HostStep).  Requires table_host, no prev
+                                  table, every job finalising its own workspace,
+                                  and no other launch in flight on the same
+                                  workspaces.                                  */
+/* Copy `bytes` (a multiple of 16, 16-B aligned both sides) from mapped pinned
+ * HOST memory to device memory with one kernel of 16-byte loads (no
+ * copy-engine launch); a following TB_STEP_X_AFTER_WAIT step launch is its
+ * programmatic dependent.  The one-token latency path's input copy
+ * (HostStep); replaces the reference's host-side activation hand-off
+ * (kernels.py:189, arrays passed to the numba kernel).                     */
+int tb_copy_in(void *dst, const void *src_host, int64_t bytes, void *stream);
 typedef struct tb_step_input {
   const float *x;          /* [K] float32 (device; 16-B alignment preferred)  */
   int64_t K;

@@ -25,6 +25,7 @@ _SIGS = {
     "tb_strerror": (C.c_char_p, [_i32]),
     "tb_abi_version": (_i32, []),
     "tb_device_sm_count": (_i32, [_i32]),
+    "tb_stream_synchronize": (_i32, [_p]),
     "tb_quantize_f32": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _p]),
     "tb_quantize_f64": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _p]),
     "tb_abs_pairwise_sums_f32": (_i32, [_p, _p, _p, _i64, _p, _p, _p]),
@@ -61,6 +62,7 @@ _SIGS = {
     "tb_gemv_step_prepare_cols": (_i32, [_i32, _i64, _p, _p, _p, _i64, _p, _p, _p, _p]),
     "tb_gemv_step_launch": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _i32, _p, _i64, _p, _p, _p]),
     "tb_gemv_batch_finalize": (_i32, [_p, _i64, _i64, _p]),
+    "tb_copy_in": (_i32, [_p, _p, _i64, _p]),
     "tb_gemv_lut": (_i32, [_i32, _p, _p, _i64, _i64, _p, _i64, _p, _p]),
     "tb_gemv_ref_int32": (_i32, [_p, _i64, _i64, _p, _p, _p]),
     "tb_gemv_f32_ref": (_i32, [_p, _i64, _i64, _f32, _p, _p, _p]),

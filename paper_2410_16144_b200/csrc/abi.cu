@@ -37,3 +37,8 @@ extern "C" int tb_device_sm_count(int device) {
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
   return v;
 }
+
+extern "C" int tb_stream_synchronize(void *stream) {
+  return cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) == cudaSuccess ? TB_OK
+                                                                                 : TB_ERR_CUDA;
+}

@@ -215,6 +215,7 @@ struct StepInputs {
   int n;
   int x_after_wait;      // inputs produced by the preceding grid: read them after the wait
   int sticky_flags;      // store the non-finite flag only when set
+  int self_fin;          // the launch finalises its own outputs (per-tile counters)
   const GemvJob *prev;   // device job table finalised after this launch's own work
   int prev_njobs;
   int prev_inline;       // 1: prev jobs are in fin[] below
@@ -925,8 +926,39 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       }
     ns = 0;
   };
-  auto flush = [&](const Acc<FMT, MT> &acc, int M) {
+  // Self-finalising launch (TB_STEP_SELF_FINALIZE, one launch at a time):
+  // after publishing a tile's partial sums the warp adds the chunks it
+  // contracted to the tile's counter (ws_cnt, behind a fence: the
+  // threadfence-reduction pattern); the warp that completes the count (C
+  // chunks) reads and resets the sums and writes the tile's outputs with this
+  // launch's own scale -- the same expression as the finalize kernel.
+  auto tile_done = [&](int j, int t, int cnt) {
     if constexpr (kFused) {
+      const GemvJob J = job_at(b, j);
+      __threadfence();
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(J.ws_cnt + t, cnt) + cnt == J.C;
+      if (!__shfl_sync(0xffffffffu, last, 0)) return;
+      __threadfence();
+      const int row = t * kRowTile + lane;
+      const int32_t v = atomicExch(J.ws_acc + row, 0);
+      if (lane == 0) atomicExch(J.ws_cnt + t, 0);
+      if (row < J.N) {
+        if (J.acc_out) J.acc_out[row] = v;
+        const double y = static_cast<double>(v) * J.w_scale * s_scale[J.src];  // core.py:99-101
+        if (J.out64) J.out64[row] = y;
+        if (J.out32) J.out32[row] = static_cast<float>(y);
+      }
+    }
+  };
+  auto flush = [&](const Acc<FMT, MT> &acc, int M, int cnt) {
+    if constexpr (kFused) {
+      if (b.in.self_fin) {
+        flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
+        tile_done(cur.j, cur.t, cnt);
+        return;
+      }
       if (!waited) {
         if (ns < kStash) {
           const int32_t v = acc.total(0);
@@ -994,7 +1026,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       } else {
         for (int j = 0; j < nk; ++j) {
           if (cur.c == C) {  // next row tile (or next job)
-            flush(acc, M);
+            flush(acc, M, nch);
             nch = 0;
             acc.zero();
             cur.c = 0;
@@ -1016,7 +1048,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
         }
       }
       if (cur.c == C && k + 1 < nst) {  // tile finished exactly at a stage boundary
-        flush(acc, M);
+        flush(acc, M, nch);
         nch = 0;
         acc.zero();
         cur.c = 0;
@@ -1032,7 +1064,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       cp_async_commit();
     }
     TL_LMARK(3);
-    if (nch > 0) flush(acc, M);
+    if (nch > 0) flush(acc, M, nch);
   }
   TL_MARK(4);
   if constexpr (kTable) {
@@ -1707,6 +1739,15 @@ extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t nj
   b.in.n = (int)ninputs;
   b.in.x_after_wait = (x_after_wait & TB_STEP_X_AFTER_WAIT) ? 1 : 0;
   b.in.sticky_flags = (x_after_wait & TB_STEP_STICKY_FLAGS) ? 1 : 0;
+  b.in.self_fin = (x_after_wait & TB_STEP_SELF_FINALIZE) ? 1 : 0;
+  if (b.in.self_fin) {
+    // every job finalises its own workspace (no K-window sharing one), and
+    // nothing of a previous launch is pending on this launch's grid
+    if (!table_host || prev_njobs > 0) return TB_ERR_ARGUMENT;
+    const GemvJob *h = static_cast<const GemvJob *>(table_host);
+    for (int64_t j = 0; j < njobs; ++j)
+      if (h[j].fin_m != 1) return TB_ERR_ARGUMENT;
+  }
   const bool isolated = (x_after_wait & TB_STEP_ISOLATED) != 0;
   b.in.prev = static_cast<const GemvJob *>(prev_table_device);
   b.in.prev_njobs = (int)prev_njobs;
@@ -1745,6 +1786,56 @@ extern "C" int tb_gemv_batch_finalize(const void *table_device, int64_t njobs,
   b.njobs = (int)njobs;
   b.max_entries = (int)max_entries;
   return launch_finalize(b, static_cast<cudaStream_t>(stream));
+}
+
+// Copy-in of a step's inputs from mapped pinned HOST memory with SM loads:
+// one 16-byte load per thread, all in flight at once, so the copy costs about
+// one PCIe round trip instead of a copy-engine launch (~10 us measured for a
+// 72 KB H2D memcpy behind a busy stream).  The loads bypass the caches
+// (ld.global.cv): the host rewrites the buffer between launches.  A
+// programmatic-dependent step (TB_STEP_X_AFTER_WAIT) launches early and
+// prefetches its weights meanwhile.
+// Few, wide CTAs: an SM running one cannot host the dependent step's
+// one-CTA-per-SM grid until it exits, so the copy occupies as few SMs as
+// possible (kCopyPer loads in flight per thread).
+constexpr int kCopyThreads = 1024, kCopyPer = 4;
+__global__ void __launch_bounds__(kCopyThreads) copy_in_kernel(uint4 *__restrict__ dst,
+                                                               const uint4 *src, int64_t n) {
+  asm volatile("griddepcontrol.launch_dependents;");
+#ifdef TB_TIMELINE  // the copy's entry / exit in the timeline's last row
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_timeline[kTimelineWarps - 1][0] = globaltimer_ns();
+#endif
+  const int64_t i0 = (int64_t)blockIdx.x * kCopyThreads * kCopyPer + threadIdx.x;
+  uint4 v[kCopyPer];
+#pragma unroll
+  for (int u = 0; u < kCopyPer; ++u)
+    if (i0 + u * kCopyThreads < n) v[u] = __ldcv(src + i0 + u * kCopyThreads);
+#pragma unroll
+  for (int u = 0; u < kCopyPer; ++u)
+    if (i0 + u * kCopyThreads < n) dst[i0 + u * kCopyThreads] = v[u];
+#ifdef TB_TIMELINE
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_timeline[kTimelineWarps - 1][1] = globaltimer_ns();
+#endif
+}
+
+extern "C" int tb_copy_in(void *dst, const void *src_host, int64_t bytes, void *stream) {
+  if (!dst || !src_host || bytes < 1 || (bytes & 15) ||
+      (reinterpret_cast<uintptr_t>(dst) & 15) || (reinterpret_cast<uintptr_t>(src_host) & 15))
+    return TB_ERR_ARGUMENT;
+  const int64_t n = bytes / 16;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)ceil_div(n, (int64_t)kCopyThreads * kCopyPer));
+  cfg.blockDim = dim3(kCopyThreads);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, copy_in_kernel, static_cast<uint4 *>(dst),
+                         static_cast<const uint4 *>(src_host), n) != cudaSuccess)
+    return TB_ERR_CUDA;
+  return TB_OK;
 }
 
 extern "C" int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs,

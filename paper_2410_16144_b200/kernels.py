@@ -22,6 +22,8 @@ from __future__ import annotations
 
 import enum
 
+import numpy as np
+
 import torch
 
 from . import _lib as L
@@ -423,7 +425,8 @@ class GemvStep:
     """
 
     def __init__(self, pairs, input_k, x_after_wait: bool = False, flags=None,
-                 isolated: bool = False, sticky_flags: bool = False):
+                 isolated: bool = False, sticky_flags: bool = False,
+                 self_finalize: bool = False):
         import ctypes as C
         import numpy as np
 
@@ -482,8 +485,11 @@ class GemvStep:
         self.njobs, self.total, self.max_entries = len(pairs), total.value, maxe.value
         self.x_after_wait = bool(x_after_wait)
         # isolated: launched one at a time (e.g. HostStep), not as a chain
+        # self_finalize: the launch writes its own outputs (no finalize, no
+        # next step); one launch at a time on these workspaces
+        self.self_finalize = bool(self_finalize)
         self._launch_flags = ((1 if x_after_wait else 0) | (2 if isolated else 0)
-                              | (4 if sticky_flags else 0))
+                              | (4 if sticky_flags else 0) | (8 if self_finalize else 0))
         self.inputs = (L.StepInput * len(input_k))()
         for i, k in enumerate(self.input_k):
             self.inputs[i].K = k
@@ -520,6 +526,8 @@ class GemvStep:
             self.bind(xs)
         if prev is self:
             raise ValueError("a step cannot finalise its own previous launch")
+        if prev is not None and (self.self_finalize or prev.self_finalize):
+            raise ValueError("a self-finalising step is not chained")
         st = self._lib.tb_gemv_step_launch(
             self.fmt, self.table.data_ptr(), self.njobs, self.total, len(self.input_k),
             self._inputs_ptr, self._launch_flags,
@@ -532,6 +540,8 @@ class GemvStep:
 
     def finalize(self, stream_ptr: int | None = None):
         """Finalise this step's outputs now (e.g. after the last step)."""
+        if self.self_finalize:
+            return  # the launch wrote them
         st = self._lib.tb_gemv_batch_finalize(self.table.data_ptr(), self.njobs,
                                               self.max_entries,
                                               stream_ptr if stream_ptr is not None
@@ -550,6 +560,12 @@ class HostStep:
     outputs and the step its non-finite verdict straight into mapped pinned
     host memory (zero-copy), so a token is one captured graph -- copy, step
     kernel, finalize -- and one stream synchronisation.
+
+    The copy is a kernel of 16-byte loads from the mapped staging buffer
+    (``tb_copy_in``), the step its programmatic dependent (it prefetches
+    weights while the copy runs and reads the inputs after it), and the step
+    finalises its own outputs (``TB_STEP_SELF_FINALIZE``: the warp that
+    completes a row tile writes it), so a token is two kernels.
     """
 
     def __init__(self, pairs, input_k, out_dtype=torch.float32):
@@ -577,14 +593,17 @@ class HostStep:
                 out64=o if out_dtype == torch.float64 else None), *rest))
         self.flags_host = torch.zeros(len(input_k), dtype=torch.int32).pin_memory()
         self._flags_np = self.flags_host.numpy()  # shares the pinned buffer
-        self.step = GemvStep(host_pairs, input_k, flags=self.flags_host, isolated=True)
+        self.step = GemvStep(host_pairs, input_k, flags=self.flags_host, isolated=True,
+                             x_after_wait=True, self_finalize=True)
+        self._lib = L.load()
+        self._x_np = [h.numpy() for h in self.x_host]  # share the pinned buffer
         self._record = self._capture()
         self._stream = torch.cuda.current_stream()
 
     def _issue(self):
-        self.x_dev_all.copy_(self.x_host_all, non_blocking=True)
+        L.check(self._lib.tb_copy_in(self.x_dev_all.data_ptr(), self.x_host_all.data_ptr(),
+                                     self.x_host_all.numel() * 4, L.stream_ptr()), "copy_in")
         self.step.run(self.x_dev)
-        self.step.finalize()
 
     def _capture(self):
         s = torch.cuda.Stream()
@@ -603,12 +622,20 @@ class HostStep:
         if len(xs) != len(self.x_host):
             raise ValueError(f"expected {len(self.x_host)} input vectors")
         try:
-            for h, x in zip(self.x_host, xs):
-                h.copy_(x if isinstance(x, torch.Tensor) else torch.from_numpy(x))
-        except RuntimeError as e:
+            for h, x in zip(self._x_np, xs):
+                if isinstance(x, torch.Tensor):
+                    x = x.detach()
+                    x = x.numpy() if x.device.type == "cpu" and x.dtype != torch.bfloat16 \
+                        else x.float().cpu().numpy()
+                x = np.asarray(x).reshape(-1)
+                if x.size != h.size:
+                    raise ValueError
+                np.copyto(h, x, casting="unsafe")
+        except (RuntimeError, ValueError) as e:
             raise ValueError("dimension mismatch: input length != matrix cols") from e
+        sp = L.stream_ptr()  # replay() launches on the caller's current stream
         self._record.replay()
-        self._stream.synchronize()
+        L.check(self._lib.tb_stream_synchronize(sp), "stream_synchronize")
         if self._flags_np.any():
             raise ValueError("activations must be finite")  # core.py:116-134
         return self.out_host

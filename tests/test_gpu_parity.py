@@ -661,6 +661,44 @@ def test_host_step(tb):
         hs([bad, x1])
 
 
+def test_host_step_self_finalize(tb):
+    """HostStep = copy-in kernel + a self-finalising step (the warp completing
+    a row tile writes its outputs): every format, ragged rows, the cfg1 FFN
+    shapes, consecutive tokens (the per-tile counters reset), a non-finite
+    token in between."""
+    rng = np.random.default_rng(41)
+    enc = {"i2s": tb.encode_i2s, "tl1": tb.encode_tl1, "tl2": tb.encode_tl2}
+    cases = [("i2s", [((300, 1000), 0), ((70, 200), 1)], [1000, 200]),
+             ("tl2", [((33, 960), 0), ((257, 97), 1)], [960, 97]),
+             ("tl1", [((14336, 4096), 0), ((14336, 4096), 0), ((4096, 14336), 1)], [4096, 14336])]
+    for fmt, shapes, ks in cases:
+        e = enc[fmt]
+        vals, pairs = [], []
+        for (rows, cols), src in shapes:
+            v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+            vals.append(v)
+            pairs.append((tb.GemvPlan(e(tb.TernaryMatrix(rows, cols, v, 0.375)),
+                                      out_dtype=torch.float32), src))
+        hs = tb.HostStep(pairs, ks)
+        for tok in range(4):
+            xs = [rng.standard_normal(k).astype(np.float32) for k in ks]
+            if tok == 2:
+                bad = xs[0].copy()
+                bad[5] = np.nan
+                with pytest.raises(ValueError, match="activations must be finite"):
+                    hs([bad, xs[1]])
+            if tok == 3:  # the graph replays on the caller's current stream
+                with torch.cuda.stream(torch.cuda.Stream()):
+                    outs = hs(xs)
+            else:
+                outs = hs(xs)
+            qs = [O.quantize(x, 1) for x in xs]
+            for o, v, (_, src) in zip(outs, vals, shapes):
+                q, sc, _ = qs[src]
+                want = (O.gemv_ref_int32(v, q).astype(np.float64) * 0.375 * sc).astype(np.float32)
+                np.testing.assert_array_equal(o.numpy(), want, err_msg=f"{fmt} token {tok}")
+
+
 def test_host_pipeline(tb):
     """Independent steps streamed host -> device -> host on three streams."""
     rng = np.random.default_rng(37)

@@ -34,9 +34,13 @@ def main():
     ap.add_argument("--cols", type=int, default=4096)
     ap.add_argument("--step", action="store_true")
     ap.add_argument("--chain", type=int, default=0, help="--step: marks of the last of N chained steps")
+    ap.add_argument("--isolated", action="store_true", help="--step: HostStep's isolated launches")
+    ap.add_argument("--hoststep", action="store_true", help="HostStep's copy-in + self-finalising step")
     a = ap.parse_args()
+    if a.hoststep:
+        return hoststep_timeline()
     if a.step:
-        return step_timeline(a.chain)
+        return step_timeline(a.chain, a.isolated)
     enc = {"i2s": tb.encode_i2s, "tl1": tb.encode_tl1, "tl2": tb.encode_tl2}[a.fmt]
     g = torch.Generator(device="cuda").manual_seed(0)
     plans = []
@@ -69,8 +73,13 @@ def main():
 def report(name):
     buf = np.zeros((148 * 32, 5), dtype=np.uint64)
     lib.tb_timeline_fetch(buf.ctypes.data_as(C.c_void_p), buf.nbytes)
+    cp = buf[-1].astype(np.int64).copy()  # copy-in kernel (HostStep): entry, exit
+    buf[-1] = 0
     used = buf[:, 0] > 0
     t = buf[used].astype(np.int64)
+    if cp[0] > 0 and not os.environ.get("TL_CLOCK"):
+        t0 = t[:, 0].min()
+        print(f"  copy-in kernel: entry {(cp[0] - t0) / 1000:7.2f}  block 0 exit {(cp[1] - t0) / 1000:7.2f}")
     if os.environ.get("TL_CLOCK"):  # per-warp clock64 deltas since its own entry, in k-cycles
         rel = (t - t[:, :1]) / 1000.0
     else:
@@ -82,7 +91,7 @@ def report(name):
               f"{np.quantile(col, 0.9):7.2f} {col.max():7.2f}")
 
 
-def step_timeline(chain=0):
+def step_timeline(chain=0, isolated=False):
     H, I = 4096, 14336
     g = torch.Generator(device="cuda").manual_seed(0)
     steps = []
@@ -92,7 +101,8 @@ def step_timeline(chain=0):
             w = torch.randn(rows, cols, generator=g, device="cuda") * 0.02
             plans.append(tb.GemvPlan(tb.encode_tl1(tb.ternarize_weights(w, rows, cols))))
             del w
-        steps.append(tb.GemvStep([(plans[0], 0), (plans[1], 0), (plans[2], 1)], [H, I]))
+        steps.append(tb.GemvStep([(plans[0], 0), (plans[1], 0), (plans[2], 1)], [H, I],
+                                 isolated=isolated))
     xh = torch.randn(H, generator=g, device="cuda")
     xi = torch.randn(I, generator=g, device="cuda")
     for i in range(8):
@@ -114,9 +124,37 @@ def step_timeline(chain=0):
     for trial in range(3):
         lib.tb_timeline_clear()
         torch.cuda.synchronize()
-        steps[trial % 4].run([xh, xi], prev=steps[(trial - 1) % 4])
+        torch.cuda._sleep(200000)  # the launch is queued behind a busy GPU
+        if isolated:
+            steps[trial % 4].run([xh, xi])
+            steps[trial % 4].finalize()
+        else:
+            steps[trial % 4].run([xh, xi], prev=steps[(trial - 1) % 4])
         torch.cuda.synchronize()
         report(f"isolated step {trial}")
+
+
+def hoststep_timeline():
+    H, I = 4096, 14336
+    g = torch.Generator(device="cuda").manual_seed(0)
+    pairs = []
+    for (rows, cols), src in (((I, H), 0), ((I, H), 0), ((H, I), 1)):
+        w = torch.randn(rows, cols, generator=g, device="cuda") * 0.02
+        pairs.append((tb.GemvPlan(tb.encode_tl1(tb.ternarize_weights(w, rows, cols)),
+                                  out_dtype=torch.float32), src))
+        del w
+    hs = tb.HostStep(pairs, [H, I])
+    xs = [np.random.default_rng(0).standard_normal(k).astype(np.float32) for k in (H, I)]
+    for _ in range(3):
+        hs(xs)
+    for trial in range(3):
+        lib.tb_timeline_clear()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(hs._stream):
+            torch.cuda._sleep(200000)
+            hs._issue()
+        torch.cuda.synchronize()
+        report(f"HostStep step {trial}")
 
 
 if __name__ == "__main__":
