@@ -365,6 +365,24 @@ def make_collective(args, rank, world):
     return TP.TorchAllReduce()
 
 
+def tp_layer0_matches(torch, st, XH, XI):
+    """Layer 0 of a tensor-parallel stack (after a token pass) against the
+    same layer built whole on this GPU: this rank's rows of the column-parallel
+    projections and the full reduced rows of o/down, bit for bit."""
+    from paper_2410_16144_b200.stack import LayerStack
+    ref = LayerStack(CFG4, fmt="i2s", seed=STACK_SEED, tokens=1, layers=1)
+    ref.token_pass([XH[0]], [XI[0]])
+    torch.cuda.synchronize()
+    want, got = ref.outputs(0), st.outputs(0)
+    ok = True
+    for name, rows, cols, src, kind, lo, hi in st.plan:
+        w = want[name] if kind == "row" else want[name][lo:hi]
+        ok = ok and bool(torch.equal(got[name], w))
+    del ref
+    torch.cuda.empty_cache()
+    return ok
+
+
 def run_headline(args, rank, world):
     import torch
     import torch.distributed as dist
@@ -390,6 +408,30 @@ def run_headline(args, rank, world):
 
     run_steps(args.warmup)
     torch.cuda.synchronize()
+    tp_check = None
+    if world > 1:
+        # on-hardware parity of the sharded pass: layer 0 of this rank's stack
+        # against the same layer built unsharded (bit-identical);
+        # a peer reduction that timed out or disagrees falls back to NCCL
+        ok = tp_layer0_matches(torch, st, XH, XI) and not getattr(coll, "timed_out", lambda: 0)()
+        t = torch.tensor([int(ok)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        tp_check = {"layer": 0, "bit_identical_to_tp1": bool(t.item()),
+                    "collective": type(coll).__name__}
+        if not t.item() and type(coll).__name__ == "PeerAllReduce":
+            del st
+            torch.cuda.empty_cache()
+            from paper_2410_16144_b200 import tp as TP
+            coll = TP.TorchAllReduce()
+            st = LayerStack(CFG4, fmt="i2s", seed=STACK_SEED, tokens=1, tp_rank=rank,
+                            tp_world=world, collective=coll)
+            run_steps(args.warmup)
+            torch.cuda.synchronize()
+            t = torch.tensor([int(tp_layer0_matches(torch, st, XH, XI))], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            tp_check = {"layer": 0, "bit_identical_to_tp1": bool(t.item()),
+                        "collective": "TorchAllReduce (fallback: the peer kernel failed "
+                                      "the check)"}
     capturable = coll is None or coll.capturable
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
@@ -452,6 +494,7 @@ def run_headline(args, rank, world):
     }
     if world > 1:
         res["collective"] = type(coll).__name__
+        res["tp_check"] = tp_check
         res["roofline"]["note"] = ("per-rank bytes of its shards; the launch time includes "
                                    "the row-parallel reduction")
     graph = None

@@ -392,7 +392,10 @@ int tb_gemv_f32_ref(const int8_t *values, int64_t rows, int64_t cols,
  * shards' int32 partial accumulators exactly before the scale of
  * core.py:99-101.)  A rank's partials of every layer live in one symmetric
  * buffer (tb_sym_alloc) that every peer maps (tb_ipc_*); flags are a
- * symmetric uint32[8] per rank, ctrl a rank-local zeroed uint32[2].
+ * symmetric uint32[8] per rank, ctrl a rank-local zeroed uint32[4]
+ * {epoch, done counter, watchdog mask, spare}: a peer whose signal does not
+ * arrive within 4 s sets its bit in ctrl[2] and the launch carries on (its
+ * results are invalid; the host checks ctrl[2] and falls back).
  * tb_rowpar_allreduce: one launch per layer, a programmatic dependent of the
  * step that finalised the partials; signals this rank's epoch to every peer,
  * waits for theirs, sums layer_off + [seg.off, seg.off + seg.n) over all

@@ -37,6 +37,7 @@ namespace tb {
 constexpr int kArMaxRanks = 8;
 constexpr int kArMaxSegs = 4;
 constexpr int kArThreads = 256;
+constexpr uint64_t kArTimeoutNs = 4000000000ull;  // peer-signal watchdog: 4 s
 
 struct ArSeg {
   int64_t off, n;  // elements within the layer's partials
@@ -62,6 +63,11 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t *p) {
 }
 __device__ __forceinline__ void st_release_sys_u32(uint32_t *p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 __device__ __forceinline__ int4 ld_volatile_v4(const int32_t *p) {
   int4 v;
@@ -99,8 +105,21 @@ __global__ void __launch_bounds__(kArThreads) rowpar_allreduce_kernel(const __gr
     st_release_sys_u32(P.flags[threadIdx.x] + r, epoch);
   }
   if (threadIdx.x < P.world) {
+    // watchdog: a peer that never signals (a lost mapping, a rank that died)
+    // must not hang the GPU -- after kArTimeoutNs the wait gives up, records
+    // the peer in ctrl[2] (results of this launch are then invalid; the host
+    // reads tb_rowpar_allreduce's ctrl[2] and falls back) and carries on
     const uint32_t *f = P.flags[r] + threadIdx.x;
-    while ((int32_t)(ld_acquire_sys_u32(f) - epoch) < 0) __nanosleep(32);
+    const uint64_t t0 = globaltimer_ns();
+    // sticky: once a launch has timed out, later launches do not wait again
+    const bool dead = *reinterpret_cast<volatile uint32_t *>(ctrl + 2) != 0u;
+    while (!dead && (int32_t)(ld_acquire_sys_u32(f) - epoch) < 0) {
+      __nanosleep(32);
+      if (globaltimer_ns() - t0 > kArTimeoutNs) {
+        atomicOr(ctrl + 2, 1u << threadIdx.x);
+        break;
+      }
+    }
   }
   __syncthreads();
 

@@ -185,7 +185,7 @@ class PeerAllReduce:
             raise ValueError("the peer all-reduce supports up to 8 ranks (one NVLink domain)")
         self.rank, self.world, self.group = rank, world, group
         self.flags = sym_tensor(8, "u4")
-        self.ctrl = torch.zeros(2, dtype=torch.int32, device="cuda")
+        self.ctrl = torch.zeros(4, dtype=torch.int32, device="cuda")  # epoch, done, timeout mask
         self._opened = []
 
     def part_alloc(self, n):
@@ -250,6 +250,11 @@ class PeerAllReduce:
                                              C.cast(segs, C.c_void_p), 0, L.stream_ptr()),
                 "rowpar_allreduce")
 
+    def timed_out(self) -> int:
+        """Bit mask of peers whose signal a launch gave up waiting for (the
+        kernel's watchdog, ctrl[2]); 0 = every reduction so far completed."""
+        return int(self.ctrl[2].item())
+
     def close(self):
         from . import _lib as L
         for p in self._opened:
@@ -274,7 +279,7 @@ class EmulatedGroup:
         self.world, self.mode = world, mode
         self.stacks = [None] * world
         self.flags = [torch.zeros(8, dtype=torch.int32, device="cuda") for _ in range(world)]
-        self.ctrl = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(world)]
+        self.ctrl = [torch.zeros(4, dtype=torch.int32, device="cuda") for _ in range(world)]
 
     class _Member:
         capturable = True

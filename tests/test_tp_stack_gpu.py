@@ -148,3 +148,105 @@ def test_gloo_two_processes_share_gpu(tp1):
             else:
                 cat = np.concatenate([res[0][1][li][name], res[1][1][li][name]])
                 assert np.array_equal(cat, want[name]), (li, name)
+
+
+def test_peer_allreduce_watchdog():
+    """A peer that never signals must not hang the GPU: the kernel's wait
+    gives up after its 4 s watchdog, records the peer in ctrl[2], and later
+    launches do not wait again (the host reads the mask and falls back)."""
+    import ctypes as C
+    import time
+
+    from paper_2410_16144_b200 import _lib as L
+    from paper_2410_16144_b200 import tp as TP
+    lib = L.load()
+    n = 64
+    parts = [torch.arange(n, dtype=torch.int32, device="cuda") * (r + 1) for r in range(2)]
+    flags = [torch.zeros(8, dtype=torch.int32, device="cuda") for _ in range(2)]
+    ctrl = torch.zeros(4, dtype=torch.int32, device="cuda")
+    a_scale = torch.ones(1, dtype=torch.float64, device="cuda")
+    out = torch.zeros(n, dtype=torch.float32, device="cuda")
+    seg = (L.RowparSeg * 1)()
+    seg[0].off, seg[0].n, seg[0].w_scale = 0, n, 1.0
+    seg[0].a_scale, seg[0].out32, seg[0].acc_out = a_scale.data_ptr(), out.data_ptr(), None
+    pa = (C.c_void_p * 2)(*[p.data_ptr() for p in parts])
+    fa = (C.c_void_p * 2)(*[f.data_ptr() for f in flags])
+
+    def launch():
+        L.check(lib.tb_rowpar_allreduce(2, 0, pa, fa, ctrl.data_ptr(), 0, 1,
+                                        C.cast(seg, C.c_void_p), 0, L.stream_ptr()), "ar")
+        torch.cuda.synchronize()
+
+    t0 = time.perf_counter()
+    launch()  # rank 1 is silent: rank 0's wait on flags[0][1] times out
+    dt = time.perf_counter() - t0
+    assert 3.0 < dt < 8.0, dt
+    assert int(ctrl[2].item()) == 0b10  # the silent peer
+    t0 = time.perf_counter()
+    launch()  # sticky: no second wait
+    assert time.perf_counter() - t0 < 1.0
+    # with the peer's signal present (what rank 1's launch stores) the same
+    # launch completes at once and sums both ranks' partials
+    ctrl.zero_()
+    flags[0][1] = 1  # epoch 1 from rank 1
+    launch()
+    assert int(ctrl[2].item()) == 0 and int(ctrl[0].item()) == 1
+    assert np.array_equal(out.cpu().numpy(), (np.arange(n) * 3).astype(np.float32))
+    assert TP is not None
+
+
+def _ipc_owner(port_q, done_q):
+    import ctypes as C
+
+    from paper_2410_16144_b200 import _lib as L
+    from paper_2410_16144_b200 import tp as TP
+    torch.cuda.set_device(0)
+    lib = L.load()
+    t = TP.sym_tensor(4096, "i4")
+    t.copy_(torch.arange(4096, dtype=torch.int32, device="cuda") * 7 - 3)
+    torch.cuda.synchronize()
+    h = (C.c_uint8 * lib.tb_ipc_handle_bytes())()
+    L.check(lib.tb_ipc_get_handle(t.data_ptr(), h), "get")
+    port_q.put(bytes(h))
+    assert done_q.get(timeout=120) == "read"
+    # the reader wrote through its mapping: visible here
+    torch.cuda.synchronize()
+    port_q.put(int(t[5].item()))
+
+
+def test_cuda_ipc_handles_between_processes():
+    """tb_sym_alloc / tb_ipc_get_handle / tb_ipc_open / tb_ipc_close: a second
+    process maps the owner's buffer (what PeerAllReduce.bind does for every
+    peer) and reads / writes it.  No kernel of one process waits on the other."""
+    import ctypes as C
+
+    import torch.multiprocessing as mp
+
+    from paper_2410_16144_b200 import _lib as L
+    ctx = mp.get_context("spawn")
+    hq, dq = ctx.Queue(), ctx.Queue()
+    p = ctx.Process(target=_ipc_owner, args=(hq, dq))
+    p.start()
+    try:
+        h = hq.get(timeout=300)
+        lib = L.load()
+        torch.cuda.set_device(0)
+        torch.zeros(1, device="cuda")
+        ptr = C.c_void_p()
+        L.check(lib.tb_ipc_open((C.c_uint8 * len(h)).from_buffer_copy(h), C.byref(ptr)), "open")
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (4096,), "typestr": "<i4",
+                                        "data": (ptr.value, False), "version": 2}
+        v = torch.as_tensor(_View(), device="cuda")
+        want = np.arange(4096, dtype=np.int32) * 7 - 3
+        assert np.array_equal(v.cpu().numpy(), want)
+        v[5] = 12345
+        torch.cuda.synchronize()
+        del v
+        L.check(lib.tb_ipc_close(ptr.value), "close")
+        dq.put("read")
+        assert hq.get(timeout=120) == 12345
+    finally:
+        p.join(timeout=60)
+    assert p.exitcode == 0
