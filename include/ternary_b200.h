@@ -203,7 +203,7 @@ int tb_gemv_batch_launch(int fmt, const void *table_device, int64_t njobs,
 int tb_gemv_batch_prepare_cols(int fmt, int64_t njobs, const tb_gemv_desc *descs,
                                const int64_t *col0, const int64_t *rec_cols, void *table_host,
                                int64_t *total_chunks, int32_t *max_m, int64_t *max_entries);
-/* As tb_gemv_batch_launch, also given the host copy of a job table of <= 10
+/* As tb_gemv_batch_launch, also given the host copy of a job table of <= 20
  * jobs: the jobs ride in the kernel parameters and, for 2 <= M <= 8 tokens
  * (I2_S / TL1), every CTA keeps its segment's records in one shared-memory
  * table (no per-warp record staging); larger tables fall back to the
@@ -247,6 +247,30 @@ int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
 #define TB_GLUE_EARLY_QUANT 1
 int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs, int64_t fin_max_entries,
                     int64_t nq, const tb_quant_desc *q, int32_t flags, void *stream);
+/* Pipelined M > 1 decode layers (the reference token pass, bench.py:138-153,
+ * for 2..8 tokens per step): layer l's grouped GEMV starts streaming as soon
+ * as its activation records exist, while layer l-1's GEMV is still draining.
+ * Each layer owns a block of 4 int32 counters in device memory, zero before
+ * first use (the kernels reset them): tb_step_glue_sync quantises the layer's
+ * inputs (quantize_activations, core.py:116-134; TB_GLUE_EARLY_QUANT rules,
+ * three record sets in rotation) and counts its CTAs into sync_self; unless
+ * sync_prev is null (first layer of a pass: it waits for the whole preceding
+ * chain) it first waits for the previous layer's glue to have exited, which
+ * that glue does only after the GEMV two layers back completed.
+ * tb_gemv_batch_launch_sync is tb_gemv_batch_launch_inline in records-table
+ * mode whose table fill waits for those counts (glue_ctas as returned by the
+ * glue call) rather than for the glue's completion; it finalises the previous
+ * batch in its tail after griddepcontrol.wait.  Waits are bounded: a timeout
+ * is counted (tb_sync_timeouts, -1 on a CUDA error) instead of hanging.     */
+int tb_step_glue_sync(int64_t nq, const tb_quant_desc *q, int32_t *sync_self,
+                      int32_t *sync_prev, int32_t publish_exit, int32_t *glue_ctas,
+                      void *stream);
+int tb_gemv_batch_launch_sync(int fmt, const void *table_device, const void *table_host,
+                              int64_t njobs, int64_t total_chunks, int32_t max_m,
+                              int64_t max_entries, const void *prev_table_host,
+                              int64_t prev_njobs, int32_t *sync, int32_t glue_ctas,
+                              void *stream);
+int64_t tb_sync_timeouts(void);
 /* Fused one-token decode step in ONE launch (gemv.cu, tgemv_kernel<.,1,true>):
  * every CTA quantises the float32 input vectors itself (quantize_activations,
  * core.py:116-134, records kept in shared memory), streams the grouped GEMV

@@ -33,7 +33,7 @@
 
 namespace tb {
 
-constexpr int kMaxInlineJobs = 10;  // a layer: 6 projections on x_h + 3 K-windows of down (M > 1)
+constexpr int kMaxInlineJobs = 20;  // a layer at M = 8: 6 projections x 2 K-windows of x_h + 6 K-windows of down
 constexpr int kMaxSegs = 8;
 constexpr int kMaxStepCluster = 4;  // fused step: CTAs sharing one quantisation
 #ifndef TB_STEP_CLUSTER
@@ -122,21 +122,28 @@ struct Cfg {
 #ifndef TB_MED_RECTAB_KB
 #define TB_MED_RECTAB_KB 56
 #endif
+  // records-table CTAs: 8 warps with 3-stage rings (48 KB) and a 60 KB table,
+  // TWO per SM, so one CTA's table fill and tail (the previous layer's
+  // finalize) overlap the other's weight stream -- with the pipelined layers
+  // (tb_gemv_batch_launch_sync) the two are consecutive layers
 #ifndef TB_TABLE_WARPS
-#define TB_TABLE_WARPS 16
+#define TB_TABLE_WARPS 8
+#endif
+#ifndef TB_TABLE_MINB
+#define TB_TABLE_MINB 2
 #endif
 #ifndef TB_TABLE_RING
 #define TB_TABLE_RING 3
 #endif
 #ifndef TB_TABLE_KB
-#define TB_TABLE_KB 124
+#define TB_TABLE_KB 60
 #endif
   static constexpr int kWarps = FU == 1 ? (FMT == TB_TL2 ? TB_TL2_WARPS : TB_FUSED_WARPS)
                                 : FU == 3 ? TB_MED_WARPS
                                 : FU == 4 ? TB_TABLE_WARPS
                                           : (MT == 1 ? TB_MT1_WARPS : (MT <= 8 ? 16 : 8));
   static constexpr int kMinBlocks =
-      FU == 1 ? (FMT == TB_TL2 ? TB_TL2_MINB : TB_FUSED_MINB) : FU == 3 ? 2 : 1;
+      FU == 1 ? (FMT == TB_TL2 ? TB_TL2_MINB : TB_FUSED_MINB) : FU == 3 ? 2 : FU == 4 ? TB_TABLE_MINB : 1;
 #ifndef TB_MT1_RING
 #define TB_MT1_RING (TB_MT1_WARPS > 16 ? 3 : 4)
 #endif
@@ -220,6 +227,8 @@ struct StepInputs {
   int prev_njobs;
   int prev_inline;       // 1: prev jobs are in fin[] below
   FinJob fin[kMaxInlineFin];
+  int32_t *tab_sync;     // table mode: the layer's sync block (see LayerSync), or null
+  int tab_sync_want;     // ... and the glue's CTA count
   int16_t writer[kMaxStepInputs];  // CTA that publishes input v's scale / flag
   uint8_t need[kMaxNeedCtas];      // inputs (bit v) the CTA's jobs contract
 };
@@ -388,6 +397,12 @@ __global__ void gemv_finalize_kernel(const __grid_constant__ GemvBatch b) {
 // ---------------------------------------------------------------------------
 constexpr int kMaxGlueVecs = 4;
 
+__device__ __forceinline__ int32_t ld_acquire_gpu_fwd(const int32_t *p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 struct QuantVec {
   const void *x;
   int8_t *qnat;
@@ -403,7 +418,53 @@ struct GlueParams {
   QuantVec q[kMaxGlueVecs];
   int nq, q_tokens;
   int early;      // quantise before griddepcontrol.wait (TB_GLUE_EARLY_QUANT)
+  // pipelined layers (tb_step_glue_sync): this layer's sync block and the
+  // previous layer's (null: the first layer of a pass waits for everything)
+  int32_t *sync_self, *sync_prev;
+  int publish_exit;  // a later glue consumes this glue's exit count
 };
+
+// Pipelined M > 1 layers.  Per layer, four counters in device memory:
+//   [kSyRecs]  glue CTAs that have written their records
+//   [kSySeen]  GEMV CTAs that have seen [kSyRecs] complete (the last resets both)
+//   [kSyExit]  glue CTAs past their griddepcontrol.wait (the preceding GEMV --
+//              and, through its tail wait, everything before it -- completed)
+//   [kSyESeen] CTAs of the NEXT glue that have seen [kSyExit] complete (reset)
+// Every wait is on a grid whose CTAs are all resident (it was launched
+// before the waiter could start), so the spins cannot deadlock; they are
+// bounded anyway (kSyncSpinLimit polls), and a timeout is counted in
+// g_sync_timeouts (tb_sync_timeouts) instead of hanging the GPU.
+constexpr int kSyRecs = 0, kSySeen = 1, kSyExit = 2, kSyESeen = 3;
+constexpr int kSyncSpinLimit = 1 << 22;  // x ~100 ns: ~0.5 s
+__device__ int g_sync_timeouts;
+
+// thread 0 of the CTA waits for *cnt == want, the CTA is released by the
+// barrier; the last of `consumers` CTAs to arrive resets the pair
+__device__ __forceinline__ void sync_consume(int32_t *cnt, int32_t *seen, int want, int consumers) {
+  if (threadIdx.x == 0) {
+    int spins = 0;
+    while (ld_acquire_gpu_fwd(cnt) != want) {
+      __nanosleep(64);
+      if (++spins > kSyncSpinLimit) {
+        atomicAdd(&g_sync_timeouts, 1);
+        break;
+      }
+    }
+    if (atomicAdd(seen, 1) == consumers - 1) {
+      atomicExch(cnt, 0);
+      atomicExch(seen, 0);
+    }
+  }
+  __syncthreads();
+}
+// the CTA's writes, then one count (release: the threadfence-reduction pattern)
+__device__ __forceinline__ void sync_publish(int32_t *cnt) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(cnt, 1);
+  }
+}
 
 template <int FMT>
 __device__ __forceinline__ void glue_quant(const QuantVec &Q, int m) {
@@ -464,7 +525,7 @@ __device__ __forceinline__ void glue_finalize_flat(const GemvBatch &b, int part,
       if (jj[q] < 0) continue;
       const FinJob &J = fj[jj[q]];
       const int m = (int)(kk[q] / J.Npad), row0 = (int)(kk[q] - (int64_t)m * J.Npad);
-      const double as = (J.out64 || J.out32) ? __ldg(J.a_scale + m) : 0.0;
+      const double as = (J.out64 || J.out32) ? __ldcg(J.a_scale + m) : 0.0;
       const int32_t a[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -486,12 +547,21 @@ __global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueP
   // kernel, records that nothing in flight reads -- the caller's contract)
   // overlaps the preceding kernel; every CTA still waits for it before
   // exiting, so this grid's completion implies the predecessor's
-  if (!g.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // pipelined layers (sync_self): the first layer of a pass (no sync_prev)
+  // waits for everything before it; every other layer waits only for the
+  // previous glue's EXIT count -- that glue exits after the GEMV two layers
+  // back completed, so nothing in flight reads the record set (three in
+  // rotation) or the scales this glue writes
+  const bool piped = g.sync_self != nullptr;
+  if (!g.early || (piped && !g.sync_prev)) asm volatile("griddepcontrol.wait;" ::: "memory");
   // the next GEMV group may launch now: its prologue prefetches weights (no
   // dependence on us) and then waits for this grid before reading records
   asm volatile("griddepcontrol.launch_dependents;");
   const int y = blockIdx.y;
   if (y < g.q_tokens) {
+    const int nctas = gridDim.x * g.q_tokens;
+    if (piped && g.sync_prev)
+      sync_consume(g.sync_prev + kSyExit, g.sync_prev + kSyESeen, nctas, nctas);
     int v = 0, m = y;
     while (m >= g.q[v].M) {
       m -= g.q[v].M;
@@ -499,7 +569,9 @@ __global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueP
     }
     if (g.q[v].fmt == TB_TL2) glue_quant<TB_TL2>(g.q[v], m);
     else glue_quant<TB_I2S>(g.q[v], m);  // I2_S and TL1 share the record layout
+    if (piped) sync_publish(g.sync_self + kSyRecs);  // the GEMV's table fill waits for this
     if (g.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (piped && g.publish_exit && threadIdx.x == 0) atomicAdd(g.sync_self + kSyExit, 1);
     return;
   }
   if (g.early) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -831,7 +903,15 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     for (int k = 0; k < kRing && k < nst; ++k)
       is.issue<FMT, kIssueWeights>(b, min(kStageChunks, n - k * kStageChunks),
                                    ring + k * CF::kStageBytes, lane);
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // pipelined layers: wait for the glue's records only (its CTAs count in
+    // after writing them), not for its completion -- which would also wait
+    // for the previous layer's GEMV; that wait moves to the tail, before the
+    // previous layer is finalised
+    if (b.in.tab_sync)
+      sync_consume(b.in.tab_sync + kSyRecs, b.in.tab_sync + kSySeen, b.in.tab_sync_want,
+                   (int)gridDim.x);
+    else
+      asm volatile("griddepcontrol.wait;" ::: "memory");
     {
       int sj = 0;
       const int sc = b.seg_chunk[seg];
@@ -1072,6 +1152,10 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
     // launch waited on): every thread of the grid takes a strided share of
     // the flat (job, token, row) space, off the critical path of the next
     // launch's weight stream
+    // (pipelined layers: the glue's completion -- it exits only after the
+    // previous GEMV completed -- is awaited here; every launch of the chain
+    // waits before it exits, so completion stays transitive)
+    if (b.in.tab_sync) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (b.in.prev_inline) {
       // the jobs staged in shared memory (kernel-parameter loads with a
       // per-lane index serialise); 8 entries per thread per round, every
@@ -1112,7 +1196,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
             rw[u] = k - m * J.Npad + lane;
             int32_t *w = J.ws_acc + k + lane;
             v[u] = atomicExch(w, 0);  // read and reset (a plain store would wait for the load)
-            as[u] = J.a_scale ? __ldg(J.a_scale + m) : 0.0;
+            as[u] = J.a_scale ? __ldcg(J.a_scale + m) : 0.0;
           }
         }
 #pragma unroll
@@ -1241,7 +1325,9 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
       if (j == 0 || b.jobs[j].rec != b.jobs[j - 1].rec || b.jobs[j].c0 != b.jobs[j - 1].c0) ++runs;
     want = std::max<int64_t>(want, runs);
   }
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count_cached(), want));
+  // (table mode: kMinBlocks CTAs per SM are resident at once)
+  int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)sm_count_cached() * (CF::kTable ? CF::kMinBlocks : 1), want));
   if (kFused && kStepCQ > 1 && grid > kStepCQ) grid -= grid % kStepCQ;  // whole CTA clusters
   const int nw = grid * CF::kWarps;
   // whole ring stages per warp: with C % 4 == 0 (I2_S / TL1 at K % 256 == 0)
@@ -1585,14 +1671,47 @@ extern "C" int64_t tb_gemv_table_launches(void) { return g_table_launches.load()
 // jobs): the jobs ride in the kernel parameters, and for 2 <= M tokens each
 // CTA keeps its segment's records (one records buffer and K-window) in one
 // shared-memory table instead of staging them per warp and ring stage.
+static int batch_launch_inline(int fmt, const void *table_device, const void *table_host,
+                               int64_t njobs, int64_t total_chunks, int32_t max_m,
+                               int64_t max_entries, int32_t finalize,
+                               const void *prev_table_host, int64_t prev_njobs,
+                               int32_t *sync, int32_t glue_ctas, void *stream);
 extern "C" int tb_gemv_batch_launch_inline(int fmt, const void *table_device,
                                            const void *table_host, int64_t njobs,
                                            int64_t total_chunks, int32_t max_m,
                                            int64_t max_entries, int32_t finalize,
                                            const void *prev_table_host, int64_t prev_njobs,
                                            void *stream) {
+  return batch_launch_inline(fmt, table_device, table_host, njobs, total_chunks, max_m,
+                             max_entries, finalize, prev_table_host, prev_njobs, nullptr, 0,
+                             stream);
+}
+
+// The GEMV of a pipelined M > 1 layer: as tb_gemv_batch_launch_inline in
+// records-table mode (anything else is TB_ERR_UNSUPPORTED: no silent
+// fallback, the glue counts on its consumer), but the table fill waits for
+// the glue's records through `sync` (the layer's block, glue_ctas from
+// tb_step_glue_sync) instead of for the glue's completion, so the launch
+// streams while the previous layer's GEMV is still draining; the previous
+// batch is finalised in the tail, after griddepcontrol.wait.
+extern "C" int tb_gemv_batch_launch_sync(int fmt, const void *table_device,
+                                         const void *table_host, int64_t njobs,
+                                         int64_t total_chunks, int32_t max_m,
+                                         int64_t max_entries, const void *prev_table_host,
+                                         int64_t prev_njobs, int32_t *sync, int32_t glue_ctas,
+                                         void *stream) {
+  if (!sync || glue_ctas < 1) return TB_ERR_ARGUMENT;
+  return batch_launch_inline(fmt, table_device, table_host, njobs, total_chunks, max_m,
+                             max_entries, 0, prev_table_host, prev_njobs, sync, glue_ctas, stream);
+}
+
+static int batch_launch_inline(int fmt, const void *table_device, const void *table_host,
+                               int64_t njobs, int64_t total_chunks, int32_t max_m,
+                               int64_t max_entries, int32_t finalize,
+                               const void *prev_table_host, int64_t prev_njobs,
+                               int32_t *sync, int32_t glue_ctas, void *stream) {
   if (!table_host || njobs > kMaxInlineJobs || max_m < 2) {
-    if (prev_njobs > 0) return TB_ERR_UNSUPPORTED;  // the caller finalises the previous batch
+    if (prev_njobs > 0 || sync) return TB_ERR_UNSUPPORTED;  // the caller finalises the previous batch
     return tb_gemv_batch_launch(fmt, table_device, njobs, total_chunks, max_m, max_entries,
                                 finalize, stream);
   }
@@ -1634,6 +1753,8 @@ extern "C" int tb_gemv_batch_launch_inline(int fmt, const void *table_device,
     b.in.prev_njobs = nf;
     b.in.prev_inline = nf > 0 ? 1 : 0;
   }
+  b.in.tab_sync = sync;
+  b.in.tab_sync_want = glue_ctas;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int st = TB_ERR_UNSUPPORTED;
   if (tab <= Cfg<TB_I2S, 8, 4>::kRecTabBytes && max_m <= 8) {
@@ -1644,6 +1765,7 @@ extern "C" int tb_gemv_batch_launch_inline(int fmt, const void *table_device,
     if (st == TB_OK) g_table_launches.fetch_add(1, std::memory_order_relaxed);
     if (st == TB_OK || st == TB_ERR_CUDA) return st;
   }
+  if (sync) return TB_ERR_UNSUPPORTED;
   // too large a table or too many segments: the records path, after a
   // separate finalize launch of the previous batch
   if (prev_njobs > 0) {
@@ -1847,9 +1969,44 @@ extern "C" int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
   return tb_step_glue_ex(fin_table_device, fin_njobs, fin_max_entries, nq, q, 0, stream);
 }
 
+static int glue_launch(const void *fin_table_device, int64_t fin_njobs,
+                       int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
+                       int32_t flags, int32_t *sync_self, int32_t *sync_prev, int publish_exit,
+                       void *stream);
 extern "C" int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs,
                                int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
                                int32_t flags, void *stream) {
+  return glue_launch(fin_table_device, fin_njobs, fin_max_entries, nq, q, flags, nullptr,
+                     nullptr, 0, stream);
+}
+
+// The quantising glue of a pipelined M > 1 layer (see the sync counters above
+// glue_kernel): no finalize half; sync_self = this layer's 4-int32 block,
+// sync_prev = the previous layer's (null for the first layer of a pass, which
+// then waits for the whole preceding chain), publish_exit != 0 when the next
+// layer's glue will consume this one's exit count.  *glue_ctas = the CTA
+// count the layer's GEMV launch must be given.
+extern "C" int tb_step_glue_sync(int64_t nq, const tb_quant_desc *q, int32_t *sync_self,
+                                 int32_t *sync_prev, int32_t publish_exit, int32_t *glue_ctas,
+                                 void *stream) {
+  if (!sync_self || nq < 1 || !q) return TB_ERR_ARGUMENT;
+  int64_t tokens = 0;
+  for (int64_t v = 0; v < nq && v < kMaxGlueVecs; ++v) tokens += q[v].M;
+  if (glue_ctas) *glue_ctas = (int32_t)(8 * tokens);
+  return glue_launch(nullptr, 0, 0, nq, q, TB_GLUE_EARLY_QUANT, sync_self, sync_prev,
+                     publish_exit ? 1 : 0, stream);
+}
+
+extern "C" int64_t tb_sync_timeouts(void) {
+  int v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_sync_timeouts, sizeof(v)) != cudaSuccess) return -1;
+  return v;
+}
+
+static int glue_launch(const void *fin_table_device, int64_t fin_njobs,
+                       int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
+                       int32_t flags, int32_t *sync_self, int32_t *sync_prev, int publish_exit,
+                       void *stream) {
   if (nq < 0 || nq > kMaxGlueVecs || (nq > 0 && !q) || fin_njobs < 0 ||
       (fin_njobs > 0 && (!fin_table_device || fin_max_entries < 1 ||
                          fin_max_entries >= ((int64_t)1 << 31))))
@@ -1859,6 +2016,9 @@ extern "C" int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs,
   g.fin.njobs = (int)fin_njobs;
   g.nq = (int)nq;
   g.early = (flags & 1) ? 1 : 0;
+  g.sync_self = sync_self;
+  g.sync_prev = sync_prev;
+  g.publish_exit = publish_exit;
   int tokens = 0;
   for (int64_t v = 0; v < nq; ++v) {
     const tb_quant_desc &d = q[v];

@@ -342,11 +342,22 @@ class GemvBatch:
         self._lib = lib
 
     def run(self, stream_ptr: int | None = None, finalize: bool = True,
-            prev: "GemvBatch | None" = None):
+            prev: "GemvBatch | None" = None, sync=None):
         """One grouped GEMV launch (+ the finalize pass unless ``finalize`` is
         False, in which case a later launch must finalise this batch).
-        ``prev``: the batch launched before this one (M > 1, I2_S / TL1, <= 10
-        jobs: records-table mode), finalised in this launch's tail."""
+        ``prev``: the batch launched before this one (M > 1, I2_S / TL1, <= 20
+        jobs: records-table mode), finalised in this launch's tail.
+        ``sync``: (layer sync block pointer, glue CTA count) of a pipelined
+        layer (tb_gemv_batch_launch_sync; StepGlue(sync=...) is its producer)."""
+        if sync is not None:
+            st = self._lib.tb_gemv_batch_launch_sync(
+                self.fmt, self.table.data_ptr(), self._host_ptr, self.njobs, self.total,
+                self.max_m, self.max_entries, prev._host_ptr if prev is not None else None,
+                prev.njobs if prev is not None else 0, sync[0], sync[1],
+                stream_ptr if stream_ptr is not None else L.stream_ptr())
+            if st:
+                L.check(st, "gemv_batch_launch_sync")
+            return
         st = self._lib.tb_gemv_batch_launch_inline(self.fmt, self.table.data_ptr(),
                                                    self._host_ptr, self.njobs, self.total,
                                                    self.max_m, self.max_entries,
@@ -367,16 +378,25 @@ class StepGlue:
     they must stay allocated (e.g. a fixed buffer refilled every step).
     """
 
-    def __init__(self, inputs, finalize: "GemvBatch | None" = None, early: bool = False):
+    def __init__(self, inputs, finalize: "GemvBatch | None" = None, early: bool = False,
+                 sync=None):
         """``early``: quantise before waiting on the preceding kernel
         (TB_GLUE_EARLY_QUANT) -- only when the inputs do not depend on it and
         nothing in flight reads these records (e.g. three record sets in
-        rotation, the GEMV finalising its predecessor)."""
+        rotation, the GEMV finalising its predecessor).
+        ``sync``: (this layer's sync block pointer, the previous layer's or
+        None, publish_exit) -- the quantising glue of a pipelined layer
+        (tb_step_glue_sync); ``glue_ctas`` is then what the layer's
+        GemvBatch.run(sync=...) must be given."""
         import ctypes as C
 
         self._lib = L.load()
         self.inputs = inputs
         self._flags = 1 if early else 0
+        self._sync = sync
+        self.glue_ctas = 8 * sum(rec.M for _, rec in inputs)
+        if sync is not None and (finalize is not None or not inputs):
+            raise ValueError("a pipelined glue only quantises")
         self.fin = None
         self.descs = (L.QuantDesc * max(1, len(inputs)))()
         for d, (x, rec) in zip(self.descs, inputs):
@@ -401,6 +421,21 @@ class StepGlue:
 
     def run(self, stream_ptr: int | None = None):
         fin = self.fin
+        if self._sync is not None:
+            import ctypes as C
+
+            if fin is not None:
+                raise ValueError("a pipelined glue only quantises")
+            n = C.c_int32()
+            st = self._lib.tb_step_glue_sync(len(self.inputs), self._descs_ptr, self._sync[0],
+                                             self._sync[1], 1 if self._sync[2] else 0,
+                                             C.byref(n),
+                                             stream_ptr if stream_ptr is not None
+                                             else L.stream_ptr())
+            if st:
+                L.check(st, "step_glue_sync")
+            assert n.value == self.glue_ctas
+            return
         st = self._lib.tb_step_glue_ex(fin.table.data_ptr() if fin is not None else None,
                                        fin.njobs if fin is not None else 0,
                                        fin.max_entries if fin is not None else 0,

@@ -37,6 +37,8 @@ matrix's, as in the reference) and then sliced.
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib as L
@@ -119,9 +121,12 @@ def _slice(p, fmt: str, kind: str, lo: int, hi: int):
                      scale=p.scale, trusted=True)
 
 
-# one M-token records table per CTA (TB_TABLE_KB in csrc/gemv.cu, 124 KB):
-# the longest K-window, in record chunks, whose M-token records fit
-_TABLE_BYTES = 124 * 1024
+# one M-token records table per CTA (TB_TABLE_KB in csrc/gemv.cu, 60 KB, two
+# CTAs per SM): the longest K-window, in record chunks, whose M-token records
+# fit.  A launch takes <= _MAX_JOBS jobs in <= _MAX_SEGS runs of jobs on the
+# same (input, K-window) (kMaxInlineJobs / kMaxSegs in csrc/gemv.cu).
+_TABLE_BYTES = 60 * 1024
+_MAX_JOBS, _MAX_SEGS = 20, 8
 
 
 def window_chunks(fmt: str, tokens: int) -> int:
@@ -172,7 +177,7 @@ class LayerStack:
 
     def __init__(self, cfg: dict, fmt: str = "i2s", seed: int = 0, tokens: int = 1,
                  layers: int | None = None, device=None, tp_rank: int = 0, tp_world: int = 1,
-                 collective=None, part_alloc=None):
+                 collective=None, part_alloc=None, pipelined: bool | None = None):
         if fmt not in _ENC:
             raise ValueError(f"unknown format {fmt}")
         if tp_world > 1 and tokens != 1:
@@ -232,6 +237,8 @@ class LayerStack:
                     plan.acc = self.parts[li, off:off + rows].view(1, rows)
                 plans.append(plan)
                 jobs.append((plan, src, 0))
+            # one table segment per (input, K-window): its jobs adjacent
+            jobs.sort(key=lambda j: (j[1], j[2]))
             self.layers.append(plans)
             self.window_jobs.append(jobs)
         # algorithmic bytes of THIS rank's shards: packed bytes
@@ -251,8 +258,18 @@ class LayerStack:
             # sets -- glue l writes set l % 3 while GEMV l-1 reads set (l-1) % 3
             # and finalises with set (l-2) % 3's scales.
             self.tail_fin = fmt != "tl2" and tokens <= 8 and all(
-                len(j) <= 10 for j in self.window_jobs)
+                len(j) <= _MAX_JOBS and len({(x[1], x[2]) for x in j}) <= _MAX_SEGS
+                for j in self.window_jobs)
             self.nsets = 3 if self.tail_fin else 2
+            # pipelined layers (tb_step_glue_sync / tb_gemv_batch_launch_sync):
+            # a layer's GEMV waits for its glue's records, not for the glue's
+            # completion (= the previous GEMV's), so consecutive layers'
+            # streams overlap; 4 counters per layer, reset by the kernels
+            if pipelined is None:
+                pipelined = os.environ.get("TB_M8_PIPELINED", "1") != "0"
+            self.piped = self.tail_fin and pipelined
+            self.sync = (torch.zeros((self.nlayers, 4), dtype=torch.int32, device=dev)
+                         if self.piped else None)
             self.rec = [[ActRecords(L.TL2 if fmt == "tl2" else L.I2S, tokens, k)
                          for k in self.ks] for _ in range(self.nsets)]
             self.batches = [GemvBatch([(p, self.rec[li % self.nsets][src], c0)
@@ -294,15 +311,28 @@ class LayerStack:
             prev = None
             for li, b in enumerate(self.batches):
                 glue_pool[li].retarget(None if self.tail_fin else prev).run()
-                b.run(finalize=False, prev=prev if self.tail_fin else None)
+                b.run(finalize=False, prev=prev if self.tail_fin else None,
+                      sync=(self.sync[li].data_ptr(), glue_pool[li].glue_ctas)
+                      if self.piped else None)
                 prev = b
             self.tail.retarget(prev).run()
 
     def make_glues(self, XH, XI):
         """M > 1: one StepGlue per layer quantising rows of XH[l] / XI[l] ([M, K])."""
         n = self.nsets
+
+        def sync(li):
+            if not self.piped:
+                return None
+            return (self.sync[li].data_ptr(), self.sync[li - 1].data_ptr() if li else None,
+                    li + 1 < self.nlayers)
+
+        # (quantising before the wait is only safe behind the pipelined
+        # layers' counters: without them nothing orders the glue of layer l
+        # after the finalize of layer l-3 when the grids are small enough
+        # for several layers to be resident at once)
         return [StepGlue([(XH[li], self.rec[li % n][0]), (XI[li], self.rec[li % n][1])],
-                         early=self.tail_fin)
+                         early=self.piped, sync=sync(li))
                 for li in range(self.nlayers)]
 
     def outputs(self, li: int) -> dict:

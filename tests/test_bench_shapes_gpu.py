@@ -335,3 +335,68 @@ def test_records_table_mode_windows(tb, fmt, M):
                 q, s, _ = O.quantize(xh[src][t], 1)
                 want = O.make_output(O.gemv_ref_int32(v, q), plan.p.scale, s).astype(np.float32)
                 assert np.array_equal(got[t], want), (fmt, M, b, v.shape, t)
+
+
+@pytest.mark.parametrize("M", [2, 8])
+def test_pipelined_layers(tb, M):
+    """Pipelined M > 1 layers (tb_step_glue_sync / tb_gemv_batch_launch_sync:
+    a layer's GEMV waits for its glue's records through counters, not for the
+    previous GEMV) against the oracle and the serial chain: EVERY layer of a
+    small stack (grids of a few CTAs, so many layers are resident at once),
+    back-to-back token passes eagerly and as replays of one CUDA graph with
+    fresh inputs; the counters are back at zero and no wait timed out."""
+    from paper_2410_16144_b200 import _lib as L
+    from paper_2410_16144_b200.stack import LayerStack
+    cfg = {"hidden": 1024, "kv": 256, "inter": 3072, "layers": 6}
+    nl, h, i = 6, 1024, 3072
+    g = torch.Generator(device="cuda").manual_seed(7)
+    XH = torch.randn(nl, M, h, generator=g, device="cuda")
+    XI = torch.randn(nl, M, i, generator=g, device="cuda")
+    serial = LayerStack(cfg, seed=5, tokens=M, pipelined=False)
+    piped = LayerStack(cfg, seed=5, tokens=M, pipelined=True)
+    assert piped.piped and not serial.piped
+    sglues = serial.make_glues(XH, XI)
+    glues = piped.make_glues(XH, XI)
+
+    def oracle_check(st):
+        for li in range(nl):
+            xs = [host(XH[li]), host(XI[li])]
+            for plan, (pname, rows, cols, src) in zip(st.layers[li], st.shapes):
+                got = host(plan.out32)
+                planes = _planes(plan.p, "i2s")
+                for t in range(M):
+                    acc, sc = _c_acc("i2s", planes, xs[src][t], cols)
+                    want = O.make_output(acc, plan.p.scale, sc).astype(np.float32)
+                    assert np.array_equal(got[t], want), (M, li, pname, t)
+
+    serial.token_pass(None, None, sglues)
+    for _ in range(3):
+        piped.token_pass(None, None, glues)
+    torch.cuda.synchronize()
+    oracle_check(piped)
+    oracle_check(serial)
+    assert int(piped.sync.abs().sum().item()) == 0
+    assert L.load().tb_sync_timeouts() == 0
+    # graph replays (fresh inputs in the fixed buffers each time)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(gr, stream=s):
+            piped.token_pass(None, None, glues)
+            piped.token_pass(None, None, glues)
+    for rep in range(3):
+        XH.copy_(torch.randn(nl, M, h, generator=g, device="cuda"))
+        XI.copy_(torch.randn(nl, M, i, generator=g, device="cuda"))
+        for plans in piped.layers:
+            for pl in plans:
+                pl.out32.zero_()
+        gr.replay()
+        serial.token_pass(None, None, sglues)
+        torch.cuda.synchronize()
+        for li in range(nl):
+            for a, b in zip(serial.layers[li], piped.layers[li]):
+                assert torch.equal(a.out32, b.out32), (M, rep, li)
+        assert int(piped.sync.abs().sum().item()) == 0
+        assert L.load().tb_sync_timeouts() == 0
+    oracle_check(piped)
