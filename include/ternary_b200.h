@@ -253,17 +253,22 @@ int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs, int64_t fin
  * Each layer owns a block of 4 int32 counters in device memory, zero before
  * first use (the kernels reset them): tb_step_glue_sync quantises the layer's
  * inputs (quantize_activations, core.py:116-134; TB_GLUE_EARLY_QUANT rules,
- * three record sets in rotation) and counts its CTAs into sync_self; unless
+ * three record sets in rotation) and counts its CTAs into sync_self, then --
+ * the same CTAs, once the previous GEMV has completed -- finalises the previous
+ * layer's batch (fin_table_host: its prepared host job table, or null); unless
  * sync_prev is null (first layer of a pass: it waits for the whole preceding
  * chain) it first waits for the previous layer's glue to have exited, which
- * that glue does only after the GEMV two layers back completed.
+ * that glue does only after the GEMV two layers back completed and was
+ * finalised (prev_ctas = that call's *glue_ctas).
  * tb_gemv_batch_launch_sync is tb_gemv_batch_launch_inline in records-table
  * mode whose table fill waits for those counts (glue_ctas as returned by the
- * glue call) rather than for the glue's completion; it finalises the previous
- * batch in its tail after griddepcontrol.wait.  Waits are bounded: a timeout
+ * glue call) rather than for the glue's completion (prev_njobs = 0 when the
+ * glue finalises; otherwise the previous batch is finalised in this launch's
+ * tail, after griddepcontrol.wait).  Waits are bounded: a timeout
  * is counted (tb_sync_timeouts, -1 on a CUDA error) instead of hanging.     */
-int tb_step_glue_sync(int64_t nq, const tb_quant_desc *q, int32_t *sync_self,
-                      int32_t *sync_prev, int32_t publish_exit, int32_t *glue_ctas,
+int tb_step_glue_sync(const void *fin_table_host, int64_t fin_njobs, int64_t nq,
+                      const tb_quant_desc *q, int32_t *sync_self, int32_t *sync_prev,
+                      int32_t prev_ctas, int32_t publish_exit, int32_t *glue_ctas,
                       void *stream);
 int tb_gemv_batch_launch_sync(int fmt, const void *table_device, const void *table_host,
                               int64_t njobs, int64_t total_chunks, int32_t max_m,

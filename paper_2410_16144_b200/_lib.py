@@ -71,7 +71,7 @@ _SIGS = {
     "tb_gemm_act_bytes": (_i64, [_i64, _i64]),
     "tb_gemm_tile_act": (_i32, [_p, _i64, _i64, _i64, _p, _p]),
     "tb_gemv_table_launches": (_i64, []),
-    "tb_step_glue_sync": (_i32, [_i64, _p, _p, _p, _i32, _p, _p]),
+    "tb_step_glue_sync": (_i32, [_p, _i64, _i64, _p, _p, _p, _i32, _i32, _p, _p]),
     "tb_gemv_batch_launch_sync": (_i32, [_i32, _p, _p, _i64, _i64, _i32, _i64, _p, _i64, _p,
                                          _i32, _p]),
     "tb_sync_timeouts": (_i64, []),

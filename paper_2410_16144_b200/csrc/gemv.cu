@@ -156,6 +156,12 @@ struct Cfg {
                                : FU == 4 ? TB_TABLE_RING
                                : (MT == 1 ? TB_MT1_RING : (kFit >= 4 ? 4 : (kFit >= 2 ? kFit : 2)));
   static constexpr int kThreads = 32 * kWarps;
+  // register cap through the launch bounds (table mode: room for a glue CTA
+  // beside two table CTAs -- 2 x 256 x 96 + 256 x 64 registers = the SM's 64K)
+#ifndef TB_TABLE_BOUND_THREADS
+#define TB_TABLE_BOUND_THREADS kThreads
+#endif
+  static constexpr int kBoundThreads = FU == 4 ? TB_TABLE_BOUND_THREADS : kThreads;
   // fused step: previous-step outputs finalised per thread at the wait point
   static constexpr int kFinPer = FU == 3 ? 3 : 2;
   // fused step: records live in a CTA-wide table after the ring, not per stage
@@ -422,6 +428,11 @@ struct GlueParams {
   // previous layer's (null: the first layer of a pass waits for everything)
   int32_t *sync_self, *sync_prev;
   int publish_exit;  // a later glue consumes this glue's exit count
+  int prev_exit_ctas;  // CTAs of the previous glue (what its exit count reaches)
+  // pipelined layers: the previous layer's outputs, finalised by the
+  // quantising CTAs themselves after their wait (jobs inline: no table loads)
+  FinJob finl[kMaxInlineFin];
+  int nfinl;
 };
 
 // Pipelined M > 1 layers.  Per layer, four counters in device memory:
@@ -482,6 +493,8 @@ __device__ __forceinline__ void glue_quant(const QuantVec &Q, int m) {
 // only as many CTAs as that needs (a few hundred, not one per 256 entries).
 constexpr int kMaxGlueFin = 16;
 constexpr int kGlueIlp = 4;
+__device__ __forceinline__ void glue_finalize_units(const FinJob *fj, const int64_t *pre, int njobs,
+                                                    int part, int nparts);
 __device__ __forceinline__ void glue_finalize_flat(const GemvBatch &b, int part, int nparts) {
   __shared__ FinJob fj[kMaxGlueFin];
   __shared__ int64_t pre[kMaxGlueFin + 1];
@@ -496,6 +509,25 @@ __device__ __forceinline__ void glue_finalize_flat(const GemvBatch &b, int part,
     for (int j = 0; j < b.njobs; ++j) pre[j + 1] = pre[j] + (int64_t)fj[j].M * fj[j].Npad;
   }
   __syncthreads();
+  glue_finalize_units(fj, pre, b.njobs, part, nparts);
+}
+// ... over jobs given inline in the kernel parameters (pipelined layers)
+__device__ __forceinline__ void glue_finalize_inline(const FinJob *jobs, int njobs, int part,
+                                                     int nparts) {
+  __shared__ FinJob fj[kMaxInlineFin];
+  __shared__ int64_t pre[kMaxInlineFin + 1];
+  if ((int)threadIdx.x < njobs) fj[threadIdx.x] = jobs[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    pre[0] = 0;
+    for (int j = 0; j < njobs; ++j) pre[j + 1] = pre[j] + (int64_t)fj[j].M * fj[j].Npad;
+  }
+  __syncthreads();
+  glue_finalize_units(fj, pre, njobs, part, nparts);
+}
+__device__ __forceinline__ void glue_finalize_units(const FinJob *fj, const int64_t *pre, int njobs,
+                                                    int part, int nparts) {
+  struct { int njobs; } b{njobs};
   const int64_t units = pre[b.njobs] >> 2;
   const int64_t stride = (int64_t)nparts * blockDim.x;
   for (int64_t u0 = (int64_t)part * blockDim.x + threadIdx.x; u0 < units; u0 += stride * kGlueIlp) {
@@ -542,7 +574,10 @@ __device__ __forceinline__ void glue_finalize_flat(const GemvBatch &b, int part,
   }
 }
 
-__global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueParams g) {
+#ifndef TB_GLUE_MINB
+#define TB_GLUE_MINB 3
+#endif
+__global__ void __launch_bounds__(256, TB_GLUE_MINB) glue_kernel(const __grid_constant__ GlueParams g) {
   // early: the quantisation (inputs that do not depend on the preceding
   // kernel, records that nothing in flight reads -- the caller's contract)
   // overlaps the preceding kernel; every CTA still waits for it before
@@ -559,9 +594,9 @@ __global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueP
   asm volatile("griddepcontrol.launch_dependents;");
   const int y = blockIdx.y;
   if (y < g.q_tokens) {
-    const int nctas = gridDim.x * g.q_tokens;
     if (piped && g.sync_prev)
-      sync_consume(g.sync_prev + kSyExit, g.sync_prev + kSyESeen, nctas, nctas);
+      sync_consume(g.sync_prev + kSyExit, g.sync_prev + kSyESeen, g.prev_exit_ctas,
+                   (int)gridDim.x * g.q_tokens);
     int v = 0, m = y;
     while (m >= g.q[v].M) {
       m -= g.q[v].M;
@@ -571,7 +606,16 @@ __global__ void __launch_bounds__(256) glue_kernel(const __grid_constant__ GlueP
     else glue_quant<TB_I2S>(g.q[v], m);  // I2_S and TL1 share the record layout
     if (piped) sync_publish(g.sync_self + kSyRecs);  // the GEMV's table fill waits for this
     if (g.early) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (piped && g.publish_exit && threadIdx.x == 0) atomicAdd(g.sync_self + kSyExit, 1);
+    if (piped) {
+      // the previous GEMV has completed: its outputs, finalised by these same
+      // CTAs (already resident beside the streaming GEMV: no CTA sits waiting
+      // in an SM slot the next layer's GEMV could use), then the exit count --
+      // the glue that overwrites the scales read here waits for it
+      if (g.nfinl > 0)
+        glue_finalize_inline(g.finl, g.nfinl, y * gridDim.x + blockIdx.x,
+                             g.q_tokens * gridDim.x);
+      if (g.publish_exit) sync_publish(g.sync_self + kSyExit);
+    }
     return;
   }
   if (g.early) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -743,7 +787,7 @@ struct IssueState {
 };
 
 template <int FMT, int MT, int FU, int CQ = 1>  // CQ: cluster size of the fused step
-__global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::kMinBlocks)
+__global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kBoundThreads, Cfg<FMT, MT, FU>::kMinBlocks)
     tgemv_kernel(const __grid_constant__ GemvBatch b) {
   using F = Fmt<FMT>;
   using CF = Cfg<FMT, MT, FU>;
@@ -1092,6 +1136,18 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kThreads, Cfg<FMT, MT, FU>::
       if (nk == kStageChunks && cur.c + kStageChunks <= C) {
         // fast path: four chunks of the current row tile, fully unrolled
         const uint8_t *act = kFused ? rtab + cur.c * F::kRecBytes : slot_act;
+        if constexpr (kPairChunks<FMT, MT>) {
+          // unshifted-plane tensor-core path: chunks contracted two at a time
+#pragma unroll
+          for (int j = 0; j < kStageChunks; j += 2) {
+            const uint4 wa = load_wchunk<FMT, MT>(slot + j * kTileChunkBytes, lane);
+            const uint4 wb = load_wchunk<FMT, MT>(slot + (j + 1) * kTileChunkBytes, lane);
+            process_chunk_pair<MT>(wa, wb,
+                                   kTable ? tab_rec(cur.c + j) : act + j * F::kRecBytes,
+                                   kTable ? tab_rec(cur.c + j + 1) : act + (j + 1) * F::kRecBytes,
+                                   M, acc);
+          }
+        } else
 #pragma unroll
         for (int j = 0; j < kStageChunks; ++j) {
           const uint4 w4 = load_wchunk<FMT, MT>(slot + j * kTileChunkBytes, lane);
@@ -1325,9 +1381,16 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
       if (j == 0 || b.jobs[j].rec != b.jobs[j - 1].rec || b.jobs[j].c0 != b.jobs[j - 1].c0) ++runs;
     want = std::max<int64_t>(want, runs);
   }
-  // (table mode: kMinBlocks CTAs per SM are resident at once)
+  // (table mode: two CTAs per SM.  One per SM and launch -- the resident pair
+  // then belongs to consecutive layers, one streaming while the other fills
+  // or finalises -- moves data at the M = 1 rate (57.9 us per cfg4 layer with
+  // the MMAs compiled out) but leaves a layer only 8 warps per SM to contract
+  // with, and the ldmatrix -> LOP -> IMMA chains are latency bound: 106 us)
+#ifndef TB_TABLE_GRID_MULT
+#define TB_TABLE_GRID_MULT 2
+#endif
   int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>((int64_t)sm_count_cached() * (CF::kTable ? CF::kMinBlocks : 1), want));
+      1, std::min<int64_t>((int64_t)sm_count_cached() * (CF::kTable ? TB_TABLE_GRID_MULT : 1), want));
   if (kFused && kStepCQ > 1 && grid > kStepCQ) grid -= grid % kStepCQ;  // whole CTA clusters
   const int nw = grid * CF::kWarps;
   // whole ring stages per warp: with C % 4 == 0 (I2_S / TL1 at K % 256 == 0)
@@ -1972,29 +2035,44 @@ extern "C" int tb_step_glue(const void *fin_table_device, int64_t fin_njobs,
 static int glue_launch(const void *fin_table_device, int64_t fin_njobs,
                        int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
                        int32_t flags, int32_t *sync_self, int32_t *sync_prev, int publish_exit,
-                       void *stream);
+                       int prev_exit_ctas, const FinJob *finl, int nfinl, void *stream);
 extern "C" int tb_step_glue_ex(const void *fin_table_device, int64_t fin_njobs,
                                int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
                                int32_t flags, void *stream) {
   return glue_launch(fin_table_device, fin_njobs, fin_max_entries, nq, q, flags, nullptr,
-                     nullptr, 0, stream);
+                     nullptr, 0, 0, nullptr, 0, stream);
 }
 
-// The quantising glue of a pipelined M > 1 layer (see the sync counters above
-// glue_kernel): no finalize half; sync_self = this layer's 4-int32 block,
-// sync_prev = the previous layer's (null for the first layer of a pass, which
-// then waits for the whole preceding chain), publish_exit != 0 when the next
-// layer's glue will consume this one's exit count.  *glue_ctas = the CTA
-// count the layer's GEMV launch must be given.
-extern "C" int tb_step_glue_sync(int64_t nq, const tb_quant_desc *q, int32_t *sync_self,
-                                 int32_t *sync_prev, int32_t publish_exit, int32_t *glue_ctas,
-                                 void *stream) {
-  if (!sync_self || nq < 1 || !q) return TB_ERR_ARGUMENT;
+// The glue of a pipelined M > 1 layer (see the sync counters above
+// glue_kernel): quantises the layer's inputs and then -- the same CTAs, once
+// the previous GEMV has completed -- finalises the PREVIOUS layer's batch
+// (fin_table_host: its prepared host job table, or null).  sync_self = this
+// layer's 4-int32 block, sync_prev = the previous layer's (null for the first
+// layer of a pass, which then waits for the whole preceding chain),
+// publish_exit != 0 when the next layer's glue will consume this one's exit
+// count.  *glue_ctas = the CTA count the layer's GEMV launch (and the next
+// glue, as prev_ctas) must be given.
+extern "C" int tb_step_glue_sync(const void *fin_table_host, int64_t fin_njobs, int64_t nq,
+                                 const tb_quant_desc *q, int32_t *sync_self,
+                                 int32_t *sync_prev, int32_t prev_ctas, int32_t publish_exit,
+                                 int32_t *glue_ctas, void *stream) {
+  if (!sync_self || nq < 1 || !q || (sync_prev && prev_ctas < 1) || fin_njobs < 0 ||
+      (fin_njobs > 0 && !fin_table_host))
+    return TB_ERR_ARGUMENT;
   int64_t tokens = 0;
   for (int64_t v = 0; v < nq && v < kMaxGlueVecs; ++v) tokens += q[v].M;
   if (glue_ctas) *glue_ctas = (int32_t)(8 * tokens);
+  FinJob fin[kMaxInlineFin];
+  int nf = 0;
+  const GemvJob *ph = static_cast<const GemvJob *>(fin_table_host);
+  for (int64_t j = 0; j < fin_njobs; ++j) {
+    if (ph[j].fin_m == 0) continue;  // K-windows finalised through another job
+    if (nf == kMaxInlineFin) return TB_ERR_UNSUPPORTED;
+    fin[nf++] = FinJob{ph[j].ws_acc, ph[j].acc_out, ph[j].out64, ph[j].out32, ph[j].a_scale,
+                       ph[j].w_scale, ph[j].N, ph[j].Npad, ph[j].fin_m};
+  }
   return glue_launch(nullptr, 0, 0, nq, q, TB_GLUE_EARLY_QUANT, sync_self, sync_prev,
-                     publish_exit ? 1 : 0, stream);
+                     publish_exit ? 1 : 0, prev_ctas, fin, nf, stream);
 }
 
 extern "C" int64_t tb_sync_timeouts(void) {
@@ -2006,7 +2084,7 @@ extern "C" int64_t tb_sync_timeouts(void) {
 static int glue_launch(const void *fin_table_device, int64_t fin_njobs,
                        int64_t fin_max_entries, int64_t nq, const tb_quant_desc *q,
                        int32_t flags, int32_t *sync_self, int32_t *sync_prev, int publish_exit,
-                       void *stream) {
+                       int prev_exit_ctas, const FinJob *finl, int nfinl, void *stream) {
   if (nq < 0 || nq > kMaxGlueVecs || (nq > 0 && !q) || fin_njobs < 0 ||
       (fin_njobs > 0 && (!fin_table_device || fin_max_entries < 1 ||
                          fin_max_entries >= ((int64_t)1 << 31))))
@@ -2019,6 +2097,9 @@ static int glue_launch(const void *fin_table_device, int64_t fin_njobs,
   g.sync_self = sync_self;
   g.sync_prev = sync_prev;
   g.publish_exit = publish_exit;
+  g.prev_exit_ctas = prev_exit_ctas;
+  g.nfinl = nfinl;
+  for (int j = 0; j < nfinl; ++j) g.finl[j] = finl[j];
   int tokens = 0;
   for (int64_t v = 0; v < nq; ++v) {
     const tb_quant_desc &d = q[v];

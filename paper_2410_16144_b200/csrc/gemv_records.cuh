@@ -661,7 +661,27 @@ struct Acc<TB_I2S, MT, true> {
   static constexpr bool kPlaneCols = MT <= 2;
   // P0/P1 (twice for M = 1: even / odd chunks, shorter MMA chains) or 8-token blocks
   static constexpr int kSets = kPlaneCols ? (MT == 1 ? 4 : 2) : (MT + 7) / 8;
-  int32_t d[2][kSets][4];  // [row half h][set][fragment reg]
+  // Token columns, one 8-token block (M = 3..8): the planes stay UNSHIFTED
+  // (codes x 4^s, one LOP per A register instead of a shift and a mask) and
+  // every plane accumulates in its own fragment, folded exactly at the end;
+  // an MMA then contracts plane s of TWO consecutive chunks (its two K
+  // halves), so it is still 4 MMAs per chunk but 16 ALU ops instead of 28
+  // (ncu had the ALU pipe at 71 % with the GEMV at 0.7 of HBM).
+  // Off by default: bit-exact, but 115 registers instead of 79 (no room for a
+  // glue CTA beside two table CTAs) and no faster -- the chains are latency
+  // bound, not ALU-throughput bound (cfg4 M = 8 layer 75.2 vs 73.8 us).
+#ifndef TB_MMA_UNSHIFT
+#define TB_MMA_UNSHIFT 0
+#endif
+  static constexpr bool kUnshift = TB_MMA_UNSHIFT && !kPlaneCols && kSets == 1;
+  static constexpr int kFrags = kUnshift ? 4 : kSets;
+  int32_t d[2][kFrags][4];  // [row half h][set, or plane when kUnshift][fragment reg]
+  __device__ __forceinline__ int32_t val(int h, int nb, int r) const {
+    if constexpr (kUnshift)
+      return d[h][0][r] + (d[h][1][r] >> 2) + (d[h][2][r] >> 4) + (d[h][3][r] >> 6);
+    else
+      return d[h][nb][r];
+  }
   // Activation sums of this lane's own fragment columns only (plane columns:
   // token t/2; token columns: tokens 8nb + 2t, 8nb + 2t + 1); total() fetches
   // a token's sum from the lane that holds it.
@@ -671,7 +691,7 @@ struct Acc<TB_I2S, MT, true> {
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int q = 0; q < kSets; ++q)
+      for (int q = 0; q < kFrags; ++q)
 #pragma unroll
         for (int r = 0; r < 4; ++r) d[h][q][r] = 0;
 #pragma unroll
@@ -708,8 +728,8 @@ struct Acc<TB_I2S, MT, true> {
         if (q == 2 * nb + which) cs = csum[q];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        R[2 * h] = which ? d[h][nb][1] : d[h][nb][0];
-        R[2 * h + 1] = which ? d[h][nb][3] : d[h][nb][2];
+        R[2 * h] = which ? val(h, nb, 1) : val(h, nb, 0);
+        R[2 * h + 1] = which ? val(h, nb, 3) : val(h, nb, 2);
       }
       src = 4 * (lane & 7) + (c >> 1);
     }
@@ -758,7 +778,7 @@ struct Acc<TB_I2S, MT, true> {
             const int tok = 8 * nb + 2 * t + (r & 1);
             if (tok < M)
               red_add_s32(ws + (int64_t)tok * npad + row0 + g + 8 * (r >> 1) + 16 * h,
-                          d[h][nb][r] - csum[2 * nb + (r & 1)]);
+                          val(h, nb, r) - csum[2 * nb + (r & 1)]);
           }
     }
   }
@@ -792,6 +812,62 @@ __device__ __forceinline__ uint4 load_wchunk(const uint8_t *chunk, int lane) {
   return *reinterpret_cast<const uint4 *>(chunk + lane * 16);
 }
 
+// Whether the fast path contracts chunks in pairs (process_chunk_pair).
+#ifdef TB_I2S_MMA
+template <int FMT, int MT>
+constexpr bool kPairChunks = FMT == TB_I2S && kI2sMma<MT> && Acc<TB_I2S, MT, true>::kUnshift;
+#else
+template <int FMT, int MT>
+constexpr bool kPairChunks = false;
+#endif
+
+#ifdef TB_I2S_MMA
+// Two consecutive chunks (same row tile) on the unshifted-plane token-column
+// path: MMA s contracts plane s of chunk A (K half 0) and chunk B (K half 1);
+// the records' word s of lane t holds exactly that plane's 4 activations.
+template <int MT>
+__device__ __forceinline__ void process_chunk_pair(const uint4 wa, const uint4 wb,
+                                                   const uint8_t *__restrict__ recA,
+                                                   const uint8_t *__restrict__ recB, int M,
+                                                   Acc<TB_I2S, MT> &acc) {
+  using F = Fmt<TB_I2S>;
+  constexpr int kTokStride = kStageChunks * F::kRecBytes;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#ifdef TB_NO_COMPUTE
+  acc.csum[0] += (int32_t)(wa.x ^ wb.w);
+  return;
+#endif
+  uint4 ba = make_uint4(0u, 0u, 0u, 0u), bb = ba;
+  if (g < M) {
+    ba = *reinterpret_cast<const uint4 *>(recA + g * kTokStride + 16 * t);
+    bb = *reinterpret_cast<const uint4 *>(recB + g * kTokStride + 16 * t);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t ra = h ? wa.z : wa.x, rb = h ? wa.w : wa.y;
+    const uint32_t rc = h ? wb.z : wb.x, rd = h ? wb.w : wb.y;
+    imma_u8s8(acc.d[h][0], ra & 0x03030303u, rb & 0x03030303u, rc & 0x03030303u,
+              rd & 0x03030303u, ba.x, bb.x);
+    imma_u8s8(acc.d[h][1], ra & 0x0C0C0C0Cu, rb & 0x0C0C0C0Cu, rc & 0x0C0C0C0Cu,
+              rd & 0x0C0C0C0Cu, ba.y, bb.y);
+    imma_u8s8(acc.d[h][2], ra & 0x30303030u, rb & 0x30303030u, rc & 0x30303030u,
+              rd & 0x30303030u, ba.z, bb.z);
+    imma_u8s8(acc.d[h][3], ra & 0xC0C0C0C0u, rb & 0xC0C0C0C0u, rc & 0xC0C0C0C0u,
+              rd & 0xC0C0C0C0u, ba.w, bb.w);
+  }
+  // the two chunks' activation sums of this lane's token columns (2t, 2t + 1)
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int tok = 2 * t + q;
+    if (tok < M)
+      acc.csum[q] += *reinterpret_cast<const int32_t *>(recA + tok * kTokStride +
+                                                       (F::kActWords + ((tok >> 1) & 3)) * 4) +
+                     *reinterpret_cast<const int32_t *>(recB + tok * kTokStride +
+                                                       (F::kActWords + ((tok >> 1) & 3)) * 4);
+  }
+}
+#endif
+
 // One 16-byte chunk of this lane's row against MT activation records.
 template <int FMT, int MT>
 __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn,
@@ -821,6 +897,18 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
                   rb & 0x0C0C0C0Cu, b0, b1);
         imma_u8s8(acc.d[h][q + 1], ra & 0x30303030u, rb & 0x30303030u, ra & 0xC0C0C0C0u,
                   rb & 0xC0C0C0C0u, b0, b1);
+      }
+    } else if constexpr (A::kUnshift) {
+      // a lone chunk (tile ends, odd stage tails): the second K half is empty
+      const uint4 bq = g < M ? *reinterpret_cast<const uint4 *>(rec0 + g * kTokStride + 16 * t)
+                             : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t ra = h ? w4.z : w4.x, rb = h ? w4.w : w4.y;
+        imma_u8s8(acc.d[h][0], ra & 0x03030303u, rb & 0x03030303u, 0u, 0u, bq.x, 0u);
+        imma_u8s8(acc.d[h][1], ra & 0x0C0C0C0Cu, rb & 0x0C0C0C0Cu, 0u, 0u, bq.y, 0u);
+        imma_u8s8(acc.d[h][2], ra & 0x30303030u, rb & 0x30303030u, 0u, 0u, bq.z, 0u);
+        imma_u8s8(acc.d[h][3], ra & 0xC0C0C0C0u, rb & 0xC0C0C0C0u, 0u, 0u, bq.w, 0u);
       }
     } else {
       uint4 bq[A::kSets];

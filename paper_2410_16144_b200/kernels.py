@@ -395,8 +395,8 @@ class StepGlue:
         self._flags = 1 if early else 0
         self._sync = sync
         self.glue_ctas = 8 * sum(rec.M for _, rec in inputs)
-        if sync is not None and (finalize is not None or not inputs):
-            raise ValueError("a pipelined glue only quantises")
+        if sync is not None and not inputs:
+            raise ValueError("a pipelined glue quantises")
         self.fin = None
         self.descs = (L.QuantDesc * max(1, len(inputs)))()
         for d, (x, rec) in zip(self.descs, inputs):
@@ -419,17 +419,17 @@ class StepGlue:
         self.fin = finalize
         return self
 
-    def run(self, stream_ptr: int | None = None):
+    def run(self, stream_ptr: int | None = None, prev_ctas: int = 0):
         fin = self.fin
         if self._sync is not None:
             import ctypes as C
 
-            if fin is not None:
-                raise ValueError("a pipelined glue only quantises")
             n = C.c_int32()
-            st = self._lib.tb_step_glue_sync(len(self.inputs), self._descs_ptr, self._sync[0],
-                                             self._sync[1], 1 if self._sync[2] else 0,
-                                             C.byref(n),
+            st = self._lib.tb_step_glue_sync(fin._host_ptr if fin is not None else None,
+                                             fin.njobs if fin is not None else 0,
+                                             len(self.inputs), self._descs_ptr, self._sync[0],
+                                             self._sync[1], prev_ctas,
+                                             1 if self._sync[2] else 0, C.byref(n),
                                              stream_ptr if stream_ptr is not None
                                              else L.stream_ptr())
             if st:

@@ -125,7 +125,7 @@ def _slice(p, fmt: str, kind: str, lo: int, hi: int):
 # CTAs per SM): the longest K-window, in record chunks, whose M-token records
 # fit.  A launch takes <= _MAX_JOBS jobs in <= _MAX_SEGS runs of jobs on the
 # same (input, K-window) (kMaxInlineJobs / kMaxSegs in csrc/gemv.cu).
-_TABLE_BYTES = 60 * 1024
+_TABLE_BYTES = int(os.environ.get("TB_TABLE_KB", "60")) * 1024  # (env: profiling variants)
 _MAX_JOBS, _MAX_SEGS = 20, 8
 
 
@@ -270,6 +270,7 @@ class LayerStack:
             self.piped = self.tail_fin and pipelined
             self.sync = (torch.zeros((self.nlayers, 4), dtype=torch.int32, device=dev)
                          if self.piped else None)
+            self.glue_fin = os.environ.get("TB_M8_GLUE_FIN", "1") != "0"
             self.rec = [[ActRecords(L.TL2 if fmt == "tl2" else L.I2S, tokens, k)
                          for k in self.ks] for _ in range(self.nsets)]
             self.batches = [GemvBatch([(p, self.rec[li % self.nsets][src], c0)
@@ -309,11 +310,23 @@ class LayerStack:
             # records-table mode: layer l's launch finalises layer l-1 in its
             # tail, so the glue only quantises; otherwise the glue finalises
             prev = None
+            if self.piped:
+                # pipelined: glue l quantises layer l and then, beside the
+                # streaming GEMV l, finalises layer l-1 once its GEMV completed
+                # (glue_fin False: GEMV l finalises layer l-1 in its tail instead)
+                ex = 0
+                for li, b in enumerate(self.batches):
+                    gl = glue_pool[li].retarget(prev if self.glue_fin else None)
+                    gl.run(prev_ctas=ex)
+                    ex = gl.glue_ctas
+                    b.run(finalize=False, prev=None if self.glue_fin else prev,
+                          sync=(self.sync[li].data_ptr(), gl.glue_ctas))
+                    prev = b
+                self.tail.retarget(prev).run()
+                return
             for li, b in enumerate(self.batches):
                 glue_pool[li].retarget(None if self.tail_fin else prev).run()
-                b.run(finalize=False, prev=prev if self.tail_fin else None,
-                      sync=(self.sync[li].data_ptr(), glue_pool[li].glue_ctas)
-                      if self.piped else None)
+                b.run(finalize=False, prev=prev if self.tail_fin else None)
                 prev = b
             self.tail.retarget(prev).run()
 
