@@ -381,6 +381,17 @@ int tb_gemm_tile_act(const int8_t *act, int64_t M, int64_t lda, int64_t cols,
  * the reference's per-token quantize_activations calls (bench.py:141-142).  */
 int tb_gemm_quantize_act(const float *x, int64_t M, int64_t cols, int64_t ldx, double *scale,
                          int32_t *nonfinite_flag, uint8_t *act_tiled, void *stream);
+/* The same for up to 4 activation matrices of one token count M in ONE
+ * launch pair (a layer's hidden and intermediate inputs: the reference's
+ * two quantize_activations calls per layer, bench.py:141-142).             */
+typedef struct tb_qact_desc {
+  const float *x;          /* [M][ldx] float32                               */
+  int64_t cols, ldx;
+  double *scale;           /* [M] per-token scales out                       */
+  int32_t *nonfinite_flag; /* optional                                       */
+  uint8_t *act_tiled;      /* tb_gemm_act_bytes(M, cols) bytes, 16-B aligned */
+} tb_qact_desc;
+int tb_gemm_quantize_act_multi(int64_t n, const tb_qact_desc *d, int64_t M, void *stream);
 typedef struct tb_gemm_desc {
   const uint8_t *tiled;
   int64_t rows, cols;

@@ -79,6 +79,7 @@ _SIGS = {
     "tb_gemv_batch_launch_inline": (_i32, [_i32, _p, _p, _i64, _i64, _i32, _i64, _i32, _p, _i64,
                                             _p]),
     "tb_gemm_quantize_act": (_i32, [_p, _i64, _i64, _i64, _p, _p, _p, _p]),
+    "tb_gemm_quantize_act_multi": (_i32, [_i64, _p, _i64, _p]),
     "tb_sym_alloc": (_i32, [_i64, _p]),
     "tb_sym_free": (_i32, [_p]),
     "tb_ipc_handle_bytes": (_i32, []),
@@ -111,6 +112,13 @@ class GemmDesc(C.Structure):
     _fields_ = [("tiled", _p), ("rows", _i64), ("cols", _i64), ("act_tiled", _p),
                 ("a_scale", _p), ("w_scale", _f64), ("acc_out", _p), ("out64", _p),
                 ("out32", _p)]
+
+
+class QactDesc(C.Structure):
+    """Mirror of tb_qact_desc (include/ternary_b200.h)."""
+
+    _fields_ = [("x", _p), ("cols", _i64), ("ldx", _i64), ("scale", _p),
+                ("nonfinite_flag", _p), ("act_tiled", _p)]
 
 
 class RowparSeg(C.Structure):

@@ -258,6 +258,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
   __syncthreads();
   cluster_sync_all();
   tc_fence_after();
+  // programmatic dependent of the activation quantiser (tb_gemm_quantize_act):
+  // the TMEM allocation, barrier setup and cluster rendezvous above overlap
+  // its tail; operands, scales and outputs are touched only after this wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t tmem = tmem_slot;
   const uint32_t crank = blockIdx.x % kGemmCluster;
 
@@ -695,13 +700,15 @@ static int launch_gemm(GemmBatch &b, cudaStream_t s) {
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kGemmCluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (cudaLaunchKernelEx(&cfg, tgemm_kernel<FMT>, b) != cudaSuccess) return TB_ERR_CUDA;
   return TB_OK;
 }
@@ -730,7 +737,10 @@ static int64_t gemm_mpad(int64_t M) {
 
 extern "C" int64_t tb_gemm_act_bytes(int64_t M, int64_t cols) {
   if (M < 1 || M > kGemmMaxM || cols < 1) return -1;
-  return gemm_stages_of(cols) * gemm_mpad(M) * kGemmBK + gemm_mpad(M) * (int64_t)sizeof(int32_t);
+  // codes, per-token code sums, and (tb_gemm_quantize_act scratch) per-token
+  // reciprocal scales: float64 [Mpad] + float32 [Mpad]
+  return gemm_stages_of(cols) * gemm_mpad(M) * kGemmBK +
+         gemm_mpad(M) * (int64_t)(sizeof(int32_t) + sizeof(double) + sizeof(float));
 }
 
 extern "C" int tb_gemm_tile_act(const int8_t *act, int64_t M, int64_t lda, int64_t cols,
@@ -762,13 +772,37 @@ extern "C" int tb_gemm_tile_act(const int8_t *act, int64_t M, int64_t lda, int64
 // this one 6.0 / 12.5 us).
 constexpr int kQa2Stages = 4;  // K stages per (2) CTA
 
-__global__ void __launch_bounds__(512) qa_absmax_kernel(const float *__restrict__ x, int M, int K,
-                                                       int64_t ldx, int Mpad, int ks,
-                                                       double *__restrict__ scale, int32_t *flag,
-                                                       uint8_t *__restrict__ out) {
+// Up to kQaMaxInputs activation matrices of the same token count per launch
+// pair (a layer's x_h and x_i: two launches instead of four, and the small
+// input's CTAs run beside the large one's).
+constexpr int kQaMaxInputs = 4;
+struct QaInput {
+  const float *x;
+  double *scale;
+  int32_t *flag;
+  uint8_t *out;
+  int64_t ldx;
+  int K, ks;
+  int blk0;  // first blockIdx.y of this input in the codes launch
+};
+struct QaBatch {
+  QaInput in[kQaMaxInputs];
+  int n, M, Mpad;
+};
+
+__global__ void __launch_bounds__(512) qa_absmax_kernel(const __grid_constant__ QaBatch qb) {
+  // programmatic dependent of whatever precedes it (the previous layer's
+  // GEMM reads the scales and row sums this kernel rewrites, and x may be a
+  // preceding kernel's output): everything after the wait; the launch
+  // latency and CTA scheduling still overlap the predecessor's tail
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  const int m = blockIdx.x;
-  int32_t *rowsum = reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK);
+  const int v = blockIdx.x / qb.Mpad, m = blockIdx.x - v * qb.Mpad;
+  const QaInput &I = qb.in[v];
+  const int M = qb.M, K = I.K;
+  const float *x = I.x;
+  const int64_t ldx = I.ldx;
+  int32_t *rowsum = reinterpret_cast<int32_t *>(I.out + (int64_t)I.ks * qb.Mpad * kGemmBK);
   if (m >= M) {
     if (threadIdx.x == 0) rowsum[m] = 0;
     return;
@@ -780,9 +814,9 @@ __global__ void __launch_bounds__(512) qa_absmax_kernel(const float *__restrict_
   if (vec)
 #pragma unroll 8  // several loads in flight per thread (the max is the only dependence)
     for (; k + 3 < K; k += 512 * 4) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + k));
-      amax = max(amax, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
-                           max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
+      const uint4 v4 = __ldg(reinterpret_cast<const uint4 *>(row + k));
+      amax = max(amax, max(max(v4.x & 0x7fffffffu, v4.y & 0x7fffffffu),
+                           max(v4.z & 0x7fffffffu, v4.w & 0x7fffffffu)));
     }
   for (; k < K; k += 512 * 4)
     for (int i = 0; i < 4 && k + i < K; ++i) amax = max(amax, __float_as_uint(row[k + i]) & 0x7fffffffu);
@@ -795,19 +829,34 @@ __global__ void __launch_bounds__(512) qa_absmax_kernel(const float *__restrict_
     amax = __reduce_max_sync(0xffffffffu, amax);
     if (threadIdx.x == 0) {
       const double a = (double)__uint_as_float(amax);
-      scale[m] = a > 0.0 ? a / 127.0 : 1.0;  // core.py:128-130
-      if (amax >= 0x7f800000u && flag) atomicOr(flag, 1);
+      const double sc = a > 0.0 ? a / 127.0 : 1.0;  // core.py:128-130
+      I.scale[m] = sc;
+      // the reciprocals the codes launch multiplies by, once per token: a
+      // float64 division per LANE there (2,304 CTAs x 8 warps of them for the
+      // cfg3 layer) kept this GPU's narrow float64 pipe busy for ~20 us
+      const double inv = 1.0 / sc;
+      double *invs = reinterpret_cast<double *>(rowsum + qb.Mpad);
+      invs[m] = inv;
+      reinterpret_cast<float *>(invs + qb.Mpad)[m] = (float)inv;
+      if (amax >= 0x7f800000u && I.flag) atomicOr(I.flag, 1);
       rowsum[m] = 0;
     }
   }
 }
 
-__global__ void __launch_bounds__(256) qa_codes_kernel(const float *__restrict__ x, int M, int K,
-                                                      int64_t ldx, int Mpad, int ks,
-                                                      const double *__restrict__ scale,
-                                                      uint8_t *__restrict__ out) {
+__global__ void __launch_bounds__(256) qa_codes_kernel(const __grid_constant__ QaBatch qb) {
   __shared__ uint4 stage[kQa2Stages * kGemmKC * 8];
-  const int g = blockIdx.x, blk = blockIdx.y;
+  asm volatile("griddepcontrol.launch_dependents;");  // the GEMM: its prologue overlaps our tail
+  int v = 0;
+#pragma unroll
+  for (int q = 1; q < kQaMaxInputs; ++q)
+    if (q < qb.n && (int)blockIdx.y >= qb.in[q].blk0) v = q;
+  const QaInput &I = qb.in[v];
+  const int M = qb.M, Mpad = qb.Mpad, K = I.K, ks = I.ks;
+  const float *x = I.x;
+  const int64_t ldx = I.ldx;
+  uint8_t *out = I.out;
+  const int g = blockIdx.x, blk = blockIdx.y - I.blk0;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = g * 8 + w;
   const int ks0 = blk * kQa2Stages;
@@ -818,6 +867,7 @@ __global__ void __launch_bounds__(256) qa_codes_kernel(const float *__restrict__
   const int units = nks * kGemmKC;  // one 16-column unit per lane (32 units)
   float f[16];
   const int64_t k = k0 + (int64_t)lane * 16;
+  // (x was read by the absmax launch, which waited for its producer: safe before our wait)
   if (m < M && lane < units && k < K) {
     qa_load16(row, k, K, vec, f);
   } else {
@@ -825,10 +875,13 @@ __global__ void __launch_bounds__(256) qa_codes_kernel(const float *__restrict__
     for (int e = 0; e < 16; ++e) f[e] = 0.0f;
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the scales of (1)
-  const double sc = m < M ? scale[m] : 1.0;
-  const double inv_s = 1.0 / sc;
+  const double *invs = reinterpret_cast<const double *>(
+      reinterpret_cast<const int32_t *>(out + (int64_t)ks * Mpad * kGemmBK) + Mpad);
+  const double sc = m < M ? I.scale[m] : 1.0;
+  const double inv_s = m < M ? invs[m] : 1.0;
+  const float inv_sf = m < M ? reinterpret_cast<const float *>(invs + Mpad)[m] : 1.0f;
   int32_t sum = 0;
-  if (lane < units) stage[lane * 8 + w] = qa_codes16(f, (float)inv_s, sc, inv_s, sum);
+  if (lane < units) stage[lane * 8 + w] = qa_codes16(f, inv_sf, sc, inv_s, sum);
   sum = __reduce_add_sync(0xffffffffu, sum);
   if (lane == 0 && m < M && sum != 0)
     atomicAdd(reinterpret_cast<int32_t *>(out + (int64_t)ks * Mpad * kGemmBK) + m, sum);
@@ -841,31 +894,141 @@ __global__ void __launch_bounds__(256) qa_codes_kernel(const float *__restrict__
   }
 }
 
-extern "C" int tb_gemm_quantize_act(const float *x, int64_t M, int64_t cols, int64_t ldx,
-                                    double *scale, int32_t *nonfinite_flag, uint8_t *out,
-                                    void *stream) {
-  if (!x || !scale || !out || M < 1 || M > kGemmMaxM || cols < 1 || ldx < cols ||
-      cols > (int64_t)1 << 30 || (reinterpret_cast<uintptr_t>(out) & 15))
-    return TB_ERR_ARGUMENT;
-  const int Mpad = (int)gemm_mpad(M);
-  const int ks = (int)gemm_stages_of(cols);
+// One launch, one pass over the activations: a CTA per token row holds the
+// row in registers (up to kQaRowUnits 16-column units per thread: K <= 16,384),
+// reduces the absmax, quantises from the registers and writes its 16-byte
+// units of the operand layout and the row's code sum -- no second read, no
+// atomics, nothing to zero.  (The two-launch form read the inputs twice and
+// took 13.6 + 13.8 us for the cfg3 layer's 37.7 MB.)
+constexpr int kQaRowThreads = 512, kQaRowUnits = 2;
+__global__ void __launch_bounds__(kQaRowThreads, 2) qa_row_kernel(const __grid_constant__ QaBatch qb) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");  // the GEMM: its prologue overlaps our tail
+  const int v = blockIdx.x / qb.Mpad, m = blockIdx.x - v * qb.Mpad;
+  const QaInput &I = qb.in[v];
+  const int M = qb.M, K = I.K, ks = I.ks;
+  const int nunits = ks * kGemmKC;  // 16-column units of a (stage-padded) row
+  const float *row = I.x + (int64_t)m * I.ldx;
+  const bool vec = ((reinterpret_cast<uintptr_t>(I.x) | (uintptr_t)(I.ldx * 4)) & 15) == 0;
+  int32_t *rowsum = reinterpret_cast<int32_t *>(I.out + (int64_t)ks * qb.Mpad * kGemmBK);
+  uint4 *o4 = reinterpret_cast<uint4 *>(I.out);
+  const int G = qb.Mpad / 8, g = m >> 3, w = m & 7;
+  float f[kQaRowUnits][16];
+  uint32_t amax = 0;
+#pragma unroll
+  for (int i = 0; i < kQaRowUnits; ++i) {
+    const int u = threadIdx.x + i * kQaRowThreads;
+    if (m < M && u < nunits && (int64_t)u * 16 < K) {
+      qa_load16(row, (int64_t)u * 16, K, vec, f[i]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) f[i][e] = 0.0f;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kQaRowUnits; ++i)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) amax = max(amax, __float_as_uint(f[i][e]) & 0x7fffffffu);
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  __shared__ uint32_t red[kQaRowThreads / 32];
+  __shared__ int32_t reds[kQaRowThreads / 32];
+  __shared__ double s_sc, s_inv;
+  __shared__ float s_invf;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    amax = threadIdx.x < kQaRowThreads / 32 ? red[threadIdx.x] : 0u;
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (threadIdx.x == 0) {
+      const double a = (double)__uint_as_float(amax);
+      const double sc = a > 0.0 ? a / 127.0 : 1.0;  // core.py:128-130
+      const double inv = 1.0 / sc;
+      s_sc = sc;
+      s_inv = inv;
+      s_invf = (float)inv;
+      if (m < M) {
+        I.scale[m] = sc;
+        if (amax >= 0x7f800000u && I.flag) atomicOr(I.flag, 1);
+      }
+    }
+  }
+  __syncthreads();
+  const double sc = s_sc, inv_s = s_inv;
+  const float inv_sf = s_invf;
+  int32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < kQaRowUnits; ++i) {
+    const int u = threadIdx.x + i * kQaRowThreads;
+    if (u < nunits) {
+      const uint4 c = qa_codes16(f[i], inv_sf, sc, inv_s, sum);
+      const int ksl = u / kGemmKC, kc = u - ksl * kGemmKC;
+      o4[((int64_t)ksl * G + g) * (kGemmKC * 8) + kc * 8 + w] = c;
+    }
+  }
+  sum = __reduce_add_sync(0xffffffffu, sum);
+  if ((threadIdx.x & 31) == 0) reds[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    sum = threadIdx.x < kQaRowThreads / 32 ? reds[threadIdx.x] : 0;
+    sum = __reduce_add_sync(0xffffffffu, sum);
+    if (threadIdx.x == 0) rowsum[m] = sum;
+  }
+}
+
+extern "C" int tb_gemm_quantize_act_multi(int64_t n, const tb_qact_desc *d, int64_t M,
+                                          void *stream) {
+  if (n < 1 || n > kQaMaxInputs || !d || M < 1 || M > kGemmMaxM) return TB_ERR_ARGUMENT;
+  QaBatch qb{};
+  qb.n = (int)n;
+  qb.M = (int)M;
+  qb.Mpad = (int)gemm_mpad(M);
+  int blocks = 0;
+  for (int64_t v = 0; v < n; ++v) {
+    if (!d[v].x || !d[v].scale || !d[v].act_tiled || d[v].cols < 1 || d[v].ldx < d[v].cols ||
+        d[v].cols > (int64_t)1 << 30 || (reinterpret_cast<uintptr_t>(d[v].act_tiled) & 15))
+      return TB_ERR_ARGUMENT;
+    QaInput &I = qb.in[v];
+    I.x = d[v].x;
+    I.scale = d[v].scale;
+    I.flag = d[v].nonfinite_flag;
+    I.out = d[v].act_tiled;
+    I.ldx = d[v].ldx;
+    I.K = (int)d[v].cols;
+    I.ks = (int)gemm_stages_of(d[v].cols);
+    I.blk0 = blocks;
+    blocks += (int)ceil_div(I.ks, kQa2Stages);
+  }
+  if (blocks > 65535) return TB_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  qa_absmax_kernel<<<Mpad, 512, 0, s>>>(x, (int)M, (int)cols, ldx, Mpad, ks, scale,
-                                        nonfinite_flag, out);
-  TB_CHECK_LAUNCH();
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(Mpad / 8), (unsigned)ceil_div(ks, kQa2Stages));
-  cfg.blockDim = dim3(256);
-  cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(qb.Mpad * qb.n));
+  cfg.blockDim = dim3(512);
+  cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, qa_codes_kernel, x, (int)M, (int)cols, ldx, Mpad, ks,
-                            (const double *)scale, out) == cudaSuccess
-             ? TB_OK
-             : TB_ERR_CUDA;
+#ifndef TB_QA_TWO_LAUNCH
+  bool fits = true;  // every row register resident: the one-launch form
+  for (int v = 0; v < qb.n; ++v)
+    fits = fits && qb.in[v].ks * kGemmKC <= kQaRowThreads * kQaRowUnits;
+  if (fits) {
+    cfg.blockDim = dim3(kQaRowThreads);
+    return cudaLaunchKernelEx(&cfg, qa_row_kernel, qb) == cudaSuccess ? TB_OK : TB_ERR_CUDA;
+  }
+#endif
+  if (cudaLaunchKernelEx(&cfg, qa_absmax_kernel, qb) != cudaSuccess) return TB_ERR_CUDA;
+  cfg.gridDim = dim3((unsigned)(qb.Mpad / 8), (unsigned)blocks);
+  cfg.blockDim = dim3(256);
+  return cudaLaunchKernelEx(&cfg, qa_codes_kernel, qb) == cudaSuccess ? TB_OK : TB_ERR_CUDA;
+}
+
+extern "C" int tb_gemm_quantize_act(const float *x, int64_t M, int64_t cols, int64_t ldx,
+                                    double *scale, int32_t *nonfinite_flag, uint8_t *out,
+                                    void *stream) {
+  tb_qact_desc d{x, cols, ldx, scale, nonfinite_flag, out};
+  return tb_gemm_quantize_act_multi(1, &d, M, stream);
 }
 
 extern "C" int tb_gemm_batch(int fmt, int64_t njobs, const tb_gemm_desc *descs, int64_t M,

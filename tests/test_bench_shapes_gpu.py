@@ -107,7 +107,7 @@ def test_cfg3_fused_quantize_tile(tb):
     if not hasattr(lib, "tb_gemm_quantize_act"):
         pytest.skip("no fused quantise-tile entry point")
     rng = np.random.default_rng(3)
-    for M, K in ((512, 4096), (512, 14336), (200, 1000), (1, 64), (130, 4100)):
+    for M, K in ((512, 4096), (512, 14336), (200, 1000), (1, 64), (130, 4100), (40, 20000)):
         x = torch.from_numpy(rng.standard_normal((M, K)).astype(np.float32)).cuda()
         x[0, 5] = 0.0
         if M > 3:
@@ -122,13 +122,54 @@ def test_cfg3_fused_quantize_tile(tb):
         L.check(lib.tb_gemm_quantize_act(x.data_ptr(), M, K, K, sc.data_ptr(), flag.data_ptr(),
                                          got.data_ptr(), L.stream_ptr()), "quantize_act")
         torch.cuda.synchronize()
-        assert torch.equal(got, want), (M, K)
+        # (the buffer's tail holds the quantiser's per-token reciprocal scales:
+        # scratch that tb_gemm_tile_act does not write)
+        mpad = 128 if M <= 128 else -(-M // 256) * 256
+        n = want.numel() - 12 * mpad
+        assert torch.equal(got[:n], want[:n]), (M, K)
         assert torch.equal(sc, qa.scales) and int(flag.item()) == 0
     x[1, 2] = float("inf")
     L.check(lib.tb_gemm_quantize_act(x.data_ptr(), M, K, K, sc.data_ptr(), flag.data_ptr(),
                                      got.data_ptr(), L.stream_ptr()), "quantize_act")
     torch.cuda.synchronize()
     assert int(flag.item()) == 1
+
+
+def test_cfg3_grouped_quantize(tb):
+    """tb_gemm_quantize_act_multi (a layer's two inputs in one launch pair, the
+    bench's form) writes exactly what one call per input writes, including
+    ragged shapes and the per-input non-finite flags."""
+    from paper_2410_16144_b200 import _lib as L
+    lib = L.load()
+    rng = np.random.default_rng(8)
+    for M, Ks in ((512, (4096, 14336)), (130, (1000, 64, 4100)), (1, (64,)), (9, (300, 17000))):
+        xs = [torch.from_numpy(rng.standard_normal((M, K)).astype(np.float32)).cuda() for K in Ks]
+        xs[-1][0, 1] = float("nan")
+        want, got, scw, scg, fw, fg = [], [], [], [], [], []
+        descs = (L.QactDesc * len(Ks))()
+        for d, x, K in zip(descs, xs, Ks):
+            nb = lib.tb_gemm_act_bytes(M, K)
+            want.append(torch.full((nb,), 0xAB, dtype=torch.uint8, device="cuda"))
+            got.append(torch.full((nb,), 0xAB, dtype=torch.uint8, device="cuda"))
+            scw.append(torch.empty(M, dtype=torch.float64, device="cuda"))
+            scg.append(torch.empty(M, dtype=torch.float64, device="cuda"))
+            fw.append(torch.zeros(1, dtype=torch.int32, device="cuda"))
+            fg.append(torch.zeros(1, dtype=torch.int32, device="cuda"))
+            L.check(lib.tb_gemm_quantize_act(x.data_ptr(), M, K, K, scw[-1].data_ptr(),
+                                             fw[-1].data_ptr(), want[-1].data_ptr(),
+                                             L.stream_ptr()), "quantize_act")
+            d.x, d.cols, d.ldx = x.data_ptr(), K, K
+            d.scale, d.nonfinite_flag, d.act_tiled = (scg[-1].data_ptr(), fg[-1].data_ptr(),
+                                                      got[-1].data_ptr())
+        L.check(lib.tb_gemm_quantize_act_multi(len(Ks), C.cast(descs, C.c_void_p), M,
+                                               L.stream_ptr()), "quantize_act_multi")
+        torch.cuda.synchronize()
+        mpad = 128 if M <= 128 else -(-M // 256) * 256
+        for i in range(len(Ks)):
+            n = want[i].numel() - 12 * mpad  # (the tail is the two-launch form's scratch)
+            assert torch.equal(got[i][:n], want[i][:n]), (M, Ks[i])
+            assert torch.equal(scg[i].view(torch.int64), scw[i].view(torch.int64))
+            assert int(fg[i].item()) == int(fw[i].item()) == (1 if i == len(Ks) - 1 else 0)
 
 
 # --------------------------------------------------------------------- cfg1
