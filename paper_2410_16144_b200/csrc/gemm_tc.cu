@@ -975,6 +975,16 @@ __global__ void __launch_bounds__(kQaRowThreads, 2) qa_row_kernel(const __grid_c
   }
 }
 
+// Measured and dropped (all bit-exact): a persistent streaming form -- one CTA
+// per SM, rows arriving by bulk async copies into two shared-memory buffers
+// while the previous row is quantised, float4 reads and a 4 x 4 byte
+// transpose across lane quads -- 29 us against this kernel's 21 us for the
+// cfg3 layer (one CTA per SM exposes every block-wide phase; two
+// register-resident CTAs per SM cover each other's); the float64 reciprocal
+// taken off the row's critical path (no change: 115.6 vs 116.1 us per layer);
+// a magic-number rounding of whole units with byte-permute packing (fewer
+// instructions, but 16 more live registers under the 64-register cap: spills,
+// 123 us).  ncu: 3.46 waves of 2 CTAs per SM, issue slots 45 % busy.
 extern "C" int tb_gemm_quantize_act_multi(int64_t n, const tb_qact_desc *d, int64_t M,
                                           void *stream) {
   if (n < 1 || n > kQaMaxInputs || !d || M < 1 || M > kGemmMaxM) return TB_ERR_ARGUMENT;

@@ -1,8 +1,8 @@
-run() { echo "== $*"; env "$@" timeout 300 python bench.py --configs cfg4:m8 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "
-import sys,json
-d=json.loads(sys.stdin.read())
-c=d['configs']['cfg4:m8']; print(c['value'], c['roofline']['frac'], c['roofline']['launch_us'])"; }
-run TB_M8_GLUE_FIN=1
+#!/bin/bash
+# cfg4 M=8 layer time under library variants / environment switches:
+#   tools/build_lib_variant.sh NAME -D...; tools/m8var.sh [VAR=val ...]
+run() { echo "== $*"; env "$@" GRAPH=1 timeout 200 python tools/ncu_stack.py cfg4 i2s 8 16 2>&1 | tail -1; }
+run A=default
 run TB_M8_GLUE_FIN=0
-run TB_M8_GLUE_FIN=1
-run TB_M8_GLUE_FIN=0
+run TB_M8_PIPELINED=0
+for v in "$@"; do run $v; done
