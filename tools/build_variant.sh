@@ -5,7 +5,7 @@ set -e
 name=$1; shift
 out=/tmp/variant_$name; mkdir -p $out
 pids=()
-for f in abi quantize pack gemv gemv_aux gemm_tc; do
+for f in abi quantize pack gemv gemv_aux gemm_tc allreduce; do
   rm -f $out/$f.o
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -DTB_TIMELINE "$@" \
     -c paper_2410_16144_b200/csrc/$f.cu -o $out/$f.o &
