@@ -305,6 +305,19 @@ int64_t tb_sync_timeouts(void);
                                   table, every job finalising its own workspace,
                                   and no other launch in flight on the same
                                   workspaces.                                  */
+#define TB_STEP_INDEPENDENT 16 /* with TB_STEP_SELF_FINALIZE: the launch never
+                                  waits for the preceding kernel (no
+                                  griddepcontrol.wait at all), so independent
+                                  steps overlap freely instead of completing
+                                  in launch order -- a stream of unrelated
+                                  GEMVs (BASELINE configs[0]).  The caller
+                                  guarantees that nothing the launch touches
+                                  (inputs, workspaces, outputs, scales) is
+                                  read or written by a kernel that can still
+                                  be in flight -- e.g. reuse a step only after
+                                  >= 16 other launches of this kind (a B200
+                                  holds at most 4 of their CTAs per SM), or
+                                  after a dependent (waiting) launch.          */
 /* Copy `bytes` (a multiple of 16, 16-B aligned both sides) from mapped pinned
  * HOST memory to device memory with one kernel of 16-byte loads (no
  * copy-engine launch); a following TB_STEP_X_AFTER_WAIT step launch is its

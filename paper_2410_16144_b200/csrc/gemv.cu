@@ -229,6 +229,7 @@ struct StepInputs {
   int x_after_wait;      // inputs produced by the preceding grid: read them after the wait
   int sticky_flags;      // store the non-finite flag only when set
   int self_fin;          // the launch finalises its own outputs (per-tile counters)
+  int no_wait;           // ... and never waits for the preceding kernel (TB_STEP_INDEPENDENT)
   const GemvJob *prev;   // device job table finalised after this launch's own work
   int prev_njobs;
   int prev_inline;       // 1: prev jobs are in fin[] below
@@ -1271,7 +1272,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kBoundThreads, Cfg<FMT, MT, 
     }
   }
   if constexpr (kFused) {
-    if (!waited) {
+    if (!waited && !b.in.no_wait) {
 #ifndef TB_NO_TAILWAIT  // profiling variant (results invalid): no chain serialisation
       asm volatile("griddepcontrol.wait;" ::: "memory");
       fin_load();
@@ -1925,6 +1926,8 @@ extern "C" int tb_gemv_step_launch(int fmt, const void *table_device, int64_t nj
   b.in.x_after_wait = (x_after_wait & TB_STEP_X_AFTER_WAIT) ? 1 : 0;
   b.in.sticky_flags = (x_after_wait & TB_STEP_STICKY_FLAGS) ? 1 : 0;
   b.in.self_fin = (x_after_wait & TB_STEP_SELF_FINALIZE) ? 1 : 0;
+  b.in.no_wait = (x_after_wait & TB_STEP_INDEPENDENT) ? 1 : 0;
+  if (b.in.no_wait && (!b.in.self_fin || b.in.x_after_wait)) return TB_ERR_ARGUMENT;
   if (b.in.self_fin) {
     // every job finalises its own workspace (no K-window sharing one), and
     // nothing of a previous launch is pending on this launch's grid

@@ -461,7 +461,7 @@ class GemvStep:
 
     def __init__(self, pairs, input_k, x_after_wait: bool = False, flags=None,
                  isolated: bool = False, sticky_flags: bool = False,
-                 self_finalize: bool = False):
+                 self_finalize: bool = False, independent: bool = False):
         import ctypes as C
         import numpy as np
 
@@ -522,9 +522,16 @@ class GemvStep:
         # isolated: launched one at a time (e.g. HostStep), not as a chain
         # self_finalize: the launch writes its own outputs (no finalize, no
         # next step); one launch at a time on these workspaces
-        self.self_finalize = bool(self_finalize)
+        # independent (TB_STEP_INDEPENDENT): a self-finalising launch that never
+        # waits for the preceding kernel, for streams of unrelated GEMVs; the
+        # caller reuses a step only after >= 16 other such launches
+        if independent and x_after_wait:
+            raise ValueError("an independent step cannot read a preceding kernel's outputs")
+        self_finalize = bool(self_finalize or independent)
+        self.self_finalize = self_finalize
         self._launch_flags = ((1 if x_after_wait else 0) | (2 if isolated else 0)
-                              | (4 if sticky_flags else 0) | (8 if self_finalize else 0))
+                              | (4 if sticky_flags else 0) | (8 if self_finalize else 0)
+                              | (16 if independent else 0))
         self.inputs = (L.StepInput * len(input_k))()
         for i, k in enumerate(self.input_k):
             self.inputs[i].K = k

@@ -441,3 +441,31 @@ def test_pipelined_layers(tb, M):
         assert int(piped.sync.abs().sum().item()) == 0
         assert L.load().tb_sync_timeouts() == 0
     oracle_check(piped)
+
+
+def test_independent_steps(tb):
+    """TB_STEP_INDEPENDENT: self-finalising launches that never wait for their
+    predecessor (the cfg0 bench form), 60 launches over 20 ragged plans
+    back to back, every output against the oracle."""
+    rng = np.random.default_rng(77)
+    plans, vals, steps = [], [], []
+    for c in range(20):
+        rows, cols = 100 + 37 * c, 1024 + 64 * (c % 5)
+        v = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+        p = tb.GemvPlan(tb.encode_i2s(tb.TernaryMatrix(rows, cols, v, 0.25 + c)),
+                        out_dtype=torch.float32)
+        plans.append(p)
+        vals.append(v)
+        steps.append(tb.GemvStep([(p, 0)], [cols], independent=True))
+    xs = [[torch.from_numpy(rng.standard_normal(v.shape[1]).astype(np.float32)).cuda()
+           for v in vals] for _ in range(3)]
+    for rep in range(3):
+        for c in range(20):
+            steps[c].run([xs[rep][c]])
+        torch.cuda.synchronize()
+        for c in range(20):
+            q, sc, _ = O.quantize(host(xs[rep][c]), 1)
+            want = O.make_output(O.gemv_ref_int32(vals[c], q), 0.25 + c, sc).astype(np.float32)
+            assert np.array_equal(host(plans[c].out32[0]), want), (rep, c)
+    with pytest.raises(ValueError):
+        tb.GemvStep([(plans[0], 0)], [vals[0].shape[1]], independent=True, x_after_wait=True)
