@@ -1368,7 +1368,15 @@ static int launch_tgemv(GemvBatch &b, cudaStream_t s, int rec_tab_bytes = 0) {
 #ifndef TB_MIN_WARP_CHUNKS
 #define TB_MIN_WARP_CHUNKS 32
 #endif
-  int64_t want = ceil_div(b.total, (int64_t)CF::kWarps * TB_MIN_WARP_CHUNKS);
+  // independent launches (TB_STEP_INDEPENDENT) overlap many at a time: fewer,
+  // fatter CTAs each (4096 x 4096: 25 CTAs, 1.01 us per launch against 1.31
+  // at 50 and 1.98 at 100)
+#ifndef TB_MIN_WARP_CHUNKS_IND
+#define TB_MIN_WARP_CHUNKS_IND 64
+#endif
+  int64_t want = ceil_div(b.total, (int64_t)CF::kWarps *
+                                       (kFused && b.in.no_wait ? TB_MIN_WARP_CHUNKS_IND
+                                                               : TB_MIN_WARP_CHUNKS));
   if (kFused && b.in.prev_inline) {
     // ... but enough threads that the previous step's outputs are finalised
     // at kFinPer entries per thread, not in the serial tail loop

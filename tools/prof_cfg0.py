@@ -16,6 +16,9 @@ if os.environ.get("TB_LIB"):
 import paper_2410_16144_b200 as tb  # noqa: E402
 
 
+IND = os.environ.get("CHAINED", "0") != "1"
+
+
 def main(copies=32, steps=400):
     n = k = int(os.environ.get("N", 4096))
     g = torch.Generator(device="cuda").manual_seed(3)
@@ -23,10 +26,14 @@ def main(copies=32, steps=400):
     for _ in range(copies):
         w = torch.randn(n, k, generator=g, device="cuda") * 0.02
         plan = tb.GemvPlan(tb.encode_i2s(tb.ternarize_weights(w, n, k)), out_dtype=torch.float32)
-        objs.append(tb.GemvStep([(plan, 0)], [k]))
+        objs.append(tb.GemvStep([(plan, 0)], [k], independent=IND))
     X = torch.randn(16, k, generator=g, device="cuda")
 
     def run(cnt):
+        if IND:  # independent self-finalising launches (the bench form)
+            for i in range(cnt):
+                objs[i % copies].run([X[i % 16]])
+            return
         for i in range(cnt):
             objs[i % copies].run([X[i % 16]], prev=objs[(i - 1) % copies])
         objs[(cnt - 1) % copies].finalize()
