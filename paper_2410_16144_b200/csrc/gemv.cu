@@ -842,6 +842,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kBoundThreads, Cfg<FMT, MT, 
   const int n = b.unit * (sbase + (lw < srem ? 1 : 0)) +
                 (lw == (b.seg_cta[seg + 1] - b.seg_cta[seg]) * CF::kWarps - 1 ? b.seg_tail[seg] : 0);
   bool waited = false;
+  int tab_C = 0, tab_M = 0;  // table mode: the segment's window (chunks) and tokens
   __shared__ double s_scale[kMaxStepInputs];
   int s_badm = 0;  // fused: non-finite inputs (bit v), identical in every thread
   if constexpr (!kFused && !kTable) {
@@ -963,6 +964,8 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kBoundThreads, Cfg<FMT, MT, 
       for (int j = 1; j < b.njobs; ++j)
         if (job_at(b, j).start <= sc) sj = j;
       const GemvJob J = job_at(b, sj);
+      tab_C = J.C;
+      tab_M = J.M;
       constexpr int RU = F::kRecBytes / 16;
       const int units = J.M * J.C * RU;
       for (int u = threadIdx.x; u < units; u += CF::kThreads) {
@@ -974,6 +977,32 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kBoundThreads, Cfg<FMT, MT, 
     }
     cp_async_commit();
     cp_async_wait<0>();
+    __syncthreads();
+    {
+      // per-token prefix sums of the window's chunk activation sums (one warp
+      // per token, a warp scan per 32 chunks): P[tok][c] = sum of chunks < c
+      const int C = tab_C, M = tab_M;
+      int32_t *P = reinterpret_cast<int32_t *>(rtab_base + tab_M * ((tab_C + 3) & ~3) * F::kRecBytes);
+      for (int tok = warp; tok < M; tok += CF::kWarps) {
+        int32_t carry = 0;
+        if (lane == 0) P[tok * (C + 1)] = 0;
+        for (int c0 = 0; c0 < C; c0 += 32) {
+          const int c = c0 + lane;
+          int32_t v = 0;
+          if (c < C)
+            v = *reinterpret_cast<const int32_t *>(
+                rtab_base + (((c >> 2) * M + tok) * kStageChunks + (c & 3)) * F::kRecBytes +
+                F::kActWords * 4);
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+          }
+          if (c < C) P[tok * (C + 1) + c + 1] = carry + v;
+          carry += __shfl_sync(0xffffffffu, v, 31);
+        }
+      }
+    }
     __syncthreads();
 #pragma unroll 1
     for (int k = 1; k < kRing; ++k) cp_async_commit();  // the ring's group arithmetic
@@ -1077,7 +1106,12 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kBoundThreads, Cfg<FMT, MT, 
       }
     }
   };
-  auto flush = [&](const Acc<FMT, MT> &acc, int M, int cnt) {
+  auto flush = [&](Acc<FMT, MT> &acc, int M, int cnt) {
+    if constexpr (kTable) {  // the tile's activation sums: chunks [cur.c - cnt, cur.c) of the window
+      const int32_t *P = reinterpret_cast<const int32_t *>(
+          rtab_base + tab_M * ((tab_C + 3) & ~3) * F::kRecBytes);
+      set_csum_from_prefix<FMT, MT>(acc, P, tab_C + 1, cur.c - cnt, cur.c, M);
+    }
     if constexpr (kFused) {
       if (b.in.self_fin) {
         flush_tile<FMT, MT>(b, cur.j, cur.t, acc, M, lane);
@@ -1143,7 +1177,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kBoundThreads, Cfg<FMT, MT, 
           for (int j = 0; j < kStageChunks; j += 2) {
             const uint4 wa = load_wchunk<FMT, MT>(slot + j * kTileChunkBytes, lane);
             const uint4 wb = load_wchunk<FMT, MT>(slot + (j + 1) * kTileChunkBytes, lane);
-            process_chunk_pair<MT>(wa, wb,
+            process_chunk_pair<MT, kTable>(wa, wb,
                                    kTable ? tab_rec(cur.c + j) : act + j * F::kRecBytes,
                                    kTable ? tab_rec(cur.c + j + 1) : act + (j + 1) * F::kRecBytes,
                                    M, acc);
@@ -1155,7 +1189,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kBoundThreads, Cfg<FMT, MT, 
           uint32_t sg = 0;
           if (FMT == TB_TL2)
             sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
-          process_chunk<FMT, MT>(w4, sg, kTable ? tab_rec(cur.c + j) : act + j * F::kRecBytes, M,
+          process_chunk<FMT, MT, kTable>(w4, sg, kTable ? tab_rec(cur.c + j) : act + j * F::kRecBytes, M,
                                  acc, j);
         }
         nch += kStageChunks;
@@ -1179,7 +1213,7 @@ __global__ void __launch_bounds__(Cfg<FMT, MT, FU>::kBoundThreads, Cfg<FMT, MT, 
             sg = *reinterpret_cast<const uint32_t *>(slot_sign + j * kTileSignBytes + lane * 4);
           const uint8_t *act = kTable ? tab_rec(cur.c)
                                : kFused ? rtab + cur.c * F::kRecBytes : slot_act + j * F::kRecBytes;
-          process_chunk<FMT, MT>(w4, sg, act, M, acc);
+          process_chunk<FMT, MT, kTable>(w4, sg, act, M, acc);
           ++nch;
           ++cur.c;
         }
@@ -1797,7 +1831,9 @@ static int batch_launch_inline(int fmt, const void *table_device, const void *ta
   int64_t tab = 0;
   for (int j = 0; j < njobs; ++j) {
     b.jobs[j] = h[j];
-    tab = std::max<int64_t>(tab, (int64_t)h[j].M * pad_up(h[j].C, kStageChunks) * rec_bytes_of(fmt));
+    // the segment's records + its per-token prefix sums of the chunk sums
+    tab = std::max<int64_t>(tab, (int64_t)h[j].M * pad_up(h[j].C, kStageChunks) * rec_bytes_of(fmt) +
+                                     pad_up((int64_t)h[j].M * (h[j].C + 1) * 4, 16));
   }
   b.table = nullptr;
   b.njobs = (int)njobs;

@@ -825,7 +825,7 @@ constexpr bool kPairChunks = false;
 // Two consecutive chunks (same row tile) on the unshifted-plane token-column
 // path: MMA s contracts plane s of chunk A (K half 0) and chunk B (K half 1);
 // the records' word s of lane t holds exactly that plane's 4 activations.
-template <int MT>
+template <int MT, bool kNoCsum = false>
 __device__ __forceinline__ void process_chunk_pair(const uint4 wa, const uint4 wb,
                                                    const uint8_t *__restrict__ recA,
                                                    const uint8_t *__restrict__ recB, int M,
@@ -856,6 +856,7 @@ __device__ __forceinline__ void process_chunk_pair(const uint4 wa, const uint4 w
               rd & 0xC0C0C0C0u, ba.w, bb.w);
   }
   // the two chunks' activation sums of this lane's token columns (2t, 2t + 1)
+  if constexpr (!kNoCsum)
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int tok = 2 * t + q;
@@ -869,7 +870,9 @@ __device__ __forceinline__ void process_chunk_pair(const uint4 wa, const uint4 w
 #endif
 
 // One 16-byte chunk of this lane's row against MT activation records.
-template <int FMT, int MT>
+// kNoCsum: the caller takes the activation sums from a prefix table instead
+// (records-table mode: set_csum_from_prefix at the flush).
+template <int FMT, int MT, bool kNoCsum = false>
 __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn,
                                               const uint8_t *__restrict__ rec0, int M,
                                               Acc<FMT, MT> &acc, int par = 0) {
@@ -932,7 +935,8 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
         }
       }
     }
-    if constexpr (A::kPlaneCols) {
+    if constexpr (kNoCsum) {
+    } else if constexpr (A::kPlaneCols) {
       const int tok = t >> 1;
       if (tok == 0 || tok < M)
         acc.csum[0] += *reinterpret_cast<const int32_t *>(rec0 + tok * kTokStride + F::kActWords * 4);
@@ -1024,10 +1028,40 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
       }
     }
   }
+  if constexpr (!kNoCsum)
 #pragma unroll
   for (int m = 0; m < MT; ++m)
     if (m == 0 || m < M)
       acc.csum[m] += *reinterpret_cast<const int32_t *>(rec0 + m * kTokStride + F::kActWords * 4);
+}
+
+// Records-table mode: the activation sums of chunks [c0, c1) of the CTA's
+// K-window for the tokens whose sums this lane's accumulator holds, from the
+// per-token prefix table P[tok][c] (stride C + 1) built at the table fill --
+// instead of one or two shared-memory loads and adds per chunk in the loop.
+template <int FMT, int MT>
+__device__ __forceinline__ void set_csum_from_prefix(Acc<FMT, MT> &acc, const int32_t *P,
+                                                     int stride, int c0, int c1, int M) {
+  const int t = threadIdx.x & 3;
+#ifdef TB_I2S_MMA
+  if constexpr (FMT == TB_I2S && kI2sMma<MT>) {
+    using A = Acc<TB_I2S, MT>;
+    if constexpr (A::kPlaneCols) {
+      const int tok = t >> 1;
+      acc.csum[0] = (tok == 0 || tok < M) ? P[tok * stride + c1] - P[tok * stride + c0] : 0;
+    } else {
+#pragma unroll
+      for (int q = 0; q < A::kCs; ++q) {
+        const int tok = 8 * (q >> 1) + 2 * t + (q & 1);
+        acc.csum[q] = tok < M ? P[tok * stride + c1] - P[tok * stride + c0] : 0;
+      }
+    }
+    return;
+  }
+#endif
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+    acc.csum[m] = (m == 0 || m < M) ? P[m * stride + c1] - P[m * stride + c0] : 0;
 }
 
 

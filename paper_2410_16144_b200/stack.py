@@ -130,8 +130,8 @@ _MAX_JOBS, _MAX_SEGS = 20, 8
 
 
 def window_chunks(fmt: str, tokens: int) -> int:
-    rec = 112 if fmt == "tl2" else 80
-    return (_TABLE_BYTES // (tokens * rec)) // 4 * 4
+    rec = (112 if fmt == "tl2" else 80) + 4  # + the chunk's entry of the prefix-sum table
+    return ((_TABLE_BYTES - 4 * tokens - 16) // (tokens * rec)) // 4 * 4
 
 
 class _WindowedView:
