@@ -764,7 +764,8 @@ def run_stack_cfg(torch, tb, args, name, fmt, tokens, passes=10):
     ms /= passes
     launches = L if tokens == 1 else 2 * L
     kern = (f"tgemv_kernel<{fmt.upper()},1,fused> per layer" if tokens == 1 else
-            f"glue_kernel + tgemv_kernel<{fmt.upper()},{tokens}> per layer")
+            f"glue_kernel (quantise, previous finalize) + tgemv_kernel<{fmt.upper()},{tokens},records table> "
+            "per layer, pipelined through per-layer counters")
     out = {"workload": f"{name}: {L} layers, hidden {h}, {fmt.upper()}, M={tokens}",
            "value": round(tokens * 1000.0 / ms, 2), "unit": "tokens/s",
            "ms_per_token_pass": round(ms, 4), "algo_bytes_per_pass": int(st.algo_bytes),
@@ -772,6 +773,10 @@ def run_stack_cfg(torch, tb, args, name, fmt, tokens, passes=10):
                                 measured_traffic(f"{name}_{fmt}_m{tokens}"),
                                 f"graph of {passes} token passes / {L} layers"),
            "launches_per_pass": launches + 1, "build_s": round(build_s, 1)}
+    if tokens > 1:
+        from paper_2410_16144_b200 import _lib as L
+        out["pipelined_layers"] = bool(getattr(st, "piped", False))
+        out["sync_timeouts"] = int(L.load().tb_sync_timeouts())  # bounded waits that expired: 0
     if tokens == 1 and not args.no_e2e:
         out["e2e"] = e2e_stack(torch, tb, st, 20)
     if not args.no_cpu_baseline:
