@@ -774,9 +774,9 @@ def run_stack_cfg(torch, tb, args, name, fmt, tokens, passes=10):
                                 f"graph of {passes} token passes / {L} layers"),
            "launches_per_pass": launches + 1, "build_s": round(build_s, 1)}
     if tokens > 1:
-        from paper_2410_16144_b200 import _lib as L
+        from paper_2410_16144_b200 import _lib as tb_lib
         out["pipelined_layers"] = bool(getattr(st, "piped", False))
-        out["sync_timeouts"] = int(L.load().tb_sync_timeouts())  # bounded waits that expired: 0
+        out["sync_timeouts"] = int(tb_lib.load().tb_sync_timeouts())  # bounded waits that expired: 0
     if tokens == 1 and not args.no_e2e:
         out["e2e"] = e2e_stack(torch, tb, st, 20)
     if not args.no_cpu_baseline:
