@@ -139,6 +139,23 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
+// Tiled TL2 sign plane (one 32-bit word per row and 96-weight chunk): the
+// bit 4 of triple t = 8 i + 2 b + h (index word i, byte b, nibble h of the
+// chunk's 16 index bytes) sits at bit 8 b + 2 i + h -- byte b of the word
+// holds the bits of byte lane b of all eight (word, nibble) groups, so the
+// decode puts a group's four bits at bit 4 of its four byte lanes with ONE
+// shift and one and-or (it was a mask, a multiply and an and-or per group).
+// The map swaps i and b: it is its own inverse.
+__host__ __device__ __forceinline__ int tl2_sign_pos(int t) {
+  return 8 * ((t >> 1) & 3) + 2 * (t >> 3) + (t & 1);
+}
+__host__ __device__ __forceinline__ uint32_t tl2_sign_perm(uint32_t bits) {
+  uint32_t out = 0;
+#pragma unroll
+  for (int t = 0; t < 32; ++t) out |= ((bits >> t) & 1u) << tl2_sign_pos(t);
+  return out;
+}
+
 __device__ __forceinline__ uint32_t lop3_sel(uint32_t p, uint32_t q, uint32_t m) {
   // (p & ~m) | (q & m)
   return (p & ~m) | (q & m);

@@ -41,7 +41,7 @@ __global__ void gemv_lut_kernel(const uint8_t *__restrict__ tiled,
           if (idx <= 8) acc += lut[g * 9 + idx];
         } else {
           // tiled TL2 holds v = 13 + signed index, bit 4 in the sign plane (pack.cu)
-          const int v = (int)idx | (int)(((sg >> (2 * b + h)) & 1u) << 4);
+          const int v = (int)idx | (int)(((sg >> tl2_sign_pos(2 * b + h)) & 1u) << 4);
           const int d = v - 13;
           const int32_t e = lut[g * 14 + (d < 0 ? -d : d)];
           acc += d < 0 ? -e : e;

@@ -984,12 +984,14 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
       // TL2 (packing.py:63-74): the tiled layout holds v = 13 + signed index =
       // the base-3 number 9 c0 + 3 c1 + c2 of the triple's codes (c = w + 1),
       // bits 0-3 in the index plane, bit 4 in the sign plane (pack.cu repack).
-      const uint32_t S = sgn >> (8 * i);
       const uint32_t lo = W & 0x0F0F0F0Fu, hi = (W >> 4) & 0x0F0F0F0Fu;
-      // bit 4 of every byte: even plane bits -> low-nibble triples, odd -> high
-      // (the multiplies place bit 2b / 2b + 1 at bit 8b + 4, carry-free there)
-      const uint32_t vlo = lo | (((S & 0x55u) * 0x00410410u) & 0x10101010u);
-      const uint32_t vhi = hi | (((S & 0xAAu) * 0x00208208u) & 0x10101010u);
+      // bit 4 of every byte: byte lane b of the sign word holds, at bit 2i + h,
+      // the bit of (word i, nibble h, byte b) (tl2_sign_pos, common.cuh): one
+      // shift puts a group's four bits at bit 4 of the four lanes
+      const uint32_t slo = 2 * i < 4 ? sgn << (4 - 2 * i) : sgn >> (2 * i - 4);
+      const uint32_t shi = 2 * i + 1 < 4 ? sgn << (3 - 2 * i) : sgn >> (2 * i - 3);
+      const uint32_t vlo = (slo & 0x10101010u) | lo;
+      const uint32_t vhi = (shi & 0x10101010u) | hi;
       uint32_t code[6];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {

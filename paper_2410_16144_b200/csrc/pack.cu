@@ -257,7 +257,7 @@ __global__ void repack_kernel(int fmt, const uint8_t *ref, const uint8_t *ref_si
       }
       memcpy(&sv, sb, 4);
       tl2_to_v(buf, sv);
-      reinterpret_cast<uint32_t *>(tiled_sign)[i] = sv;
+      reinterpret_cast<uint32_t *>(tiled_sign)[i] = tl2_sign_perm(sv);  // common.cuh
     }
     uint4 v;
     memcpy(&v, buf, 16);
@@ -280,7 +280,7 @@ __global__ void unrepack_kernel(int fmt, const uint8_t *tiled, const uint8_t *ti
       if (fmt == TB_TL2) {  // the chunk's triples back to (sign, index)
         uint8_t idx16[16];
         memcpy(idx16, tiled + q * 16, 16);
-        uint32_t bits = reinterpret_cast<const uint32_t *>(tiled_sign)[q];
+        uint32_t bits = tl2_sign_perm(reinterpret_cast<const uint32_t *>(tiled_sign)[q]);
         v_to_tl2(idx16, bits);
         ref[i] = idx16[b];
       } else {
@@ -294,7 +294,7 @@ __global__ void unrepack_kernel(int fmt, const uint8_t *tiled, const uint8_t *ti
       const int64_t q = (t * C + c) * kRowTile + rin;
       uint8_t idx16[16];
       memcpy(idx16, tiled + q * 16, 16);
-      uint32_t bits = reinterpret_cast<const uint32_t *>(tiled_sign)[q];
+      uint32_t bits = tl2_sign_perm(reinterpret_cast<const uint32_t *>(tiled_sign)[q]);
       v_to_tl2(idx16, bits);
       ref_sign[k] = (uint8_t)(bits >> (8 * b));
     }

@@ -55,13 +55,30 @@ def test_tl1_word_decode_all_nibble_pairs():
                 assert bytes_of(r)[b] == nib[b] % 3
 
 
-def test_tl2_sign_masks_all_bytes():
-    for S in range(256):
-        mlo = prmt_sign_replicate(U((S & 0x55) * 0x02082080 & 0xFFFFFFFF))
-        mhi = prmt_sign_replicate(U((S & 0xAA) * 0x01041040 & 0xFFFFFFFF))
-        for b in range(4):
-            assert bytes_of(mlo)[b] == (0xFF if (S >> (2 * b)) & 1 else 0)
-            assert bytes_of(mhi)[b] == (0xFF if (S >> (2 * b + 1)) & 1 else 0)
+def tl2_sign_pos(t):
+    """csrc/common.cuh: bit of triple t = 8i + 2b + h in the tiled sign word."""
+    return 8 * ((t >> 1) & 3) + 2 * (t >> 3) + (t & 1)
+
+
+def test_tl2_sign_word_layout():
+    """The tiled TL2 sign word: a self-inverse bit permutation, and one shift
+    plus one mask puts the four bits of group (word i, nibble h) at bit 4 of
+    the four byte lanes (gemv_records.cuh process_chunk)."""
+    pos = [tl2_sign_pos(t) for t in range(32)]
+    assert sorted(pos) == list(range(32))
+    assert all(tl2_sign_pos(pos[t]) == t for t in range(32))
+    rng = np.random.default_rng(0)
+    for S in [0, 0xFFFFFFFF, 1, 0x80000000] + [int(v) for v in rng.integers(0, 2 ** 32, 200)]:
+        tiled = 0
+        for t in range(32):
+            tiled |= ((S >> t) & 1) << pos[t]
+        for i in range(4):
+            for h in range(2):
+                j = 2 * i + h
+                sh = (tiled << (4 - j)) if j < 4 else (tiled >> (j - 4))
+                m = int(U(sh & 0xFFFFFFFF) & U(0x10101010))
+                for b in range(4):
+                    assert (m >> (8 * b + 4)) & 1 == (S >> (8 * i + 2 * b + h)) & 1
 
 
 def test_tl2_triple_decode_all_codes():
