@@ -139,21 +139,50 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
-// Tiled TL2 sign plane (one 32-bit word per row and 96-weight chunk): the
-// bit 4 of triple t = 8 i + 2 b + h (index word i, byte b, nibble h of the
-// chunk's 16 index bytes) sits at bit 8 b + 2 i + h -- byte b of the word
-// holds the bits of byte lane b of all eight (word, nibble) groups, so the
-// decode puts a group's four bits at bit 4 of its four byte lanes with ONE
-// shift and one and-or (it was a mask, a multiply and an and-or per group).
-// The map swaps i and b: it is its own inverse.
-__host__ __device__ __forceinline__ int tl2_sign_pos(int t) {
-  return 8 * ((t >> 1) & 3) + 2 * (t >> 3) + (t & 1);
+// Tiled TL2 (one row of a 96-weight chunk = 32 triples = 160 bits: four
+// "main" words X0..X3 and the "sign" word X4).  Triple t = 8 i + 2 b + h
+// (index byte 4 i + b of the chunk, nibble h) is lane b of group j = 2 i + h;
+// its 5-bit value v (pack.cu tl2_to_v) is laid out so the decode gets a
+// group's four values in the byte lanes of one register with masks and a
+// shift or two -- no nibble split, no per-group sign merge:
+//   groups 0..4: bits 0-4 of byte lane b of X_j             (one mask)
+//   group 5: v bits 0-2 = bits 5-7 of X0, bits 3-4 = bits 5-6 of X1
+//   group 6: v bits 0-2 = bits 5-7 of X2, bits 3-4 = bits 5-6 of X3
+//   group 7: v bits 0-2 = bits 5-7 of X4, bit 3 = bit 7 of X1, bit 4 = bit 7 of X3
+// (19 logic ops per 32 triples; the nibble + sign-plane form took 27.)
+// tl2_bit(t, k): (word, bit) of bit k of triple t's value.
+struct Tl2Bit {
+  int word, bit;
+};
+__host__ __device__ __forceinline__ Tl2Bit tl2_bit(int t, int k) {
+  const int i = t >> 3, b = (t >> 1) & 3, h = t & 1, j = 2 * i + h;
+  if (j < 5) return Tl2Bit{j, 8 * b + k};
+  if (j == 5) return k < 3 ? Tl2Bit{0, 8 * b + 5 + k} : Tl2Bit{1, 8 * b + 2 + k};
+  if (j == 6) return k < 3 ? Tl2Bit{2, 8 * b + 5 + k} : Tl2Bit{3, 8 * b + 2 + k};
+  return k < 3 ? Tl2Bit{4, 8 * b + 5 + k} : (k == 3 ? Tl2Bit{1, 8 * b + 7} : Tl2Bit{3, 8 * b + 7});
 }
-__host__ __device__ __forceinline__ uint32_t tl2_sign_perm(uint32_t bits) {
-  uint32_t out = 0;
+// value of triple t from a row's five words
+__host__ __device__ __forceinline__ uint32_t tl2_tile_value(const uint32_t X[5], int t) {
+  uint32_t v = 0;
 #pragma unroll
-  for (int t = 0; t < 32; ++t) out |= ((bits >> t) & 1u) << tl2_sign_pos(t);
-  return out;
+  for (int k = 0; k < 5; ++k) {
+    const Tl2Bit p = tl2_bit(t, k);
+    v |= ((X[p.word] >> p.bit) & 1u) << k;
+  }
+  return v;
+}
+// the eight groups' byte-lane registers (group j: lane b = value of triple 8 (j/2) + 2 b + j%2)
+__device__ __forceinline__ void tl2_tile_groups(const uint32_t X0, const uint32_t X1,
+                                                const uint32_t X2, const uint32_t X3,
+                                                const uint32_t X4, uint32_t v[8]) {
+  v[0] = X0 & 0x1F1F1F1Fu;
+  v[1] = X1 & 0x1F1F1F1Fu;
+  v[2] = X2 & 0x1F1F1F1Fu;
+  v[3] = X3 & 0x1F1F1F1Fu;
+  v[4] = X4 & 0x1F1F1F1Fu;
+  v[5] = ((X0 >> 5) & 0x07070707u) | ((X1 >> 2) & 0x18181818u);
+  v[6] = ((X2 >> 5) & 0x07070707u) | ((X3 >> 2) & 0x18181818u);
+  v[7] = ((X4 >> 5) & 0x07070707u) | ((X1 >> 4) & 0x08080808u) | ((X3 >> 3) & 0x10101010u);
 }
 
 __device__ __forceinline__ uint32_t lop3_sel(uint32_t p, uint32_t q, uint32_t m) {

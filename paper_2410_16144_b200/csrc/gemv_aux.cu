@@ -25,9 +25,12 @@ __global__ void gemv_lut_kernel(const uint8_t *__restrict__ tiled,
   const int ce = min(C, cb + chunks_per_warp);
   for (int c = cb; c < ce; ++c) {
     const uint8_t *src = tiled + ((t * C + c) * kRowTile + lane) * 16;
-    uint32_t sg = 0;
-    if (FMT == TB_TL2)
-      sg = *reinterpret_cast<const uint32_t *>(tiled_sign + ((t * C + c) * kRowTile + lane) * 4);
+    uint32_t X[5] = {0, 0, 0, 0, 0};
+    if (FMT == TB_TL2) {  // the row's five tile words (common.cuh tl2_bit)
+      const uint4 m = *reinterpret_cast<const uint4 *>(src);
+      X[0] = m.x, X[1] = m.y, X[2] = m.z, X[3] = m.w;
+      X[4] = *reinterpret_cast<const uint32_t *>(tiled_sign + ((t * C + c) * kRowTile + lane) * 4);
+    }
     for (int b = 0; b < 16; ++b) {
       const uint32_t byte = src[b];
 #pragma unroll
@@ -40,8 +43,8 @@ __global__ void gemv_lut_kernel(const uint8_t *__restrict__ tiled,
         if (FMT == TB_TL1) {
           if (idx <= 8) acc += lut[g * 9 + idx];
         } else {
-          // tiled TL2 holds v = 13 + signed index, bit 4 in the sign plane (pack.cu)
-          const int v = (int)idx | (int)(((sg >> tl2_sign_pos(2 * b + h)) & 1u) << 4);
+          // tiled TL2 holds v = 13 + signed index (pack.cu)
+          const int v = (int)tl2_tile_value(X, 2 * b + h);
           const int d = v - 13;
           const int32_t e = lut[g * 14 + (d < 0 ? -d : d)];
           acc += d < 0 ? -e : e;

@@ -955,9 +955,13 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
   const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
   uint4 tq[3];  // TL2, one token: activation words of the current word pair
   (void)tq;
+  uint32_t tv[8];  // TL2: the eight groups' byte-lane values (common.cuh tl2_tile_groups)
+  (void)tv;
+  if constexpr (FMT == TB_TL2) tl2_tile_groups(w4.x, w4.y, w4.z, w4.w, sgn, tv);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t W = w[i];
+    (void)W;
     if constexpr (FMT == TB_I2S) {
 #ifdef TB_I2S_MMA
       if constexpr (!kI2sMma<MT>) {
@@ -983,15 +987,9 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
     } else {
       // TL2 (packing.py:63-74): the tiled layout holds v = 13 + signed index =
       // the base-3 number 9 c0 + 3 c1 + c2 of the triple's codes (c = w + 1),
-      // bits 0-3 in the index plane, bit 4 in the sign plane (pack.cu repack).
-      const uint32_t lo = W & 0x0F0F0F0Fu, hi = (W >> 4) & 0x0F0F0F0Fu;
-      // bit 4 of every byte: byte lane b of the sign word holds, at bit 2i + h,
-      // the bit of (word i, nibble h, byte b) (tl2_sign_pos, common.cuh): one
-      // shift puts a group's four bits at bit 4 of the four lanes
-      const uint32_t slo = 2 * i < 4 ? sgn << (4 - 2 * i) : sgn >> (2 * i - 4);
-      const uint32_t shi = 2 * i + 1 < 4 ? sgn << (3 - 2 * i) : sgn >> (2 * i - 3);
-      const uint32_t vlo = (slo & 0x10101010u) | lo;
-      const uint32_t vhi = (shi & 0x10101010u) | hi;
+      // its bits placed for byte-lane extraction (common.cuh tl2_tile_groups).
+      // Groups 2i (low nibbles of reference word i) and 2i + 1 (high nibbles):
+      const uint32_t vlo = tv[2 * i], vhi = tv[2 * i + 1];
       uint32_t code[6];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {

@@ -198,33 +198,40 @@ __device__ __forceinline__ uint8_t codes_to_tl1(uint32_t c) {
 
 // TL2 triples are re-encoded on the way to the tiled layout: (sign s, index
 // idx) -> v = 13 + (s ? -idx : idx) = 9 c0 + 3 c1 + c2 (c = w + 1, the
-// base-3 number of the triple, packing.py:63-74), low 4 bits in the index
-// plane and bit 4 in the sign plane: the same 5 bits per triple, a
-// bijection (zero is v = 13), and the decode needs no sign masks (the digits
-// come straight from v).  tb_unrepack inverts it.
-__device__ __forceinline__ void tl2_to_v(uint8_t *idx16, uint32_t &sgn32) {
-  uint32_t out = 0;
+// base-3 number of the triple, packing.py:63-74): the same 5 bits per triple,
+// a bijection (zero is v = 13), so the decode takes the digits straight from
+// v; the bits are placed for a cheap byte-lane extraction (common.cuh
+// tl2_bit).  tb_unrepack inverts it.
+// idx16 / sgn32: the chunk row's 16 reference index bytes and 32 sign bits
+// -> the five tile words (common.cuh tl2_bit)
+__device__ __forceinline__ void tl2_to_tile(const uint8_t *idx16, uint32_t sgn32, uint32_t X[5]) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) X[k] = 0;
 #pragma unroll
   for (int t = 0; t < 32; ++t) {
     const uint32_t nib = (idx16[t >> 1] >> (4 * (t & 1))) & 15u;
     const uint32_t s = (sgn32 >> t) & 1u;
     const uint32_t v = s ? 13u - nib : 13u + nib;
-    idx16[t >> 1] = (uint8_t)((idx16[t >> 1] & (0xF0u >> (4 * (t & 1)))) | ((v & 15u) << (4 * (t & 1))));
-    out |= (v >> 4) << t;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const Tl2Bit p = tl2_bit(t, k);
+      X[p.word] |= ((v >> k) & 1u) << p.bit;
+    }
   }
-  sgn32 = out;
 }
-__device__ __forceinline__ void v_to_tl2(uint8_t *idx16, uint32_t &bits32) {
+__device__ __forceinline__ void tile_to_tl2(const uint32_t X[5], uint8_t *idx16, uint32_t &sgn32) {
   uint32_t out = 0;
 #pragma unroll
+  for (int b = 0; b < 16; ++b) idx16[b] = 0;
+#pragma unroll
   for (int t = 0; t < 32; ++t) {
-    const uint32_t v = ((idx16[t >> 1] >> (4 * (t & 1))) & 15u) | (((bits32 >> t) & 1u) << 4);
+    const uint32_t v = tl2_tile_value(X, t);
     const uint32_t s = v < 13u ? 1u : 0u;
     const uint32_t nib = s ? 13u - v : v - 13u;
-    idx16[t >> 1] = (uint8_t)((idx16[t >> 1] & (0xF0u >> (4 * (t & 1)))) | (nib << (4 * (t & 1))));
+    idx16[t >> 1] |= (uint8_t)(nib << (4 * (t & 1)));
     out |= s << t;
   }
-  bits32 = out;
+  sgn32 = out;
 }
 
 __global__ void repack_kernel(int fmt, const uint8_t *ref, const uint8_t *ref_sign, int64_t rows,
@@ -256,8 +263,11 @@ __global__ void repack_kernel(int fmt, const uint8_t *ref, const uint8_t *ref_si
         sb[b] = (r < rows && j < sbpr) ? ref_sign[r * sbpr + j] : 0;
       }
       memcpy(&sv, sb, 4);
-      tl2_to_v(buf, sv);
-      reinterpret_cast<uint32_t *>(tiled_sign)[i] = tl2_sign_perm(sv);  // common.cuh
+      uint32_t X[5];
+      tl2_to_tile(buf, sv, X);
+      reinterpret_cast<uint32_t *>(tiled_sign)[i] = X[4];
+      reinterpret_cast<uint4 *>(tiled)[i] = make_uint4(X[0], X[1], X[2], X[3]);
+      continue;
     }
     uint4 v;
     memcpy(&v, buf, 16);
@@ -279,9 +289,10 @@ __global__ void unrepack_kernel(int fmt, const uint8_t *tiled, const uint8_t *ti
       const int64_t q = (t * C + c) * kRowTile + rin;
       if (fmt == TB_TL2) {  // the chunk's triples back to (sign, index)
         uint8_t idx16[16];
-        memcpy(idx16, tiled + q * 16, 16);
-        uint32_t bits = tl2_sign_perm(reinterpret_cast<const uint32_t *>(tiled_sign)[q]);
-        v_to_tl2(idx16, bits);
+        uint32_t X[5], bits;
+        memcpy(X, tiled + q * 16, 16);
+        X[4] = reinterpret_cast<const uint32_t *>(tiled_sign)[q];
+        tile_to_tl2(X, idx16, bits);
         ref[i] = idx16[b];
       } else {
         const uint8_t v = tiled[q * 16 + b];
@@ -293,9 +304,10 @@ __global__ void unrepack_kernel(int fmt, const uint8_t *tiled, const uint8_t *ti
       int64_t t = r / kRowTile, rin = r % kRowTile, c = j / 4, b = j % 4;
       const int64_t q = (t * C + c) * kRowTile + rin;
       uint8_t idx16[16];
-      memcpy(idx16, tiled + q * 16, 16);
-      uint32_t bits = tl2_sign_perm(reinterpret_cast<const uint32_t *>(tiled_sign)[q]);
-      v_to_tl2(idx16, bits);
+      uint32_t X[5], bits;
+      memcpy(X, tiled + q * 16, 16);
+      X[4] = reinterpret_cast<const uint32_t *>(tiled_sign)[q];
+      tile_to_tl2(X, idx16, bits);
       ref_sign[k] = (uint8_t)(bits >> (8 * b));
     }
   }

@@ -55,30 +55,44 @@ def test_tl1_word_decode_all_nibble_pairs():
                 assert bytes_of(r)[b] == nib[b] % 3
 
 
-def tl2_sign_pos(t):
-    """csrc/common.cuh: bit of triple t = 8i + 2b + h in the tiled sign word."""
-    return 8 * ((t >> 1) & 3) + 2 * (t >> 3) + (t & 1)
+def tl2_bit(t, k):
+    """csrc/common.cuh tl2_bit: (word, bit) of bit k of triple t's 5-bit value
+    in a row chunk's five tile words (X0..X3 main, X4 sign plane)."""
+    i, b, h = t >> 3, (t >> 1) & 3, t & 1
+    j = 2 * i + h
+    if j < 5:
+        return j, 8 * b + k
+    if j == 5:
+        return (0, 8 * b + 5 + k) if k < 3 else (1, 8 * b + 2 + k)
+    if j == 6:
+        return (2, 8 * b + 5 + k) if k < 3 else (3, 8 * b + 2 + k)
+    if k < 3:
+        return 4, 8 * b + 5 + k
+    return (1, 8 * b + 7) if k == 3 else (3, 8 * b + 7)
 
 
-def test_tl2_sign_word_layout():
-    """The tiled TL2 sign word: a self-inverse bit permutation, and one shift
-    plus one mask puts the four bits of group (word i, nibble h) at bit 4 of
-    the four byte lanes (gemv_records.cuh process_chunk)."""
-    pos = [tl2_sign_pos(t) for t in range(32)]
-    assert sorted(pos) == list(range(32))
-    assert all(tl2_sign_pos(pos[t]) == t for t in range(32))
+def test_tl2_tile_layout():
+    """The tiled TL2 row chunk: 32 triples x 5 bits fill the five words exactly
+    once, and the decode's masks and shifts (common.cuh tl2_tile_groups) put
+    group j's four values in the byte lanes of one register."""
+    slots = [tl2_bit(t, k) for t in range(32) for k in range(5)]
+    assert sorted(slots) == [(w, b) for w in range(5) for b in range(32)]
     rng = np.random.default_rng(0)
-    for S in [0, 0xFFFFFFFF, 1, 0x80000000] + [int(v) for v in rng.integers(0, 2 ** 32, 200)]:
-        tiled = 0
+    for _ in range(200):
+        v = rng.integers(0, 27, 32)
+        X = [0] * 5
         for t in range(32):
-            tiled |= ((S >> t) & 1) << pos[t]
-        for i in range(4):
-            for h in range(2):
-                j = 2 * i + h
-                sh = (tiled << (4 - j)) if j < 4 else (tiled >> (j - 4))
-                m = int(U(sh & 0xFFFFFFFF) & U(0x10101010))
-                for b in range(4):
-                    assert (m >> (8 * b + 4)) & 1 == (S >> (8 * i + 2 * b + h)) & 1
+            for k in range(5):
+                w, bit = tl2_bit(t, k)
+                X[w] |= ((int(v[t]) >> k) & 1) << bit
+        g = [X[j] & 0x1F1F1F1F for j in range(5)]
+        g.append(((X[0] >> 5) & 0x07070707) | ((X[1] >> 2) & 0x18181818))
+        g.append(((X[2] >> 5) & 0x07070707) | ((X[3] >> 2) & 0x18181818))
+        g.append(((X[4] >> 5) & 0x07070707) | ((X[1] >> 4) & 0x08080808) | ((X[3] >> 3) & 0x10101010))
+        for j in range(8):
+            i, h = j >> 1, j & 1
+            for b in range(4):
+                assert (g[j] >> (8 * b)) & 0xFF == v[8 * i + 2 * b + h], (j, b)
 
 
 def test_tl2_triple_decode_all_codes():
