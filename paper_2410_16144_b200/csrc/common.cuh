@@ -161,7 +161,8 @@ __host__ __device__ __forceinline__ Tl2Bit tl2_bit(int t, int k) {
   if (j == 6) return k < 3 ? Tl2Bit{2, 8 * b + 5 + k} : Tl2Bit{3, 8 * b + 2 + k};
   return k < 3 ? Tl2Bit{4, 8 * b + 5 + k} : (k == 3 ? Tl2Bit{1, 8 * b + 7} : Tl2Bit{3, 8 * b + 7});
 }
-// value of triple t from a row's five words
+// value v = 9 c0 + 3 c1 + c2 of triple t from a row's five words (the tile
+// stores v + 1: the decode's two divisions then need no bias add)
 __host__ __device__ __forceinline__ uint32_t tl2_tile_value(const uint32_t X[5], int t) {
   uint32_t v = 0;
 #pragma unroll
@@ -169,9 +170,9 @@ __host__ __device__ __forceinline__ uint32_t tl2_tile_value(const uint32_t X[5],
     const Tl2Bit p = tl2_bit(t, k);
     v |= ((X[p.word] >> p.bit) & 1u) << k;
   }
-  return v;
+  return v - 1u;
 }
-// the eight groups' byte-lane registers (group j: lane b = value of triple 8 (j/2) + 2 b + j%2)
+// the eight groups' byte-lane registers (group j: lane b = v + 1 of triple 8 (j/2) + 2 b + j%2)
 __device__ __forceinline__ void tl2_tile_groups(const uint32_t X0, const uint32_t X1,
                                                 const uint32_t X2, const uint32_t X3,
                                                 const uint32_t X4, uint32_t v[8]) {

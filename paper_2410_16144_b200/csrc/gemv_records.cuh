@@ -24,7 +24,8 @@ struct Fmt {
 // activation records
 //   I2_S / TL1 (64 acts / chunk): word 4i+s = (a[16i+s], a[16i+4+s], a[16i+8+s], a[16i+12+s])
 //   TL2        (96 acts / chunk): word 6i+s = (a[24i+s], a[24i+6+s], a[24i+12+s], a[24i+18+s])
-//   word kActWords = sum of the chunk's activations
+//   word kActWords = sum of the chunk's activations (TL2: + the sum over the
+//   triples' third members, see write_group)
 // One thread per (token, chunk, group i); the 4 group threads are adjacent lanes.
 // ---------------------------------------------------------------------------
 // Distributed shared memory (thread-block clusters): the fused step's CTAs
@@ -70,13 +71,8 @@ template <int FMT>
 __device__ __forceinline__ void write_group(uint8_t *rec_chunk, int i, const uint32_t (&r)[Fmt<FMT>::kGroup],
                                             int32_t gsum, bool on, int Q = 1) {
   using F = Fmt<FMT>;
-  // chunk sum over the 4 adjacent group lanes (all 32 lanes shuffle)
-  gsum += __shfl_xor_sync(0xffffffffu, gsum, 1);
-  gsum += __shfl_xor_sync(0xffffffffu, gsum, 2);
-  if (!on) return;
-  uint32_t *dst = reinterpret_cast<uint32_t *>(rec_chunk) + i * F::kGroup;
+  uint32_t wv[FMT == TB_TL2 ? 6 : 1];
   if constexpr (FMT == TB_TL2) {
-    uint32_t wv[6];
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       uint32_t word = 0;
@@ -87,6 +83,18 @@ __device__ __forceinline__ void write_group(uint8_t *rec_chunk, int i, const uin
       }
       wv[s] = word;
     }
+    // The TL2 decode keeps a triple's third digit as c2 + 1 (it saves the
+    // subtraction): the chunk "sum" the contraction subtracts is therefore
+    // sum(a) + sum(a over the third members) -- words 2 and 5 of the group.
+    gsum = __dp4a((int)wv[2], 0x01010101, gsum);
+    gsum = __dp4a((int)wv[5], 0x01010101, gsum);
+  }
+  // chunk sum over the 4 adjacent group lanes (all 32 lanes shuffle)
+  gsum += __shfl_xor_sync(0xffffffffu, gsum, 1);
+  gsum += __shfl_xor_sync(0xffffffffu, gsum, 2);
+  if (!on) return;
+  uint32_t *dst = reinterpret_cast<uint32_t *>(rec_chunk) + i * F::kGroup;
+  if constexpr (FMT == TB_TL2) {
     if (Q == 1) {
 #pragma unroll
       for (int s = 0; s < 6; ++s) dst[s] = wv[s];
@@ -994,12 +1002,18 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint32_t d = h ? vhi : vlo;
-        const uint32_t c0 = ((d * 7u + 0x07070707u) >> 6) & 0x03030303u;  // d / 9
-        const uint32_t r = d - 9u * c0;                                      // d % 9
-        const uint32_t c1 = __umulhi(r, 11u << 27) & 0x03030303u;           // r / 3
+        // d = v + 1 (the tile stores the biased value, so the divisions need no
+        // bias add): (7 d) >> 6 = v / 9; r = v % 9 + 1;
+        // (10 r) >> 5 = (v % 9) / 3; the third digit stays biased, c2 + 1 --
+        // the records' chunk sums carry the matching term (write_group)
+        // (multiply + shift, not multiply-high: IMAD.HI issues slower on B200 --
+        // both divisions by mul.hi 16.4 us per cfg2 layer, both this way 15.6)
+        const uint32_t c0 = ((d * 7u) >> 6) & 0x03030303u;
+        const uint32_t r = d - 9u * c0;
+        const uint32_t c1 = ((r * 10u) >> 5) & 0x03030303u;
         code[3 * h + 0] = c0;
         code[3 * h + 1] = c1;
-        code[3 * h + 2] = r - 3u * c1;  // r % 3
+        code[3 * h + 2] = r - 3u * c1;
       }
       if constexpr (MT == 1) {
         // one token: the 12 activation words of a word pair in three 16-byte loads

@@ -211,7 +211,7 @@ __device__ __forceinline__ void tl2_to_tile(const uint8_t *idx16, uint32_t sgn32
   for (int t = 0; t < 32; ++t) {
     const uint32_t nib = (idx16[t >> 1] >> (4 * (t & 1))) & 15u;
     const uint32_t s = (sgn32 >> t) & 1u;
-    const uint32_t v = s ? 13u - nib : 13u + nib;
+    const uint32_t v = (s ? 13u - nib : 13u + nib) + 1u;  // stored biased: 1..27 (tl2_tile_value)
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       const Tl2Bit p = tl2_bit(t, k);

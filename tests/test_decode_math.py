@@ -124,3 +124,21 @@ def test_activation_permutation_covers_chunk():
     for width, G in ((64, 4), (96, 6)):
         seen = sorted(i * 4 * G + s + G * j for i in range(4) for s in range(G) for j in range(4))
         assert seen == list(range(width))
+
+
+def test_tl2_biased_digits():
+    """gemv_records.cuh: with d = v + 1 in every byte lane, (7 d) >> 6 = v / 9,
+    r = d - 9 c0 = v % 9 + 1, (10 r) >> 5 = (v % 9) / 3 and r - 3 c1 = v % 3 + 1,
+    as whole-word multiplies (no lane reaches into its neighbour's low bits)."""
+    rng = np.random.default_rng(1)
+    cases = [np.array([v] * 4) for v in range(27)] + [rng.integers(0, 27, 4) for _ in range(500)]
+    for v in cases:
+        d = sum((int(x) + 1) << (8 * b) for b, x in enumerate(v))
+        c0 = (((d * 7) & 0xFFFFFFFF) >> 6) & 0x03030303
+        r = d - 9 * c0
+        c1 = (((r * 10) & 0xFFFFFFFF) >> 5) & 0x03030303
+        c2 = r - 3 * c1
+        for b, x in enumerate(v):
+            x = int(x)
+            assert bytes_of(c0)[b] == x // 9 and bytes_of(c1)[b] == (x % 9) // 3
+            assert bytes_of(c2)[b] == x % 3 + 1
