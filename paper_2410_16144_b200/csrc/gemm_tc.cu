@@ -516,6 +516,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tgemm_kernel(const __grid_con
             __syncwarp();
           }
         }
+        // the staging rows live in the B slots: no warp may start unpacking the
+        // next tile's first stages into them while another still stages its
+        // accumulators there (the epilogue warps finish at different times,
+        // most visibly on the float64 outputs)
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         tc_fence_before();
         mbar_arrive(&tempty);
 #ifdef TB_GEMM_TRACE_EPI
