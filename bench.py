@@ -82,6 +82,16 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def measured_int8_frac(tops):
+    """tops against twice the measured dense bf16 burst rate of
+    MEASURED_PEAKS.json (int8 tensor-core rate = 2 x bf16), or None."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return round(tops / (2.0 * float(json.load(f)["bf16_tflops"])), 4)
+    except Exception:
+        return None
+
+
 def measured_traffic(name):
     """dram bytes read + write per launch of the named kernel capture
     (profiles/r2_traffic.json, from an ncu --set full capture), or None."""
@@ -867,6 +877,7 @@ def run_cfg3(torch, tb, args, copies=2, reps=10):
            "roofline": {"bound": "tensor", "achieved": round(tops_g, 1), "peak": round(peak, 1),
                         "unit": "TOPS", "frac": round(tops_g / peak, 4),
                         "frac_vs_nominal_4500": round(tops_g / 4500.0, 4),
+                        "frac_vs_2x_measured_bf16": measured_int8_frac(tops_g),
                         "kernel": "tgemm_kernel (tcgen05.mma kind::i8, TMEM accumulators)",
                         "peak_kind": "cuBLASLt int8 (torch._int_mm 8192^3) measured in this run",
                         "traffic": None}}
