@@ -608,6 +608,10 @@ constexpr bool kI2sMma = MT >= 2 || TB_MMA_M1;  // M = 1 stays on dp4a (measured
 template <int MT>
 constexpr bool kI2sMma = false;
 #endif
+#ifndef TB_TL2_LIN
+#define TB_TL2_LIN 1  // one-token TL2: third digit by linearity (see process_chunk)
+#endif
+constexpr bool kTl2Lin = TB_TL2_LIN != 0;
 template <int FMT, int MT, bool kMma = (FMT == TB_I2S && kI2sMma<MT>)>
 struct Acc {
   static_assert(FMT != TB_TL1, "TL1 tiles are decoded by the I2_S path");
@@ -636,6 +640,8 @@ struct Acc {
         r += v[m][4 * q] + (v[m][4 * q + 1] >> 2) + (v[m][4 * q + 2] >> 4) + (v[m][4 * q + 3] >> 6);
       return r;
     } else {
+      if constexpr (MT == 1 && kTl2Lin)  // process_chunk's one-token TL2 slots
+        return v[m][0] + v[m][3] + ((v[m][1] + v[m][4]) >> 5) + v[m][2] - 3 * (v[m][5] >> 5) - csum[m];
       int32_t s = -csum[m];
 #pragma unroll
       for (int k = 0; k < kSlots; ++k) s += v[m][k];
@@ -998,6 +1004,37 @@ __device__ __forceinline__ void process_chunk(const uint4 w4, const uint32_t sgn
       // its bits placed for byte-lane extraction (common.cuh tl2_tile_groups).
       // Groups 2i (low nibbles of reference word i) and 2i + 1 (high nibbles):
       const uint32_t vlo = tv[2 * i], vhi = tv[2 * i + 1];
+      if constexpr (MT == 1 && kTl2Lin) {
+        // One token: the second digit stays unshifted (c1s = 32 c1, one mask)
+        // and the third is never formed: with r = 3 c1 + (c2 + 1),
+        //   sum (c2 + 1) a2 = sum r a2 - 3 sum c1 a2,
+        // so the group costs a fourth dp4a (c1s against the a2 word) instead of
+        // a shift and a multiply-subtract: 10 instructions per four triples
+        // instead of 11, the FMA pipe's share unchanged.  Slots: 0/3 c0 a0
+        // (low / high nibble groups), 1/4 c1s a1, 2 r a2, 5 c1s a2;
+        // Acc::total folds them exactly (c1s sums are multiples of 32).
+        if ((i & 1) == 0) {
+          const uint4 *Q = reinterpret_cast<const uint4 *>(rec0 + 24 * i);
+          tq[0] = Q[0];
+          tq[1] = Q[1];
+          tq[2] = Q[2];
+        }
+        const uint32_t a[6] = {(i & 1) ? tq[1].z : tq[0].x, (i & 1) ? tq[1].w : tq[0].y,
+                               (i & 1) ? tq[2].x : tq[0].z, (i & 1) ? tq[2].y : tq[0].w,
+                               (i & 1) ? tq[2].z : tq[1].x, (i & 1) ? tq[2].w : tq[1].y};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t d = h ? vhi : vlo;
+          const uint32_t c0 = ((d * 7u) >> 6) & 0x03030303u;
+          const uint32_t r = d - 9u * c0;
+          const uint32_t c1s = (r * 10u) & 0x60606060u;
+          acc.v[0][3 * h] = dp4a_us(c0, a[3 * h], acc.v[0][3 * h]);
+          acc.v[0][3 * h + 1] = dp4a_us(c1s, a[3 * h + 1], acc.v[0][3 * h + 1]);
+          acc.v[0][2] = dp4a_us(r, a[3 * h + 2], acc.v[0][2]);
+          acc.v[0][5] = dp4a_us(c1s, a[3 * h + 2], acc.v[0][5]);
+        }
+        continue;
+      }
       uint32_t code[6];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
