@@ -142,3 +142,28 @@ def test_tl2_biased_digits():
             x = int(x)
             assert bytes_of(c0)[b] == x // 9 and bytes_of(c1)[b] == (x % 9) // 3
             assert bytes_of(c2)[b] == x % 3 + 1
+
+
+def test_tl2_third_digit_by_linearity():
+    """gemv_records.cuh, one-token TL2: the second digit stays unshifted
+    (c1s = (10 r) & 0x60 per lane = 32 c1) and the third is never formed:
+    sum (c2 + 1) a2 = sum r a2 - 3 sum c1 a2, folded as
+    v0 + v1s / 32 + v2 - 3 v5s / 32 (Acc::total), for whole words of four
+    triples against int8 activations."""
+    rng = np.random.default_rng(2)
+    dp4a = lambda u, a: sum(int(x) * int(y) for x, y in zip(u, a))  # noqa: E731
+    for _ in range(400):
+        v = rng.integers(0, 27, 4)
+        a0, a1, a2 = (rng.integers(-127, 128, 4) for _ in range(3))
+        d = sum((int(x) + 1) << (8 * b) for b, x in enumerate(v))
+        c0 = (((d * 7) & 0xFFFFFFFF) >> 6) & 0x03030303
+        r = d - 9 * c0
+        c1s = ((r * 10) & 0xFFFFFFFF) & 0x60606060
+        assert [b // 32 for b in bytes_of(c1s)] == [(int(x) % 9) // 3 for x in v]
+        s0, s1, s2, s5 = (dp4a(bytes_of(c0), a0), dp4a(bytes_of(c1s), a1),
+                          dp4a(bytes_of(r), a2), dp4a(bytes_of(c1s), a2))
+        assert s1 % 32 == 0 and s5 % 32 == 0
+        got = s0 + (s1 >> 5) + s2 - 3 * (s5 >> 5)
+        want = sum((int(x) // 9) * int(p) + ((int(x) % 9) // 3) * int(q) + (int(x) % 3 + 1) * int(t)
+                   for x, p, q, t in zip(v, a0, a1, a2))
+        assert got == want
