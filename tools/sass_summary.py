@@ -21,7 +21,7 @@ def kernels(obj):
         if m:
             cur = m.group(1)
             continue
-        m = re.match(r"\s+/\*[0-9a-f]{4}\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)", ln)
+        m = re.match(r"\s+/\*[0-9a-f]{4,6}\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)", ln)
         if cur and m:
             op = m.group(1)
             res[cur]["_total"] += 1
